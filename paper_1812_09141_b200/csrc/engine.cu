@@ -1,0 +1,795 @@
+// engine.cu -- the C ABI (include/ssjoin_b200.h) over the sm_100a verification kernels.
+//
+// One ssj_engine = one VerificationEngine (verify.hpp:241-351) bound to one GPU:
+//   * the Collection (collection.hpp:76-94) is re-laid out into a 32-byte-aligned padded
+//     CSR plus {pos8, size} descriptors and uploaded once;
+//   * each chunk (chunk.hpp:20-28) crosses PCIe in pieces on a copy stream while the
+//     compute stream verifies the pieces already resident and a second copy stream returns
+//     their flags (the paper's co-process scheme inside one chunk);
+//   * two chunk slots allow ssj_submit_chunk / ssj_wait_chunk double buffering.
+// No CPU verification path exists here: without a device every entry point fails.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/ssjoin_b200.h"
+#include "verify_kernels.cuh"
+
+using ssjb::KParams;
+using ssjb::PredDev;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, std::string msg) {
+    g_err = std::move(msg);
+    return code;
+}
+
+#define SSJ_CK(x)                                                                       \
+    do {                                                                                \
+        cudaError_t _e = (x);                                                           \
+        if (_e != cudaSuccess)                                                          \
+            return fail(SSJ_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+typedef unsigned __int128 u128;
+
+uint64_t host_ceil_div(u128 a, u128 b) { return (uint64_t)((a + b - 1) / b); }
+
+// Restores the caller's current device on scope exit (torch and other users keep theirs).
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceScope() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+constexpr int kEventsPerSlot = 96;
+constexpr uint64_t kPieceMinSlots = 1ull << 22;  // 4M candidates = 16 MB of C per piece
+constexpr int kMaxPieces = 32;
+
+template <typename T>
+int ensure_device(T** ptr, size_t* cap, size_t need) {
+    if (need <= *cap && *ptr) return SSJ_OK;
+    if (*ptr) cudaFree(*ptr);
+    *ptr = nullptr;
+    *cap = 0;
+    size_t alloc = std::max<size_t>(need, 1);
+    alloc = alloc + alloc / 4;  // grow with headroom
+    SSJ_CK(cudaMalloc(reinterpret_cast<void**>(ptr), alloc * sizeof(T)));
+    *cap = alloc;
+    return SSJ_OK;
+}
+
+template <typename T>
+int ensure_pinned(T** ptr, size_t* cap, size_t need) {
+    if (need <= *cap && *ptr) return SSJ_OK;
+    if (*ptr) cudaFreeHost(*ptr);
+    *ptr = nullptr;
+    *cap = 0;
+    size_t alloc = std::max<size_t>(need, 1);
+    alloc = alloc + alloc / 4;
+    SSJ_CK(cudaHostAlloc(reinterpret_cast<void**>(ptr), alloc * sizeof(T), cudaHostAllocDefault));
+    *cap = alloc;
+    return SSJ_OK;
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+struct ChunkSlot {
+    uint32_t* dC = nullptr;
+    size_t capC = 0;
+    uint32_t* dCO = nullptr;
+    size_t capCO = 0;
+    uint8_t* dflags = nullptr;
+    size_t capF = 0;
+    uint32_t* dtile = nullptr;
+    size_t capT = 0;
+    unsigned long long* dacc = nullptr;
+    unsigned long long* hacc = nullptr;  // pinned mirror of dacc
+    uint8_t* hflags = nullptr;           // pinned staging for pageable flag buffers
+    size_t capHF = 0;
+    cudaEvent_t ev[kEventsPerSlot] = {};
+    cudaEvent_t done = nullptr;
+    bool busy = false;
+    uint64_t ticket = 0;
+    uint8_t* user_flags = nullptr;
+    bool flags_staged = false;
+    uint64_t nC = 0;
+};
+
+}  // namespace
+
+struct ssj_engine {
+    int device = 0;
+    ssj_predicate hpred{};
+    PredDev pred{};
+    int32_t mode = SSJ_MODE_COUNT;
+    ssj_strategy strategy{};
+    uint32_t n_sets = 0;
+    uint64_t n_tokens = 0;      // unpadded token count (Collection::tokens.size())
+    uint64_t n_padded = 0;      // padded device tokens
+    uint32_t* d_tokens = nullptr;
+    uint2* d_sets = nullptr;
+    bool owns_collection = true;
+    cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+    ChunkSlot slot[2];
+    uint64_t next_ticket = 0;
+    // pageable-input staging
+    uint32_t* bounce[2] = {nullptr, nullptr};
+    size_t bounce_cap[2] = {0, 0};
+    cudaEvent_t bounce_ev[2] = {nullptr, nullptr};
+    // device-API scratch
+    uint32_t* dev_tile = nullptr;
+    size_t dev_tile_cap = 0;
+    // results mode
+    uint32_t* d_res_slots = nullptr;
+    uint32_t* d_res_ov = nullptr;
+    size_t res_cap = 0;
+    size_t res_cap2 = 0;
+    unsigned long long* d_res_n = nullptr;
+};
+
+namespace {
+
+// verify.hpp:249-253 resolves Auto on the CPU (B for avg <= 10, else C with B >= 128).
+// The B200 policy keeps the reference's input (the integer average set size,
+// collection.hpp:91-93) but maps to the GPU kernels: the load-balanced thread-per-pair
+// tiles (A) for short sets, warp-cooperative merge paths (C, 32 lanes) for long ones.
+ssj_strategy resolve_strategy(const ssj_engine& e, ssj_strategy s) {
+    if (s.kind != SSJ_STRATEGY_AUTO) return s;
+    const uint64_t avg = e.n_sets ? e.n_tokens / e.n_sets : 0;
+    if (avg <= 256) return {SSJ_STRATEGY_A, s.group_size};
+    return {SSJ_STRATEGY_C, std::max<uint32_t>(s.group_size, 32)};
+}
+
+int make_pred_dev(const ssj_predicate& p, PredDev* out) {
+    PredDev d{};
+    d.fn = p.function;
+    d.num = p.num;
+    d.den = p.den;
+    d.ovt = p.overlap_threshold;
+    if (p.function == SSJ_JACCARD) {
+        d.A = p.num;
+        d.B = p.den + p.num;  // u64 like similarity.hpp:114
+    } else if (p.function == SSJ_DICE) {
+        d.A = p.num;
+        d.B = 2 * p.den;  // u64 like similarity.hpp:118
+    }
+    if ((p.function == SSJ_JACCARD || p.function == SSJ_DICE) && d.B == 0)
+        return fail(SSJ_ERR_INVALID_ARGUMENT, "threshold denominator overflows");
+    d.wide = (d.A >= (1ull << 30) || d.B >= (1ull << 32)) ? 1 : 0;
+    *out = d;
+    return SSJ_OK;
+}
+
+KParams base_params(const ssj_engine& e) {
+    KParams p{};
+    p.tokens = e.d_tokens;
+    p.sets = e.d_sets;
+    p.n_sets = e.n_sets;
+    p.pred = e.pred;
+    return p;
+}
+
+// Upload helper: host -> device on stream st. Pinned memory goes straight to the DMA
+// engine; pageable memory is staged through the engine's two pinned bounce buffers.
+int upload(ssj_engine& e, void* dst, const void* src, size_t bytes, cudaStream_t st, bool pinned,
+           int* bounce_turn) {
+    if (bytes == 0) return SSJ_OK;
+    if (pinned) {
+        SSJ_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return SSJ_OK;
+    }
+    const size_t piece = 8u << 20;
+    size_t done = 0;
+    while (done < bytes) {
+        const size_t n = std::min(piece, bytes - done);
+        const int b = (*bounce_turn)++ & 1;
+        SSJ_CK(cudaEventSynchronize(e.bounce_ev[b]));
+        int rc = ensure_pinned(&e.bounce[b], &e.bounce_cap[b], piece / 4);
+        if (rc) return rc;
+        std::memcpy(e.bounce[b], static_cast<const char*>(src) + done, n);
+        SSJ_CK(cudaMemcpyAsync(static_cast<char*>(dst) + done, e.bounce[b], n,
+                               cudaMemcpyHostToDevice, st));
+        SSJ_CK(cudaEventRecord(e.bounce_ev[b], st));
+        done += n;
+    }
+    return SSJ_OK;
+}
+
+cudaError_t launch_strategy(const ssj_engine& e, const KParams& p, int out, uint32_t tile_begin,
+                            uint32_t tile_end, cudaStream_t st) {
+    const bool stats = e.strategy.kind != SSJ_STRATEGY_C;
+    switch (e.strategy.kind) {
+        case SSJ_STRATEGY_B: return ssjb::launch_block(p, out, stats, e.strategy.group_size, st);
+        case SSJ_STRATEGY_C: return ssjb::launch_path(p, out, e.strategy.group_size, st);
+        default: return ssjb::launch_tiles(p, out, stats, tile_begin, tile_end, st);
+    }
+}
+
+int check_chunk_args(const ssj_engine* e, const uint32_t* C, uint64_t nC, const uint32_t* C_O,
+                     uint64_t nCO) {
+    if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
+    if (nC && !C) return fail(SSJ_ERR_INVALID_ARGUMENT, "null C with nC > 0");
+    if (nCO >= 2 && !C_O) return fail(SSJ_ERR_INVALID_ARGUMENT, "null C_O with nCO > 0");
+    if (nCO / 2 > 0xFFFFFFFFull) return fail(SSJ_ERR_INVALID_ARGUMENT, "too many slices");
+    if (nC > (0xFFFFFFFFull * (uint64_t)ssjb::kTile))
+        return fail(SSJ_ERR_INVALID_ARGUMENT, "chunk too large");
+    return SSJ_OK;
+}
+
+int decode_error(unsigned long long bits) {
+    if (bits & ssjb::kErrOutOfRange) return fail(SSJ_ERR_OUT_OF_RANGE, "set index out of range");
+    if (bits & ssjb::kErrBadOffsets)
+        return fail(SSJ_ERR_INVALID_ARGUMENT, "malformed C_O: end offsets decreasing or beyond C");
+    return SSJ_OK;
+}
+
+// Enqueue one chunk (host buffers) on slot s. out = kOutFlags / kOutCount / kOutResults.
+int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
+                  const uint32_t* C_O, uint64_t nCO, uint8_t* flags_out, int out) {
+    const uint32_t n_slices = (uint32_t)(nCO / 2);
+    const uint32_t n_tiles = (uint32_t)((nC + ssjb::kTile - 1) / ssjb::kTile);
+    int rc;
+    if ((rc = ensure_device(&s.dC, &s.capC, nC))) return rc;
+    if ((rc = ensure_device(&s.dCO, &s.capCO, (size_t)n_slices * 2))) return rc;
+    if ((rc = ensure_device(&s.dtile, &s.capT, (size_t)n_tiles + 1))) return rc;
+    if (out == ssjb::kOutFlags && (rc = ensure_device(&s.dflags, &s.capF, nC))) return rc;
+    if (out == ssjb::kOutResults) {
+        if ((rc = ensure_device(&e.d_res_slots, &e.res_cap, nC))) return rc;
+        if ((rc = ensure_device(&e.d_res_ov, &e.res_cap2, nC))) return rc;
+    }
+
+    s.user_flags = nullptr;
+    s.flags_staged = false;
+    s.nC = nC;
+    const bool flags_pinned = out == ssjb::kOutFlags && is_pinned(flags_out);
+    if (out == ssjb::kOutFlags) {
+        s.user_flags = flags_out;
+        if (!flags_pinned) {
+            if ((rc = ensure_pinned(&s.hflags, &s.capHF, nC))) return rc;
+            s.flags_staged = true;
+        }
+    }
+    const bool c_pinned = nC == 0 || is_pinned(C);
+    const bool co_pinned = n_slices == 0 || is_pinned(C_O);
+
+    KParams p = base_params(e);
+    p.C = s.dC;
+    p.nC = nC;
+    p.C_O = s.dCO;
+    p.n_slices = n_slices;
+    p.tile_first = s.dtile;
+    p.n_tiles = n_tiles;
+    p.flags = s.dflags;
+    p.res_slots = e.d_res_slots;
+    p.res_ov = e.d_res_ov;
+    p.res_n = e.d_res_n;
+    p.res_cap = nC;
+    p.acc = s.dacc;
+
+    int ev = 0;
+    int turn = 0;
+    SSJ_CK(cudaMemsetAsync(s.dacc, 0, SSJ_RESULT_WORDS * sizeof(unsigned long long), e.s_comp));
+    if (out == ssjb::kOutResults)
+        SSJ_CK(cudaMemsetAsync(e.d_res_n, 0, sizeof(unsigned long long), e.s_comp));
+    if ((rc = upload(e, s.dCO, C_O, (size_t)n_slices * 2 * sizeof(uint32_t), e.s_comp, co_pinned,
+                     &turn)))
+        return rc;
+    SSJ_CK(ssjb::launch_prep(p, e.s_comp));
+
+    // Pieces of the slot range: H2D(piece q+1) overlaps verify(piece q) overlaps D2H(q-1).
+    // Strategies B and C map CTAs to slices, so they take the chunk as one piece.
+    uint64_t piece = nC;
+    if (e.strategy.kind == SSJ_STRATEGY_A) {
+        piece = std::max<uint64_t>(kPieceMinSlots, (nC + kMaxPieces - 1) / kMaxPieces);
+        piece = (piece + ssjb::kTile - 1) / ssjb::kTile * ssjb::kTile;
+    }
+    if (piece == 0) piece = 1;
+    for (uint64_t lo = 0; lo < nC || (lo == 0 && nC == 0); lo += piece) {
+        const uint64_t hi = std::min(nC, lo + piece);
+        if (hi > lo) {
+            if ((rc = upload(e, s.dC + lo, C + lo, (hi - lo) * sizeof(uint32_t), e.s_h2d, c_pinned,
+                             &turn)))
+                return rc;
+            SSJ_CK(cudaEventRecord(s.ev[ev], e.s_h2d));
+            SSJ_CK(cudaStreamWaitEvent(e.s_comp, s.ev[ev], 0));
+            ++ev;
+        }
+        const uint32_t t0 = (uint32_t)(lo / ssjb::kTile);
+        const uint32_t t1 = (uint32_t)((hi + ssjb::kTile - 1) / ssjb::kTile);
+        SSJ_CK(launch_strategy(e, p, out, t0, t1, e.s_comp));
+        if (out == ssjb::kOutFlags && hi > lo) {
+            SSJ_CK(cudaEventRecord(s.ev[ev], e.s_comp));
+            SSJ_CK(cudaStreamWaitEvent(e.s_d2h, s.ev[ev], 0));
+            ++ev;
+            uint8_t* dst = (s.flags_staged ? s.hflags : flags_out) + lo;
+            SSJ_CK(cudaMemcpyAsync(dst, s.dflags + lo, hi - lo, cudaMemcpyDeviceToHost, e.s_d2h));
+        }
+        if (ev + 2 >= kEventsPerSlot) return fail(SSJ_ERR_RUNTIME, "too many pieces");
+        if (nC == 0) break;
+    }
+    SSJ_CK(cudaEventRecord(s.ev[ev], e.s_comp));
+    SSJ_CK(cudaStreamWaitEvent(e.s_d2h, s.ev[ev], 0));
+    SSJ_CK(cudaMemcpyAsync(s.hacc, s.dacc, SSJ_RESULT_WORDS * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, e.s_d2h));
+    SSJ_CK(cudaEventRecord(s.done, e.s_d2h));
+    return SSJ_OK;
+}
+
+int finish_chunk(ssj_engine& e, ChunkSlot& s, uint64_t* count_out, ssj_stats* stats) {
+    SSJ_CK(cudaEventSynchronize(s.done));
+    s.busy = false;
+    int rc = decode_error(s.hacc[SSJ_RESULT_ERROR]);
+    if (rc) return rc;
+    if (s.flags_staged && s.user_flags) std::memcpy(s.user_flags, s.hflags, s.nC);
+    if (count_out) *count_out = s.hacc[SSJ_RESULT_COUNT];
+    if (stats && e.strategy.kind != SSJ_STRATEGY_C) {
+        stats->pairs_verified += s.hacc[SSJ_RESULT_STATS + 0];
+        stats->early_exit_prunes += s.hacc[SSJ_RESULT_STATS + 1];
+        stats->comparison_budget_violations += s.hacc[SSJ_RESULT_STATS + 2];
+    }
+    return SSJ_OK;
+}
+
+void destroy_slot(ChunkSlot& s) {
+    cudaFree(s.dC);
+    cudaFree(s.dCO);
+    cudaFree(s.dflags);
+    cudaFree(s.dtile);
+    cudaFree(s.dacc);
+    cudaFreeHost(s.hacc);
+    cudaFreeHost(s.hflags);
+    for (auto& ev : s.ev)
+        if (ev) cudaEventDestroy(ev);
+    if (s.done) cudaEventDestroy(s.done);
+}
+
+int init_engine_runtime(ssj_engine& e) {
+    SSJ_CK(cudaStreamCreateWithFlags(&e.s_comp, cudaStreamNonBlocking));
+    SSJ_CK(cudaStreamCreateWithFlags(&e.s_h2d, cudaStreamNonBlocking));
+    SSJ_CK(cudaStreamCreateWithFlags(&e.s_d2h, cudaStreamNonBlocking));
+    for (auto& s : e.slot) {
+        for (auto& ev : s.ev) SSJ_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        SSJ_CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+        SSJ_CK(cudaMalloc(&s.dacc, SSJ_RESULT_WORDS * sizeof(unsigned long long)));
+        SSJ_CK(cudaHostAlloc(&s.hacc, SSJ_RESULT_WORDS * sizeof(unsigned long long),
+                             cudaHostAllocDefault));
+    }
+    for (auto& ev : e.bounce_ev) SSJ_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SSJ_CK(cudaMalloc(&e.d_res_n, sizeof(unsigned long long)));
+    return SSJ_OK;
+}
+
+int validate_engine_args(const ssj_predicate* pred, int32_t mode, const ssj_strategy* strategy) {
+    if (!pred || !strategy) return fail(SSJ_ERR_INVALID_ARGUMENT, "null predicate or strategy");
+    int rc = ssj_predicate_validate(pred);
+    if (rc) return rc;
+    if ((rc = ssj_strategy_validate(strategy))) return rc;
+    if (mode != SSJ_MODE_COUNT && mode != SSJ_MODE_PAIRS)
+        return fail(SSJ_ERR_INVALID_ARGUMENT, "bad output mode");
+    return SSJ_OK;
+}
+
+int check_device(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(SSJ_ERR_NO_DEVICE,
+                    "no CUDA device: the B200 verification engine has no CPU fallback");
+    }
+    if (device < 0 || device >= n) return fail(SSJ_ERR_INVALID_ARGUMENT, "bad device ordinal");
+    return SSJ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ssj_abi_version(void) { return SSJ_ABI_VERSION; }
+const char* ssj_last_error(void) { return g_err.c_str(); }
+
+int ssj_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int ssj_threshold_parse(const char* text, uint64_t* num_out, uint64_t* den_out) {
+    // similarity.hpp:30-56 (Threshold::parse) and :58-62 (reduce).
+    if (!text || !num_out || !den_out) return fail(SSJ_ERR_INVALID_ARGUMENT, "null argument");
+    const std::string t(text);
+    if (t.empty()) return fail(SSJ_ERR_INVALID_ARGUMENT, "empty threshold");
+    auto digits = [](const std::string& d, uint64_t* v) {
+        // std::stoull: optional leading whitespace/sign are not produced by this grammar;
+        // requires at least one leading digit and ignores trailing characters.
+        size_t k = 0;
+        uint64_t x = 0;
+        while (k < d.size() && d[k] >= '0' && d[k] <= '9') x = x * 10 + (uint64_t)(d[k++] - '0');
+        if (k == 0) return false;
+        *v = x;
+        return true;
+    };
+    uint64_t num = 0, den = 1;
+    const size_t slash = t.find('/');
+    if (slash != std::string::npos) {
+        if (!digits(t.substr(0, slash), &num) || !digits(t.substr(slash + 1), &den))
+            return fail(SSJ_ERR_INVALID_ARGUMENT, "bad threshold: " + t);
+    } else {
+        const size_t dot = t.find('.');
+        std::string ip = t.substr(0, dot);
+        if (ip.empty()) ip = "0";
+        if (!digits(ip, &num)) return fail(SSJ_ERR_INVALID_ARGUMENT, "bad threshold: " + t);
+        if (dot != std::string::npos) {
+            for (size_t i = dot + 1; i < t.size(); ++i) {
+                const char c = t[i];
+                if (c < '0' || c > '9') return fail(SSJ_ERR_INVALID_ARGUMENT, "bad threshold: " + t);
+                num = num * 10 + (uint64_t)(c - '0');
+                den *= 10;
+            }
+        }
+    }
+    if (den == 0) return fail(SSJ_ERR_INVALID_ARGUMENT, "bad threshold: " + t);
+    uint64_t a = num, b = den;
+    while (b) {
+        const uint64_t r = a % b;
+        a = b;
+        b = r;
+    }
+    if (a > 1) {
+        num /= a;
+        den /= a;
+    }
+    *num_out = num;
+    *den_out = den;
+    return SSJ_OK;
+}
+
+int ssj_predicate_validate(const ssj_predicate* p) {
+    // similarity.hpp:74-81
+    if (!p) return fail(SSJ_ERR_INVALID_ARGUMENT, "null predicate");
+    if (p->function < SSJ_JACCARD || p->function > SSJ_OVERLAP)
+        return fail(SSJ_ERR_INVALID_ARGUMENT, "unknown similarity function");
+    if (p->function != SSJ_OVERLAP) {
+        if (p->num == 0 || p->num > p->den)
+            return fail(SSJ_ERR_INVALID_ARGUMENT, "normalized threshold must be in (0,1]");
+    } else if (p->overlap_threshold < 1) {
+        return fail(SSJ_ERR_INVALID_ARGUMENT, "overlap threshold must be >= 1");
+    }
+    return SSJ_OK;
+}
+
+int ssj_strategy_validate(const ssj_strategy* s) {
+    // verify.hpp:25-28
+    if (!s) return fail(SSJ_ERR_INVALID_ARGUMENT, "null strategy");
+    if (s->kind < SSJ_STRATEGY_A || s->kind > SSJ_STRATEGY_AUTO)
+        return fail(SSJ_ERR_INVALID_ARGUMENT, "unknown strategy kind");
+    if (s->group_size < 1 || (s->group_size & (s->group_size - 1)) != 0)
+        return fail(SSJ_ERR_INVALID_ARGUMENT, "group size must be a power of two");
+    return SSJ_OK;
+}
+
+uint64_t ssj_equivalent_overlap(const ssj_predicate* p, uint64_t r, uint64_t s) {
+    // similarity.hpp:108-123 (host copy of the device formula in ssj_device.cuh)
+    const uint64_t num = p->num, den = p->den;
+    switch (p->function) {
+        case SSJ_JACCARD: return host_ceil_div((u128)num * (r + s), den + num);
+        case SSJ_DICE: return host_ceil_div((u128)num * (r + s), 2 * den);
+        case SSJ_OVERLAP: return p->overlap_threshold;
+        case SSJ_COSINE: {
+            u128 rhs = (u128)num * num * r * s;
+            if (rhs == 0) return 0;
+            long double est = (long double)num / den * sqrtl((long double)r * (long double)s);
+            uint64_t k = est > 2.0L ? (uint64_t)est - 2 : 0;
+            while ((u128)k * k * den * den < rhs) ++k;
+            return k;
+        }
+    }
+    return 0;
+}
+
+int ssj_engine_create(ssj_engine** out, int device, const uint32_t* tokens, const uint32_t* offsets,
+                      uint32_t n_sets, const ssj_predicate* pred, int32_t mode,
+                      const ssj_strategy* strategy) {
+    if (!out) return fail(SSJ_ERR_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    int rc = validate_engine_args(pred, mode, strategy);
+    if (rc) return rc;
+    if (!offsets) return fail(SSJ_ERR_INVALID_ARGUMENT, "null offsets");
+    if (n_sets && offsets[n_sets] && !tokens) return fail(SSJ_ERR_INVALID_ARGUMENT, "null tokens");
+    for (uint32_t i = 0; i < n_sets; ++i)
+        if (offsets[i + 1] < offsets[i])
+            return fail(SSJ_ERR_INVALID_ARGUMENT, "offsets must be non-decreasing");
+    if ((rc = check_device(device))) return rc;
+    DeviceScope ds(device);
+
+    auto* e = new ssj_engine;
+    e->device = device;
+    e->hpred = *pred;
+    e->mode = mode;
+    e->n_sets = n_sets;
+    e->n_tokens = n_sets ? (uint64_t)offsets[n_sets] - offsets[0] : 0;
+    if ((rc = make_pred_dev(*pred, &e->pred))) {
+        delete e;
+        return rc;
+    }
+    e->strategy = resolve_strategy(*e, *strategy);
+
+    // Padded CSR: every set starts on a 32-byte boundary; 8 sentinel tokens at the end so
+    // that the kernels' speculative 32-byte read of any set position stays in bounds.
+    std::vector<uint2> sets(n_sets ? n_sets : 1);
+    uint64_t pos = 0;
+    for (uint32_t i = 0; i < n_sets; ++i) {
+        const uint32_t sz = offsets[i + 1] - offsets[i];
+        sets[i] = make_uint2((uint32_t)(pos / 8), sz);
+        pos += (uint64_t)(sz + 7u) & ~7ull;
+    }
+    if (pos / 8 >= 0xFFFFFFFFull) {
+        delete e;
+        return fail(SSJ_ERR_INVALID_ARGUMENT, "collection too large for u32 set positions");
+    }
+    e->n_padded = pos + 8;
+    std::vector<uint32_t> padded(e->n_padded, 0xFFFFFFFFu);
+    for (uint32_t i = 0; i < n_sets; ++i) {
+        const uint32_t sz = offsets[i + 1] - offsets[i];
+        if (sz) std::memcpy(&padded[(size_t)sets[i].x * 8], tokens + offsets[i], sz * sizeof(uint32_t));
+    }
+    auto cleanup = [&](int code) {
+        ssj_engine_destroy(e);
+        return code;
+    };
+    if ((rc = init_engine_runtime(*e))) return cleanup(rc);
+    if (cudaMalloc(&e->d_tokens, e->n_padded * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&e->d_sets, sets.size() * sizeof(uint2)) != cudaSuccess)
+        return cleanup(fail(SSJ_ERR_CUDA, "cudaMalloc of the collection failed"));
+    if (cudaMemcpy(e->d_tokens, padded.data(), e->n_padded * sizeof(uint32_t),
+                   cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(e->d_sets, sets.data(), sets.size() * sizeof(uint2), cudaMemcpyHostToDevice) !=
+            cudaSuccess)
+        return cleanup(fail(SSJ_ERR_CUDA, "collection upload failed"));
+    *out = e;
+    return SSJ_OK;
+}
+
+int ssj_engine_create_from_device(ssj_engine** out, int device, const uint32_t* d_tokens,
+                                  uint64_t n_padded_tokens, const uint32_t* d_sets, uint32_t n_sets,
+                                  uint64_t n_tokens_total, const ssj_predicate* pred, int32_t mode,
+                                  const ssj_strategy* strategy) {
+    if (!out) return fail(SSJ_ERR_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    int rc = validate_engine_args(pred, mode, strategy);
+    if (rc) return rc;
+    if (!d_tokens || !d_sets) return fail(SSJ_ERR_INVALID_ARGUMENT, "null device collection");
+    if ((rc = check_device(device))) return rc;
+    DeviceScope ds(device);
+    auto* e = new ssj_engine;
+    e->device = device;
+    e->hpred = *pred;
+    e->mode = mode;
+    e->n_sets = n_sets;
+    e->n_tokens = n_tokens_total;
+    e->n_padded = n_padded_tokens;
+    e->owns_collection = false;
+    e->d_tokens = const_cast<uint32_t*>(d_tokens);
+    e->d_sets = reinterpret_cast<uint2*>(const_cast<uint32_t*>(d_sets));
+    if ((rc = make_pred_dev(*pred, &e->pred))) {
+        delete e;
+        return rc;
+    }
+    e->strategy = resolve_strategy(*e, *strategy);
+    if ((rc = init_engine_runtime(*e))) {
+        ssj_engine_destroy(e);
+        return rc;
+    }
+    *out = e;
+    return SSJ_OK;
+}
+
+int ssj_engine_device_collection(const ssj_engine* e, const uint32_t** d_tokens,
+                                 uint64_t* n_padded_tokens, const uint32_t** d_sets) {
+    if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
+    if (d_tokens) *d_tokens = e->d_tokens;
+    if (n_padded_tokens) *n_padded_tokens = e->n_padded;
+    if (d_sets) *d_sets = reinterpret_cast<const uint32_t*>(e->d_sets);
+    return SSJ_OK;
+}
+
+void ssj_engine_destroy(ssj_engine* e) {
+    if (!e) return;
+    DeviceScope ds(e->device);
+    if (e->s_comp) cudaStreamSynchronize(e->s_comp);
+    if (e->s_h2d) cudaStreamSynchronize(e->s_h2d);
+    if (e->s_d2h) cudaStreamSynchronize(e->s_d2h);
+    for (auto& s : e->slot) destroy_slot(s);
+    for (int b = 0; b < 2; ++b) {
+        cudaFreeHost(e->bounce[b]);
+        if (e->bounce_ev[b]) cudaEventDestroy(e->bounce_ev[b]);
+    }
+    if (e->owns_collection) {
+        cudaFree(e->d_tokens);
+        cudaFree(e->d_sets);
+    }
+    cudaFree(e->dev_tile);
+    cudaFree(e->d_res_slots);
+    cudaFree(e->d_res_ov);
+    cudaFree(e->d_res_n);
+    if (e->s_comp) cudaStreamDestroy(e->s_comp);
+    if (e->s_h2d) cudaStreamDestroy(e->s_h2d);
+    if (e->s_d2h) cudaStreamDestroy(e->s_d2h);
+    delete e;
+}
+
+int ssj_engine_strategy(const ssj_engine* e, ssj_strategy* resolved) {
+    if (!e || !resolved) return fail(SSJ_ERR_INVALID_ARGUMENT, "null argument");
+    *resolved = e->strategy;
+    return SSJ_OK;
+}
+
+int ssj_engine_device(const ssj_engine* e) { return e ? e->device : -1; }
+
+int ssj_submit_chunk(ssj_engine* e, const uint32_t* C, uint64_t nC, const uint32_t* C_O,
+                     uint64_t nCO, uint8_t* flags_out, uint64_t* ticket) {
+    int rc = check_chunk_args(e, C, nC, C_O, nCO);
+    if (rc) return rc;
+    if (!ticket) return fail(SSJ_ERR_INVALID_ARGUMENT, "null ticket");
+    DeviceScope ds(e->device);
+    const uint64_t t = e->next_ticket;
+    ChunkSlot& s = e->slot[t & 1];
+    if (s.busy) return fail(SSJ_ERR_RUNTIME, "two chunks already in flight: wait first");
+    const int out = (e->mode == SSJ_MODE_PAIRS && flags_out) ? ssjb::kOutFlags : ssjb::kOutCount;
+    if ((rc = enqueue_chunk(*e, s, C, nC, C_O, nCO, flags_out, out))) {
+        // drain whatever was enqueued so the slot is reusable
+        cudaStreamSynchronize(e->s_comp);
+        cudaStreamSynchronize(e->s_h2d);
+        cudaStreamSynchronize(e->s_d2h);
+        return rc;
+    }
+    s.busy = true;
+    s.ticket = t;
+    e->next_ticket = t + 1;
+    *ticket = t;
+    return SSJ_OK;
+}
+
+int ssj_wait_chunk(ssj_engine* e, uint64_t ticket, uint64_t* count_out, ssj_stats* stats) {
+    if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
+    DeviceScope ds(e->device);
+    ChunkSlot& s = e->slot[ticket & 1];
+    if (!s.busy || s.ticket != ticket) return fail(SSJ_ERR_INVALID_ARGUMENT, "unknown ticket");
+    return finish_chunk(*e, s, count_out, stats);
+}
+
+int ssj_verify_chunk(ssj_engine* e, const uint32_t* C, uint64_t nC, const uint32_t* C_O,
+                     uint64_t nCO, uint8_t* flags_out, uint64_t* count_out, ssj_stats* stats) {
+    uint64_t t = 0;
+    int rc = ssj_submit_chunk(e, C, nC, C_O, nCO, flags_out, &t);
+    if (rc) return rc;
+    return ssj_wait_chunk(e, t, count_out, stats);
+}
+
+int ssj_verify_chunk_results(ssj_engine* e, const uint32_t* C, uint64_t nC, const uint32_t* C_O,
+                             uint64_t nCO, uint32_t* slots_out, uint32_t* overlaps_out,
+                             uint64_t cap, uint64_t* n_out) {
+    int rc = check_chunk_args(e, C, nC, C_O, nCO);
+    if (rc) return rc;
+    if (!n_out || (cap && (!slots_out || !overlaps_out)))
+        return fail(SSJ_ERR_INVALID_ARGUMENT, "null output");
+    DeviceScope ds(e->device);
+    ChunkSlot& s = e->slot[e->next_ticket & 1];
+    if (s.busy) return fail(SSJ_ERR_RUNTIME, "a chunk is in flight on this slot: wait first");
+    if ((rc = enqueue_chunk(*e, s, C, nC, C_O, nCO, nullptr, ssjb::kOutResults))) {
+        cudaDeviceSynchronize();
+        return rc;
+    }
+    SSJ_CK(cudaEventSynchronize(s.done));
+    if ((rc = decode_error(s.hacc[SSJ_RESULT_ERROR]))) return rc;
+    unsigned long long n = 0;
+    SSJ_CK(cudaMemcpy(&n, e->d_res_n, sizeof(n), cudaMemcpyDeviceToHost));
+    *n_out = n;
+    std::vector<uint32_t> sl(n), ov(n);
+    if (n) {
+        SSJ_CK(cudaMemcpy(sl.data(), e->d_res_slots, n * 4, cudaMemcpyDeviceToHost));
+        SSJ_CK(cudaMemcpy(ov.data(), e->d_res_ov, n * 4, cudaMemcpyDeviceToHost));
+    }
+    // Ascending slot order (the warp-aggregated appends are unordered).
+    std::vector<uint64_t> key(n);
+    for (uint64_t i = 0; i < n; ++i) key[i] = ((uint64_t)sl[i] << 32) | ov[i];
+    std::sort(key.begin(), key.end());
+    const uint64_t w = std::min<uint64_t>(n, cap);
+    for (uint64_t i = 0; i < w; ++i) {
+        slots_out[i] = (uint32_t)(key[i] >> 32);
+        overlaps_out[i] = (uint32_t)key[i];
+    }
+    if (n > cap) return fail(SSJ_ERR_RUNTIME, "result capacity exceeded");
+    return SSJ_OK;
+}
+
+int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, const uint32_t* d_C_O,
+                            uint64_t nCO, uint8_t* d_flags, uint64_t* d_result, void* stream) {
+    int rc = check_chunk_args(e, d_C, nC, d_C_O, nCO);
+    if (rc) return rc;
+    if (!d_result) return fail(SSJ_ERR_INVALID_ARGUMENT, "null d_result");
+    DeviceScope ds(e->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : e->s_comp;
+    const uint32_t n_slices = (uint32_t)(nCO / 2);
+    const uint32_t n_tiles = (uint32_t)((nC + ssjb::kTile - 1) / ssjb::kTile);
+    if ((rc = ensure_device(&e->dev_tile, &e->dev_tile_cap, (size_t)n_tiles + 1))) return rc;
+    KParams p = base_params(*e);
+    p.C = d_C;
+    p.nC = nC;
+    p.C_O = d_C_O;
+    p.n_slices = n_slices;
+    p.tile_first = e->dev_tile;
+    p.n_tiles = n_tiles;
+    p.flags = d_flags;
+    p.acc = reinterpret_cast<unsigned long long*>(d_result);
+    const int out = (e->mode == SSJ_MODE_PAIRS && d_flags) ? ssjb::kOutFlags : ssjb::kOutCount;
+    SSJ_CK(cudaMemsetAsync(d_result, 0, SSJ_RESULT_WORDS * sizeof(uint64_t), st));
+    SSJ_CK(ssjb::launch_prep(p, st));
+    SSJ_CK(launch_strategy(*e, p, out, 0, n_tiles, st));
+    return SSJ_OK;
+}
+
+int ssj_launches_per_chunk(const ssj_engine* e, uint64_t nC, uint64_t nCO) {
+    (void)e;
+    (void)nC;
+    (void)nCO;
+    return 2;  // prep + one verification kernel (the memset is not a kernel of ours)
+}
+
+int ssj_chunk_algorithmic_bytes_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC,
+                                       const uint32_t* d_C_O, uint64_t nCO, uint64_t* d_bytes,
+                                       void* stream) {
+    int rc = check_chunk_args(e, d_C, nC, d_C_O, nCO);
+    if (rc) return rc;
+    DeviceScope ds(e->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : e->s_comp;
+    KParams p = base_params(*e);
+    p.C = d_C;
+    p.nC = nC;
+    p.C_O = d_C_O;
+    p.n_slices = (uint32_t)(nCO / 2);
+    SSJ_CK(cudaMemsetAsync(d_bytes, 0, sizeof(uint64_t), st));
+    SSJ_CK(ssjb::launch_bytes(p, reinterpret_cast<unsigned long long*>(d_bytes), st));
+    return SSJ_OK;
+}
+
+void* ssj_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        g_err = "cudaHostAlloc failed";
+        return nullptr;
+    }
+    return p;
+}
+
+void ssj_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

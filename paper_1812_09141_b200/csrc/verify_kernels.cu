@@ -1,0 +1,527 @@
+// verify_kernels.cu -- sm_100a candidate-verification kernels.
+//
+// The reference verifies a chunk on a CPU worker pool under one of three work
+// assignments (verify.hpp:232-345, the paper's thread-allocation alternatives A/B/C,
+// PAPER.md:605-644). Here each becomes a grid:
+//   A  tile_kernel  : load-balanced thread-per-pair. The chunk's slot range is cut into
+//                     fixed tiles of kTile candidates (independent of slice lengths); a CTA
+//                     maps its slots to slices with a shared-memory search over the
+//                     tile's C_O entries and stages the tile's probe sets in shared memory.
+//   B  block_kernel : one CTA per probe slice (paper Alt B): the probe set is staged in
+//                     shared memory and the CTA's threads stride over the slice's
+//                     candidates, each running the sequential early-exit merge.
+//   C  path_kernel  : one CTA per probe slice, groups of G lanes per candidate pair
+//                     (paper Alt C / verify.hpp:303-345): the G lanes split the pair's
+//                     merge path with the reference's diagonal partitions
+//                     (verify.hpp:110-166) and reduce their counts with shuffles. Unlike
+//                     the reference it walks the path in rounds of G*kHops hops and stops
+//                     as soon as the verdict is decided.
+// All three produce the reference's flags bit for bit (see ssj_device.cuh).
+#include <cub/block/block_scan.cuh>
+
+#include "verify_kernels.cuh"
+
+namespace ssjb {
+
+namespace {
+
+constexpr uint32_t kNoStage = 0xFFFFFFFFu;
+
+__device__ __forceinline__ void acc_add(unsigned long long* acc, int word, unsigned v) {
+    const unsigned w = __reduce_add_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(acc + word, (unsigned long long)w);
+}
+
+__device__ __forceinline__ void flag_error(unsigned long long* acc, unsigned long long bits) {
+    atomicOr(acc + 1, bits);
+}
+
+// Warp-aggregated append of qualifying (slot, overlap) results: one atomicAdd per warp.
+// Must be called by all 32 lanes of the warp.
+__device__ __forceinline__ void warp_append(const KParams& p, bool met, uint64_t slot,
+                                            uint32_t ov) {
+    const unsigned mask = __ballot_sync(0xffffffffu, met);
+    if (!mask) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(p.res_n, (unsigned long long)__popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (met) {
+        const unsigned long long idx = base + __popc(mask & ((1u << lane) - 1u));
+        if (idx < p.res_cap) {
+            p.res_slots[idx] = (uint32_t)slot;
+            p.res_ov[idx] = ov;
+        }
+    }
+}
+
+// One candidate pair, thread-sequential (strategies A and B).
+// r/m: probe tokens (shared or global); returns met, *ov = true overlap in results mode.
+template <int kOut>
+__device__ __forceinline__ bool verify_pair(const KParams& p, const uint32_t* r, uint32_t m,
+                                            uint32_t cand, uint32_t* ov, uint32_t* n_out) {
+    if (cand >= p.n_sets) {
+        flag_error(p.acc, kErrOutOfRange);
+        *n_out = 0;
+        return false;
+    }
+    const uint2 sd = __ldg(p.sets + cand);
+    const uint32_t n = sd.y;
+    *n_out = n;
+    const uint4* s4 = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd.x * 8);
+    // Speculative: every set position has >= 8 readable tokens (padding + tail sentinel).
+    const uint4 w0 = __ldg(s4);
+    const uint4 w1 = __ldg(s4 + 1);
+    const uint64_t req = dev_required(p.pred, m, n);
+    if (req == 0) {
+        // verify.hpp:57: the loop exits before any comparison and met = (0 >= 0).
+        if (kOut == kOutResults)
+            *ov = full_overlap_seq(r, m, reinterpret_cast<const uint32_t*>(s4), n);
+        return true;
+    }
+    if (req > (uint64_t)min(m, n)) return false;  // overlap <= min(m, n) < req
+    return merge_thread<kOut == kOutResults>(r, m, s4, n, (uint32_t)req, w0, w1, ov);
+}
+
+__device__ __forceinline__ uint32_t upper_bound_smem(const uint32_t* a, uint32_t n, uint64_t key) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((uint64_t)a[mid] <= key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// First slice e in [lo, hi) whose end offset (C_O[2e+1]) is > key.
+__device__ __forceinline__ uint32_t upper_bound_ends(const uint32_t* __restrict__ C_O,
+                                                     uint32_t lo, uint32_t hi, uint64_t key) {
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((uint64_t)__ldg(C_O + 2 * (size_t)mid + 1) <= key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// ---------------------------------------------------------------------------------------
+// Prep: validate C_O (chunk.hpp:36-48 decode assumptions) and compute the first slice of
+// every tile. Thread idx handles slice idx and tile idx.
+__global__ void prep_kernel(const KParams p) {
+    const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx < p.n_slices) {
+        const uint32_t end = p.C_O[2 * idx + 1];
+        const uint32_t begin = idx ? p.C_O[2 * idx - 1] : 0;
+        if (end < begin || (uint64_t)end > p.nC) flag_error(p.acc, kErrBadOffsets);
+        if (end > begin && p.C_O[2 * idx] >= p.n_sets) flag_error(p.acc, kErrOutOfRange);
+    }
+    if (idx <= p.n_tiles) {
+        p.tile_first[idx] = idx == p.n_tiles
+                                ? p.n_slices
+                                : upper_bound_ends(p.C_O, 0, p.n_slices, idx * (uint64_t)kTile);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Strategy A: load-balanced thread-per-pair over fixed slot tiles.
+template <int kOut, bool kStats>
+__global__ void __launch_bounds__(kThreadsA) tile_kernel(const KParams p, const uint32_t tile_begin) {
+    using Scan = cub::BlockScan<uint32_t, kThreadsA>;
+    __shared__ uint32_t sh_end[kMaxTileSlices];
+    __shared__ uint32_t sh_rsize[kMaxTileSlices];
+    __shared__ uint32_t sh_rpos8[kMaxTileSlices];
+    __shared__ uint32_t sh_rofs[kMaxTileSlices];
+    __shared__ __align__(16) uint32_t sh_r[kTileRCap];
+    __shared__ typename Scan::TempStorage scan_tmp;
+
+    const uint32_t tile = tile_begin + blockIdx.x;
+    const uint64_t slot0 = (uint64_t)tile * kTile;
+    if (slot0 >= p.nC) return;
+    const uint64_t slot1 = min(slot0 + (uint64_t)kTile, p.nC);
+    const uint32_t e0 = p.tile_first[tile];
+    const uint32_t tid = threadIdx.x;
+
+    uint32_t ns = 0;
+    bool fast = false;
+    if (e0 < p.n_slices) {
+        uint32_t e_hi = p.tile_first[tile + 1];
+        if (e_hi >= p.n_slices) e_hi = p.n_slices - 1;
+        ns = e_hi - e0 + 1;
+        fast = ns <= kMaxTileSlices;
+    }
+
+    if (fast) {
+        // Describe the tile's slices: end offset, probe size and position.
+        constexpr int kItems = kMaxTileSlices / kThreadsA;
+        uint32_t padded[kItems];
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) {
+            const uint32_t k = tid * kItems + q;
+            padded[q] = 0;
+            if (k < ns) {
+                const size_t e = (size_t)e0 + k;
+                const uint32_t probe = __ldg(p.C_O + 2 * e);
+                sh_end[k] = __ldg(p.C_O + 2 * e + 1);
+                const uint2 rd = probe < p.n_sets ? __ldg(p.sets + probe) : make_uint2(0, 0);
+                sh_rsize[k] = rd.y;
+                sh_rpos8[k] = rd.x;
+                padded[q] = (rd.y + 7u) & ~7u;
+            }
+        }
+        uint32_t ofs[kItems];
+        Scan(scan_tmp).ExclusiveSum(padded, ofs);
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) {
+            const uint32_t k = tid * kItems + q;
+            if (k < ns) sh_rofs[k] = (ofs[q] + padded[q] <= kTileRCap) ? ofs[q] : kNoStage;
+        }
+        __syncthreads();
+        // Stage the probes that fit: one warp per slice, 16-byte vector copies.
+        const uint32_t warp = tid >> 5, lane = tid & 31;
+        for (uint32_t k = warp; k < ns; k += kThreadsA / 32) {
+            const uint32_t o = sh_rofs[k];
+            if (o == kNoStage) continue;
+            const uint4* src = reinterpret_cast<const uint4*>(p.tokens + (size_t)sh_rpos8[k] * 8);
+            uint4* dst = reinterpret_cast<uint4*>(sh_r + o);
+            const uint32_t units = ((sh_rsize[k] + 7u) & ~7u) >> 2;
+            for (uint32_t u = lane; u < units; u += 32) dst[u] = __ldg(src + u);
+        }
+        __syncthreads();
+    }
+
+    unsigned count = 0, prunes = 0, verified = 0;
+#pragma unroll 1
+    for (uint32_t it = 0; it < kTile / kThreadsA; ++it) {
+        const uint64_t slot = slot0 + (uint64_t)it * kThreadsA + tid;
+        bool met = false;
+        uint32_t ov = 0;
+        if (slot < slot1 && e0 < p.n_slices) {
+            const uint32_t* r = nullptr;
+            uint32_t m = 0;
+            bool covered;
+            if (fast) {
+                const uint32_t li = upper_bound_smem(sh_end, ns, slot);
+                covered = li < ns;
+                if (covered) {
+                    m = sh_rsize[li];
+                    const uint32_t o = sh_rofs[li];
+                    r = o != kNoStage ? sh_r + o : p.tokens + (size_t)sh_rpos8[li] * 8;
+                }
+            } else {
+                const uint32_t e = upper_bound_ends(p.C_O, e0, p.n_slices, slot);
+                covered = e < p.n_slices;
+                if (covered) {
+                    const uint32_t probe = __ldg(p.C_O + 2 * (size_t)e);
+                    const uint2 rd = probe < p.n_sets ? __ldg(p.sets + probe) : make_uint2(0, 0);
+                    m = rd.y;
+                    r = p.tokens + (size_t)rd.x * 8;
+                }
+            }
+            if (covered) {
+                uint32_t n = 0;
+                met = verify_pair<kOut>(p, r, m, __ldg(p.C + slot), &ov, &n);
+                if (kStats) {
+                    ++verified;
+                    prunes += (!met && (m + n) > 0);
+                }
+            }
+            if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
+        }
+        count += met;
+        if (kOut == kOutResults) warp_append(p, met, slot, ov);
+    }
+    acc_add(p.acc, 0, count);
+    if (kStats) {
+        acc_add(p.acc, 2, verified);
+        acc_add(p.acc, 3, prunes);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Strategy B: one CTA per probe slice, threads stride over the slice's candidates.
+template <int kOut, bool kStats>
+__global__ void block_kernel(const KParams p, const uint32_t rcap) {
+    extern __shared__ __align__(16) uint32_t dsh[];
+    unsigned count = 0, prunes = 0, verified = 0;
+    for (uint32_t e = blockIdx.x; e < p.n_slices; e += gridDim.x) {
+        const uint32_t begin = e ? __ldg(p.C_O + 2 * (size_t)e - 1) : 0;
+        const uint32_t end = __ldg(p.C_O + 2 * (size_t)e + 1);
+        if (end <= begin || (uint64_t)end > p.nC) continue;  // block-uniform
+        const uint32_t probe = __ldg(p.C_O + 2 * (size_t)e);
+        const uint2 rd = probe < p.n_sets ? __ldg(p.sets + probe) : make_uint2(0, 0);
+        const uint32_t m = rd.y;
+        const uint32_t padded = (m + 7u) & ~7u;
+        const bool staged = padded <= rcap;
+        __syncthreads();  // previous slice's readers are done with dsh
+        if (staged) {
+            const uint4* src = reinterpret_cast<const uint4*>(p.tokens + (size_t)rd.x * 8);
+            uint4* dst = reinterpret_cast<uint4*>(dsh);
+            for (uint32_t u = threadIdx.x; u < padded / 4; u += blockDim.x) dst[u] = __ldg(src + u);
+        }
+        __syncthreads();
+        const uint32_t* r = staged ? dsh : p.tokens + (size_t)rd.x * 8;
+        for (uint64_t base = begin; base < end; base += blockDim.x) {
+            const uint64_t slot = base + threadIdx.x;
+            bool met = false;
+            uint32_t ov = 0;
+            if (slot < end) {
+                uint32_t n = 0;
+                met = verify_pair<kOut>(p, r, m, __ldg(p.C + slot), &ov, &n);
+                if (kStats) {
+                    ++verified;
+                    prunes += (!met && (m + n) > 0);
+                }
+                if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
+            }
+            count += met;
+            if (kOut == kOutResults) warp_append(p, met, slot, ov);
+        }
+    }
+    acc_add(p.acc, 0, count);
+    if (kStats) {
+        acc_add(p.acc, 2, verified);
+        acc_add(p.acc, 3, prunes);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Strategy C: G lanes per pair over merge-path partitions, round-level early exit.
+constexpr uint32_t kHops = 16;
+
+template <int G, int kOut>
+__global__ void path_kernel(const KParams p, const uint32_t rcap) {
+    extern __shared__ __align__(16) uint32_t dsh[];
+    const uint32_t lane = threadIdx.x % G;
+    const uint32_t group = threadIdx.x / G;
+    const uint32_t ngroups = blockDim.x / G;
+    const unsigned gmask =
+        G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) / G * G));
+    unsigned count = 0;
+    for (uint32_t e = blockIdx.x; e < p.n_slices; e += gridDim.x) {
+        const uint32_t begin = e ? __ldg(p.C_O + 2 * (size_t)e - 1) : 0;
+        const uint32_t end = __ldg(p.C_O + 2 * (size_t)e + 1);
+        if (end <= begin || (uint64_t)end > p.nC) continue;
+        const uint32_t probe = __ldg(p.C_O + 2 * (size_t)e);
+        const uint2 rd = probe < p.n_sets ? __ldg(p.sets + probe) : make_uint2(0, 0);
+        const uint32_t m = rd.y;
+        const uint32_t padded = (m + 7u) & ~7u;
+        const bool staged = padded <= rcap;
+        __syncthreads();
+        if (staged) {
+            const uint4* src = reinterpret_cast<const uint4*>(p.tokens + (size_t)rd.x * 8);
+            uint4* dst = reinterpret_cast<uint4*>(dsh);
+            for (uint32_t u = threadIdx.x; u < padded / 4; u += blockDim.x) dst[u] = __ldg(src + u);
+        }
+        __syncthreads();
+        const uint32_t* r = staged ? dsh : p.tokens + (size_t)rd.x * 8;
+        for (uint64_t base = begin; base < end; base += ngroups) {
+            const uint64_t slot = base + group;
+            bool met = false;
+            uint32_t ov = 0;
+            if (slot < end) {  // group-uniform
+                const uint32_t cand = __ldg(p.C + slot);
+                if (cand >= p.n_sets) {
+                    if (lane == 0) flag_error(p.acc, kErrOutOfRange);
+                } else {
+                    const uint2 sd = __ldg(p.sets + cand);
+                    const uint32_t n = sd.y;
+                    const uint32_t* s = p.tokens + (size_t)sd.x * 8;
+                    const uint64_t req = dev_required(p.pred, m, n);
+                    const uint32_t total = m + n;
+                    bool decided = false;
+                    if (req > (uint64_t)min(m, n)) {
+                        decided = true;  // met = false
+                    } else if (req == 0 && kOut != kOutResults) {
+                        decided = true;
+                        met = true;
+                    }
+                    uint32_t D = 0;
+                    while (!decided && D < total) {
+                        const uint32_t d = D + lane * kHops;
+                        uint32_t cnt = 0, ie = m, je = n;
+                        if (d < total) {
+                            uint32_t i = dev_merge_path_split(r, m, s, n, d);
+                            uint32_t j = d - i;
+                            const uint32_t hops = min(kHops, total - d);
+                            for (uint32_t h = 0; h < hops && (i < m || j < n); ++h) {
+                                // verify.hpp:157-163: a common value counts at its r-side hop
+                                if (j >= n || (i < m && r[i] <= s[j])) {
+                                    if (j < n && r[i] == s[j]) ++cnt;
+                                    ++i;
+                                } else {
+                                    ++j;
+                                }
+                            }
+                            ie = i;
+                            je = j;
+                        }
+#pragma unroll
+                        for (int off = G / 2; off > 0; off >>= 1)
+                            cnt += __shfl_xor_sync(gmask, cnt, off, G);
+                        ov += cnt;
+                        const uint32_t Dn = min(D + G * kHops, total);
+                        const uint32_t lb = (Dn - D - 1) / kHops;  // last lane with work
+                        const uint32_t iD = __shfl_sync(gmask, ie, lb, G);
+                        const uint32_t jD = __shfl_sync(gmask, je, lb, G);
+                        D = Dn;
+                        if (kOut != kOutResults && ov >= req) {
+                            met = true;
+                            decided = true;
+                        } else if ((uint64_t)ov + min(m - iD, n - jD) < req) {
+                            decided = true;  // the bound of verify.hpp:58 at diagonal D
+                        }
+                    }
+                    if (!decided) met = ov >= req;  // full path walked: ov = |r ∩ s|
+                }
+                if (kOut == kOutFlags && lane == 0) p.flags[slot] = met ? 1 : 0;
+            }
+            const bool leader_met = met && lane == 0;
+            count += leader_met;
+            if (kOut == kOutResults) warp_append(p, leader_met, slot, ov);
+        }
+    }
+    acc_add(p.acc, 0, count);
+}
+
+// ---------------------------------------------------------------------------------------
+// Instrumentation: algorithmic bytes under the reference loop
+// verify.hpp:56-69, replayed exactly per pair.
+__global__ void bytes_kernel(const KParams p, unsigned long long* out) {
+    const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long b = 0;
+    if (idx < p.n_slices) {
+        const uint32_t probe = p.C_O[2 * idx];
+        const uint32_t m = probe < p.n_sets ? p.sets[probe].y : 0;
+        b += 8 + 8 + 4ull * m;
+    }
+    if (idx < p.nC) {
+        const uint32_t e = upper_bound_ends(p.C_O, 0, p.n_slices, idx);
+        const uint32_t cand = p.C[idx];
+        if (e < p.n_slices && cand < p.n_sets) {
+            const uint32_t probe = p.C_O[2 * (size_t)e];
+            if (probe < p.n_sets) {
+                const uint2 rd = p.sets[probe], sd = p.sets[cand];
+                const uint32_t* r = p.tokens + (size_t)rd.x * 8;
+                const uint32_t* s = p.tokens + (size_t)sd.x * 8;
+                const uint32_t m = rd.y, n = sd.y;
+                const uint64_t req = dev_required(p.pred, m, n);
+                uint64_t ov = 0;
+                uint32_t i = 0, j = 0;
+                while (i < m && j < n) {
+                    if (ov >= req) break;
+                    if (ov + min(m - i, n - j) < req) break;
+                    if (r[i] == s[j]) {
+                        ++ov; ++i; ++j;
+                    } else if (r[i] < s[j]) {
+                        ++i;
+                    } else {
+                        ++j;
+                    }
+                }
+                const uint32_t touched = min(j + 1, n);
+                b += 4 + 8 + 1 + 4ull * touched;
+            }
+        }
+    }
+    for (int off = 16; off > 0; off >>= 1) b += __shfl_xor_sync(0xffffffffu, b, off);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(out, b);
+}
+
+template <int G, int kOut>
+cudaError_t launch_path_g(const KParams& p, uint32_t grid, uint32_t rcap, size_t smem,
+                          cudaStream_t st) {
+    auto k = path_kernel<G, kOut>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<grid, 256, smem, st>>>(p, rcap);
+    return cudaGetLastError();
+}
+
+template <int G>
+cudaError_t launch_path_out(const KParams& p, int out, uint32_t grid, uint32_t rcap, size_t smem,
+                            cudaStream_t st) {
+    switch (out) {
+        case kOutFlags: return launch_path_g<G, kOutFlags>(p, grid, rcap, smem, st);
+        case kOutResults: return launch_path_g<G, kOutResults>(p, grid, rcap, smem, st);
+        default: return launch_path_g<G, kOutCount>(p, grid, rcap, smem, st);
+    }
+}
+
+uint32_t slice_grid(uint32_t n_slices) {
+    // One CTA per probe slice (the paper's launch shape), capped; CTAs grid-stride.
+    const uint32_t cap = 148u * 64u;
+    return n_slices < cap ? (n_slices ? n_slices : 1) : cap;
+}
+
+constexpr uint32_t kSliceRCap = 12288;  // tokens staged per CTA in strategies B/C (48 KB)
+
+}  // namespace
+
+cudaError_t launch_prep(const KParams& p, cudaStream_t st) {
+    const uint64_t work = (uint64_t)max(p.n_slices, p.n_tiles + 1);
+    const uint32_t threads = 256;
+    const uint32_t grid = (uint32_t)((work + threads - 1) / threads);
+    prep_kernel<<<grid ? grid : 1, threads, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_begin,
+                         uint32_t tile_end, cudaStream_t st) {
+    if (tile_end <= tile_begin) return cudaSuccess;
+    const uint32_t grid = tile_end - tile_begin;
+    switch (out * 2 + (stats ? 1 : 0)) {
+        case 0: tile_kernel<kOutCount, false><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
+        case 1: tile_kernel<kOutCount, true><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
+        case 2: tile_kernel<kOutFlags, false><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
+        case 3: tile_kernel<kOutFlags, true><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
+        case 4: tile_kernel<kOutResults, false><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
+        default: tile_kernel<kOutResults, true><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_block(const KParams& p, int out, bool stats, uint32_t threads,
+                         cudaStream_t st) {
+    threads = threads < 32 ? 32 : (threads > 1024 ? 1024 : threads);
+    const uint32_t grid = slice_grid(p.n_slices);
+    const size_t smem = kSliceRCap * sizeof(uint32_t);
+    const uint32_t rcap = kSliceRCap;
+#define SSJB_LAUNCH_B(O, S)                                                                   \
+    do {                                                                                      \
+        auto k = block_kernel<O, S>;                                                          \
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+        k<<<grid, threads, smem, st>>>(p, rcap);                                              \
+    } while (0)
+    switch (out * 2 + (stats ? 1 : 0)) {
+        case 0: SSJB_LAUNCH_B(kOutCount, false); break;
+        case 1: SSJB_LAUNCH_B(kOutCount, true); break;
+        case 2: SSJB_LAUNCH_B(kOutFlags, false); break;
+        case 3: SSJB_LAUNCH_B(kOutFlags, true); break;
+        case 4: SSJB_LAUNCH_B(kOutResults, false); break;
+        default: SSJB_LAUNCH_B(kOutResults, true); break;
+    }
+#undef SSJB_LAUNCH_B
+    return cudaGetLastError();
+}
+
+cudaError_t launch_path(const KParams& p, int out, uint32_t group, cudaStream_t st) {
+    const uint32_t grid = slice_grid(p.n_slices);
+    const size_t smem = kSliceRCap * sizeof(uint32_t);
+    const uint32_t rcap = kSliceRCap;
+    if (group >= 32) return launch_path_out<32>(p, out, grid, rcap, smem, st);
+    if (group >= 16) return launch_path_out<16>(p, out, grid, rcap, smem, st);
+    if (group >= 8) return launch_path_out<8>(p, out, grid, rcap, smem, st);
+    if (group >= 4) return launch_path_out<4>(p, out, grid, rcap, smem, st);
+    if (group >= 2) return launch_path_out<2>(p, out, grid, rcap, smem, st);
+    return launch_path_out<1>(p, out, grid, rcap, smem, st);
+}
+
+cudaError_t launch_bytes(const KParams& p, unsigned long long* d_bytes, cudaStream_t st) {
+    const uint64_t work = p.nC > p.n_slices ? p.nC : p.n_slices;
+    const uint32_t threads = 256;
+    const uint64_t grid = (work + threads - 1) / threads;
+    bytes_kernel<<<(uint32_t)(grid ? grid : 1), threads, 0, st>>>(p, d_bytes);
+    return cudaGetLastError();
+}
+
+}  // namespace ssjb

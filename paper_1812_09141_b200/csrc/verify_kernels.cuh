@@ -1,0 +1,52 @@
+// verify_kernels.cuh -- the sm_100a verification kernels (declarations + launch params).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ssj_device.cuh"
+
+namespace ssjb {
+
+// Tile geometry of the load-balanced thread-per-pair kernel (strategy A).
+constexpr uint32_t kTile = 2048;           // candidate slots per CTA
+constexpr uint32_t kThreadsA = 256;        // threads per CTA (8 slots per thread)
+constexpr uint32_t kMaxTileSlices = 512;   // slices of one tile described in shared memory
+constexpr uint32_t kTileRCap = 4096;       // probe tokens staged in shared memory per tile
+
+// Everything a verification kernel needs. Device pointers only.
+struct KParams {
+    const uint32_t* tokens;  // padded CSR
+    const uint2* sets;       // {pos8, size}
+    uint32_t n_sets;
+    const uint32_t* C;       // candidate slots
+    uint64_t nC;
+    const uint32_t* C_O;     // (probe, end) pairs
+    uint32_t n_slices;
+    uint32_t* tile_first;        // [n_tiles + 1], first slice with end > t * kTile
+    uint32_t n_tiles;
+    PredDev pred;
+    uint8_t* flags;                 // Pairs mode (nullable)
+    uint32_t* res_slots;            // results mode (nullable)
+    uint32_t* res_ov;
+    unsigned long long* res_n;
+    uint64_t res_cap;
+    unsigned long long* acc;  // SSJ_RESULT_WORDS: count, err, stats[3]
+};
+
+enum OutKind : int { kOutCount = 0, kOutFlags = 1, kOutResults = 2 };
+
+// Launchers (stream-ordered, no synchronisation). Return cudaGetLastError().
+cudaError_t launch_prep(const KParams& p, cudaStream_t st);
+// Strategy A: tiles [tile_begin, tile_end)
+cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_begin,
+                         uint32_t tile_end, cudaStream_t st);
+// Strategy B: block of `threads` per probe slice
+cudaError_t launch_block(const KParams& p, int out, bool stats, uint32_t threads,
+                         cudaStream_t st);
+// Strategy C: groups of G lanes per pair, merge-path partitions with round-level exits
+cudaError_t launch_path(const KParams& p, int out, uint32_t group, cudaStream_t st);
+// Instrumentation: algorithmic bytes under the reference loop
+cudaError_t launch_bytes(const KParams& p, unsigned long long* d_bytes, cudaStream_t st);
+
+}  // namespace ssjb

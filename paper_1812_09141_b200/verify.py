@@ -1,0 +1,258 @@
+"""The B200 verification engine (mirror of proj/include/ssjoin/verify.hpp:241-351).
+
+`VerificationEngine` has the reference's constructor and `verify_chunk` surface; every
+call goes through the C ABI (include/ssjoin_b200.h) into the sm_100a kernels. There is no
+CPU path: constructing an engine without a CUDA device raises RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import Optional, Tuple
+
+import numpy as np
+
+from . import _native as N
+from .collection import CandidateChunk, Collection
+from .similarity import SimilarityPredicate
+
+
+class StrategyKind(IntEnum):
+    """verify.hpp:18"""
+    A = 0
+    B = 1
+    C = 2
+    Auto = 3
+
+
+class OutputMode(IntEnum):
+    """verify.hpp:31"""
+    Count = 0
+    Pairs = 1
+
+
+@dataclass
+class Strategy:
+    """verify.hpp:21-29"""
+    kind: StrategyKind = StrategyKind.Auto
+    group_size: int = 32
+
+    def validate(self) -> None:
+        s = N.ssj_strategy(int(self.kind), self.group_size)
+        N.check(N.lib().ssj_strategy_validate(C.byref(s)))
+
+
+@dataclass
+class VerificationOutput:
+    """verify.hpp:36-39: flags (Pairs mode, slot order = C order) + count."""
+    flags: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint8))
+    count: int = 0
+
+
+@dataclass
+class VerifyStats:
+    """verify.hpp:183-195 (accumulated across calls)."""
+    pairs_verified: int = 0
+    early_exit_prunes: int = 0
+    comparison_budget_violations: int = 0
+
+
+def _vp(a: Optional[np.ndarray]):
+    return C.c_void_p(a.ctypes.data) if a is not None and a.size else None
+
+
+class VerificationEngine:
+    """verify.hpp:241-351 on a B200.
+
+    VerificationEngine(collection, pred, mode, strategy[, device]) uploads the collection
+    once (padded CSR); verify_chunk(chunk[, pool, stats]) returns VerificationOutput with
+    byte-identical flags and the same count as the reference. `pool` is accepted for
+    signature parity and ignored (the grid replaces the WorkerPool).
+    """
+
+    def __init__(self, collection: Collection, pred: SimilarityPredicate, mode: OutputMode,
+                 strategy: Strategy, device: int = 0):
+        self._lib = N.lib()
+        self._h = C.c_void_p()
+        self.collection = collection
+        self.pred = pred
+        self.mode = OutputMode(mode)
+        p = pred._c()
+        s = N.ssj_strategy(int(strategy.kind), strategy.group_size)
+        tokens = collection.tokens if collection.tokens.size else np.zeros(1, np.uint32)
+        N.check(self._lib.ssj_engine_create(
+            C.byref(self._h), device, tokens.ctypes.data_as(N.u32p),
+            collection.offsets.ctypes.data_as(N.u32p), collection.size(), C.byref(p),
+            int(self.mode), C.byref(s)))
+        r = N.ssj_strategy()
+        N.check(self._lib.ssj_engine_strategy(self._h, C.byref(r)))
+        self._strategy = Strategy(StrategyKind(r.kind), r.group_size)
+        self.device = device
+
+    @classmethod
+    def from_device(cls, d_tokens: int, n_padded: int, d_sets: int, n_sets: int, n_tokens: int,
+                    pred: SimilarityPredicate, mode: OutputMode, strategy: Strategy,
+                    device: int = 0) -> "VerificationEngine":
+        """Engine over a collection already resident on `device` in the padded layout
+        (e.g. NCCL-broadcast from another rank's engine)."""
+        self = cls.__new__(cls)
+        self._lib = N.lib()
+        self._h = C.c_void_p()
+        self.collection = None
+        self.pred = pred
+        self.mode = OutputMode(mode)
+        p = pred._c()
+        s = N.ssj_strategy(int(strategy.kind), strategy.group_size)
+        N.check(self._lib.ssj_engine_create_from_device(
+            C.byref(self._h), device, C.c_void_p(d_tokens), n_padded, C.c_void_p(d_sets),
+            n_sets, n_tokens, C.byref(p), int(self.mode), C.byref(s)))
+        r = N.ssj_strategy()
+        N.check(self._lib.ssj_engine_strategy(self._h, C.byref(r)))
+        self._strategy = Strategy(StrategyKind(r.kind), r.group_size)
+        self.device = device
+        return self
+
+    def device_collection(self) -> Tuple[int, int, int]:
+        """(d_tokens, n_padded_tokens, d_sets) of the engine's resident collection."""
+        t, s = C.c_void_p(), C.c_void_p()
+        n = C.c_uint64()
+        N.check(self._lib.ssj_engine_device_collection(self._h, C.byref(t), C.byref(n),
+                                                       C.byref(s)))
+        return t.value, n.value, s.value
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.ssj_engine_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def strategy(self) -> Strategy:
+        """verify.hpp:255: the resolved strategy (never Auto)."""
+        return self._strategy
+
+    # -- the hot call ----------------------------------------------------------------
+    def verify_chunk(self, chunk: CandidateChunk, pool=None,
+                     stats: Optional[VerifyStats] = None,
+                     flags_out: Optional[np.ndarray] = None) -> VerificationOutput:
+        """verify.hpp:257-275. `flags_out` (optional, uint8[nC], e.g. pinned) receives the
+        flags in place instead of a fresh array."""
+        out = VerificationOutput()
+        nC = chunk.candidate_count()
+        flags = None
+        if self.mode == OutputMode.Pairs:
+            flags = flags_out if flags_out is not None else np.zeros(nC, np.uint8)
+            assert flags.size >= nC and flags.dtype == np.uint8
+        cnt = C.c_uint64()
+        st = N.ssj_stats()
+        N.check(self._lib.ssj_verify_chunk(self._h, _vp(chunk.C), nC, _vp(chunk.C_O),
+                                           chunk.C_O.size, _vp(flags) if nC else None,
+                                           C.byref(cnt), C.byref(st)))
+        if flags is not None:
+            out.flags = flags[:nC]
+        out.count = cnt.value
+        if stats is not None:
+            stats.pairs_verified += st.pairs_verified
+            stats.early_exit_prunes += st.early_exit_prunes
+            stats.comparison_budget_violations += st.comparison_budget_violations
+        return out
+
+    def submit_chunk(self, chunk: CandidateChunk, flags: Optional[np.ndarray] = None) -> int:
+        """Asynchronous half of verify_chunk (<= 2 in flight). Keep `chunk` and `flags`
+        alive until wait_chunk returns."""
+        t = C.c_uint64()
+        N.check(self._lib.ssj_submit_chunk(self._h, _vp(chunk.C), chunk.candidate_count(),
+                                           _vp(chunk.C_O), chunk.C_O.size, _vp(flags),
+                                           C.byref(t)))
+        return t.value
+
+    def wait_chunk(self, ticket: int, stats: Optional[VerifyStats] = None) -> int:
+        cnt = C.c_uint64()
+        st = N.ssj_stats()
+        N.check(self._lib.ssj_wait_chunk(self._h, ticket, C.byref(cnt), C.byref(st)))
+        if stats is not None:
+            stats.pairs_verified += st.pairs_verified
+            stats.early_exit_prunes += st.early_exit_prunes
+            stats.comparison_budget_violations += st.comparison_budget_violations
+        return cnt.value
+
+    def verify_chunk_results(self, chunk: CandidateChunk) -> Tuple[np.ndarray, np.ndarray]:
+        """Qualifying slots (ascending) and their true overlaps |r ∩ s|."""
+        nC = chunk.candidate_count()
+        slots = np.zeros(max(nC, 1), np.uint32)
+        ovs = np.zeros(max(nC, 1), np.uint32)
+        n = C.c_uint64()
+        N.check(self._lib.ssj_verify_chunk_results(self._h, _vp(chunk.C), nC, _vp(chunk.C_O),
+                                                   chunk.C_O.size, _vp(slots), _vp(ovs), nC,
+                                                   C.byref(n)))
+        return slots[: n.value], ovs[: n.value]
+
+    # -- device-resident (kernel-only) path --------------------------------------------
+    def verify_chunk_device(self, d_C: int, nC: int, d_C_O: int, nCO: int, d_flags: int,
+                            d_result: int, stream: int = 0) -> None:
+        """Enqueue verification of a device-resident chunk on `stream` (cudaStream_t as
+        int). d_result: device uint64[8] -> [count, error bits, stats...]."""
+        N.check(self._lib.ssj_verify_chunk_device(self._h, C.c_void_p(d_C), nC,
+                                                  C.c_void_p(d_C_O), nCO,
+                                                  C.c_void_p(d_flags) if d_flags else None,
+                                                  C.c_void_p(d_result),
+                                                  C.c_void_p(stream) if stream else None))
+
+    def launches_per_chunk(self, nC: int, nCO: int) -> int:
+        return self._lib.ssj_launches_per_chunk(self._h, nC, nCO)
+
+    def chunk_algorithmic_bytes_device(self, d_C: int, nC: int, d_C_O: int, nCO: int,
+                                       d_bytes: int, stream: int = 0) -> None:
+        N.check(self._lib.ssj_chunk_algorithmic_bytes_device(
+            self._h, C.c_void_p(d_C), nC, C.c_void_p(d_C_O), nCO, C.c_void_p(d_bytes),
+            C.c_void_p(stream) if stream else None))
+
+
+def result_error(words) -> None:
+    """Raise for the error bits of a device result block (ssj_verify_chunk_device)."""
+    bits = int(words[1])
+    if bits & 1:
+        raise IndexError("set index out of range")
+    if bits & 2:
+        raise ValueError("malformed C_O: end offsets decreasing or beyond C")
+
+
+def device_count() -> int:
+    return N.lib().ssj_device_count()
+
+
+class PinnedBuffer:
+    """Pinned host memory from ssj_host_alloc viewed as a numpy array."""
+
+    def __init__(self, nbytes: int):
+        self.ptr = N.lib().ssj_host_alloc(nbytes)
+        if not self.ptr:
+            raise MemoryError(N.last_error())
+        self.nbytes = nbytes
+
+    def view(self, dtype, count: int) -> np.ndarray:
+        arr_t = C.c_uint8 * self.nbytes
+        raw = np.frombuffer(arr_t.from_address(self.ptr), dtype=np.uint8)
+        return raw.view(dtype)[:count]
+
+    def close(self):
+        if self.ptr:
+            N.lib().ssj_host_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
