@@ -3,7 +3,7 @@
 # and the test-infrastructure oracle (oracle/Makefile).
 NVCC     ?= nvcc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS  := $(ARCH) -lineinfo -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 -Xcompiler -pthread
+NVFLAGS  := $(ARCH) -lineinfo -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 -Xcompiler -pthread $(NVFLAGS_EXTRA)
 CSRC     := paper_1812_09141_b200/csrc
 OBJDIR   := build/obj
 LIB      := paper_1812_09141_b200/libssjoin_b200.so

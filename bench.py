@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Benchmark: candidate pairs verified per second on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], the DBLP-like row): 1M synthetic sets, Zipf tokens over a
+7,200-token universe (frequency-coded, rare first), 40..120 distinct tokens per set (avg 80),
+1% near-duplicates; Jaccard 4/5; AllPairs candidates (the reference's generator,
+joiners.hpp:47-71, run in parallel on the host). A full 1M-set join at 0.8 produces ~5e9
+candidates, so one step verifies a fixed, stratified batch of it: `--windows` probe windows
+spread evenly over the collection (so the batch has the full join's mix of set sizes),
+~256M candidates = 1 GiB of C, i.e. one chunk at the paper's M_c regime (PAPER.md:827:
+M_c = 4 GB). The chunk is larger than L2 (126 MB), so no L2 flush is needed between steps.
+
+Arms:
+  value  kernel-only: chunk resident in HBM, ssj_verify_chunk_device per step (CUDA events on
+         the launching stream, max over ranks);
+  e2e    through the C ABI with host buffers: ssj_verify_chunk from pinned C/C_O, H2D + kernels
+         + D2H of the flags inside the timed region;
+  --impl reference: the reference's own VerificationEngine::verify_chunk (strategy A, all host
+         threads) compiled from its headers (oracle/_ref/libssjref.so), bounded sample per step.
+
+Multi-GPU (torchrun): weak scaling -- every rank verifies its own batch (different probe
+windows); the collection is uploaded by rank 0 and broadcast once over NVLink (NCCL); no
+collective in the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1812_09141_b200.parallel import broadcast_device_collection, shard_probe_windows  # noqa: E402
+
+WORKLOADS = {
+    # name: (synth kwargs, threshold, algorithm, description)
+    "cfg2": (dict(sets=1_000_000, min_size=40, max_size=120, universe=7200, zipf_tokens=True,
+                  token_skew=1.0, duplicate_fraction=0.01, max_edits=2, distinct_tokens=True),
+             (4, 5), "allpairs",
+             "DBLP-like Zipf self-join, 1M sets, avg 80 tokens, universe 7200, Jaccard 0.80"),
+    "cfg1": (dict(sets=100_000, min_size=5, max_size=15, universe=10_000, zipf_tokens=False,
+                  duplicate_fraction=0.10, max_edits=1, distinct_tokens=True),
+             (9, 10), "allpairs",
+             "uniform self-join, 100K sets, avg 10 tokens, 10K-token universe, Jaccard 0.9"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def build_batch(ssj, coll, pred, algorithm, rank, world, target, windows, threads):
+    """Stratified probe windows over the collection; rank r takes window offset r."""
+    n = coll.size()
+    alg = ssj.Algorithm.AllPairs if algorithm == "allpairs" else ssj.Algorithm.PPJoin
+    # calibrate the window width on a small probe sample
+    stride = n // windows
+    sample_w = max(1, min(64, stride // max(world, 1)))
+    cal = ssj.generate_candidates_windows(coll, pred, alg,
+                                          [(k * stride, k * stride + sample_w)
+                                           for k in range(windows)], threads)
+    per_probe = max(cal.C.size / (windows * sample_w), 1e-9)
+    width = int(min(stride // max(world, 1), max(1, target / (per_probe * windows))))
+    wins = shard_probe_windows(n, windows, width, rank, world)
+    chunk = ssj.generate_candidates_windows(coll, pred, alg, wins, threads)
+    return chunk, width
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.device),
+                                          f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                         capture_output=True, text=True, timeout=5).stdout
+                    f = [x.strip() for x in out.strip().split(",")]
+                    if len(f) >= 7:
+                        self.samples.append(f)
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def ncu_traffic(workload):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_reference_rate(coll, pred_t, chunk, sample, reps=3):
+    """The reference's verify_chunk (strategy A, all host threads) on the first `sample`
+    candidates (slice-aligned) of the batch. Returns (pairs/s, cores, kind, sample)."""
+    from oracle import pyoracle as po
+    CO = chunk.C_O.reshape(-1, 2)
+    k = int(np.searchsorted(CO[:, 1].astype(np.int64), sample, side="left")) + 1
+    k = min(k, CO.shape[0])
+    sub_CO = CO[:k].reshape(-1).copy()
+    nC = int(CO[k - 1, 1]) if k else 0
+    sub_C = chunk.C[:nC]
+    if po.ref_available():
+        R = po.Ref()
+        h = R.coll(coll.tokens, coll.offsets, coll.original_id)
+        workers = R.L.ref_hardware_concurrency()
+        pool = R.pool(workers)
+        sec, cnt = R.time_verify_chunk(h, pool, 0, pred_t[0], pred_t[1], 1, 0, 1, True, sub_C,
+                                       sub_CO, reps=reps)
+        return nC / sec, int(workers), "reference", nC, cnt
+    t0 = time.perf_counter()
+    res = po.verify_chunk(coll.tokens, coll.offsets, sub_C, sub_CO, po.pred(0, *pred_t))
+    sec = time.perf_counter() - t0
+    return nC / sec, 1, "port", nC, res["count"]
+
+
+def run_reference_arm(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    import paper_1812_09141_b200 as ssj
+    synth_kw, pred_t, algorithm, desc = WORKLOADS[args.workload]
+    coll = ssj.synth_collection(args.seed, ssj.SynthConfig(**synth_kw))
+    pred = ssj.jaccard(*pred_t)
+    chunk, width = build_batch(ssj, coll, pred, algorithm, 0, 1, args.ref_sample, args.windows,
+                               args.threads)
+    from oracle import pyoracle as po
+    if not po.ref_available():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libssjref.so missing (reference not built)"}))
+        return 0
+    R = po.Ref()
+    h = R.coll(coll.tokens, coll.offsets, coll.original_id)
+    workers = R.L.ref_hardware_concurrency()
+    pool = R.pool(workers)
+    for _ in range(args.warmup):
+        R.time_verify_chunk(h, pool, 0, pred_t[0], pred_t[1], 1, 0, 1, True, chunk.C, chunk.C_O,
+                            reps=1)
+    elapsed = 0.0
+    for _ in range(args.steps):  # each step: verify_chunk timed inside the reference shim
+        sec, cnt = R.time_verify_chunk(h, pool, 0, pred_t[0], pred_t[1], 1, 0, 1, True, chunk.C,
+                                       chunk.C_O, reps=1)
+        elapsed += sec
+    pairs = chunk.C.size * args.steps
+    value = pairs / elapsed
+    line = {
+        "impl": "reference", "metric": "candidate pairs verified/sec", "value": value,
+        "unit": "pairs/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": desc, "sample_candidates_per_step": int(chunk.C.size),
+                   "strategy": "A", "workers": int(workers)},
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": int(workers),
+                         "kind": "reference",
+                         "sample": f"{chunk.C.size} candidates of the {args.workload} batch"},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--candidates", type=float, default=256e6, help="candidates per step")
+    ap.add_argument("--windows", type=int, default=64)
+    ap.add_argument("--seed", type=int, default=1812)
+    ap.add_argument("--threads", type=int, default=0, help="host generator threads (0 = all)")
+    ap.add_argument("--strategy", default="Auto")
+    ap.add_argument("--group", type=int, default=32)
+    ap.add_argument("--cpu-sample", type=float, default=24e6)
+    ap.add_argument("--ref-sample", type=float, default=24e6)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.ref_sample = int(args.ref_sample)
+
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import paper_1812_09141_b200 as ssj
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    synth_kw, pred_t, algorithm, desc = WORKLOADS[args.workload]
+    t0 = time.perf_counter()
+    coll = ssj.synth_collection(args.seed, ssj.SynthConfig(**synth_kw))
+    pred = ssj.jaccard(*pred_t)
+    chunk, width = build_batch(ssj, coll, pred, algorithm, rank, world, args.candidates,
+                               args.windows, args.threads)
+    nC, nCO = chunk.C.size, chunk.C_O.size
+    log(f"[rank {rank}] collection {coll.size()} sets avg {coll.tokens.size / coll.size():.1f}; "
+        f"batch {nC} candidates in {nCO // 2} slices ({time.perf_counter() - t0:.1f}s setup)")
+
+    strategy = ssj.Strategy(ssj.StrategyKind[args.strategy], args.group)
+    mode = ssj.OutputMode.Pairs
+    bcast_ms = None
+    if world == 1:
+        eng = ssj.VerificationEngine(coll, pred, mode, strategy, device=local)
+    else:
+        # rank 0 uploads once; the padded device collection is broadcast over NVLink (NCCL)
+        eng0 = (ssj.VerificationEngine(coll, pred, mode, strategy, device=local)
+                if rank == 0 else None)
+        tb = time.perf_counter()
+        eng, keep = broadcast_device_collection(eng0, coll.size(), int(coll.tokens.size),
+                                                coll.offsets, pred, mode, strategy, local, rank)
+        bcast_ms = 1e3 * (time.perf_counter() - tb)
+    resolved = eng.strategy()
+
+    # ---- kernel-only arm ---------------------------------------------------------------
+    dC = torch.from_numpy(chunk.C.view(np.int32)).to(dev)
+    dCO = torch.from_numpy(chunk.C_O.view(np.int32)).to(dev)
+    dF = torch.empty(nC, dtype=torch.uint8, device=dev)
+    dR = torch.zeros(8, dtype=torch.int64, device=dev)
+    dB = torch.zeros(1, dtype=torch.int64, device=dev)
+    stream = torch.cuda.Stream(device=dev)  # a real stream handle (not the legacy default)
+    sp = stream.cuda_stream
+    torch.cuda.synchronize()
+    eng.chunk_algorithmic_bytes_device(dC.data_ptr(), nC, dCO.data_ptr(), nCO, dB.data_ptr(), sp)
+    torch.cuda.synchronize()
+    algo_bytes = int(dB.item())
+
+    def step():
+        eng.verify_chunk_device(dC.data_ptr(), nC, dCO.data_ptr(), nCO, dF.data_ptr(),
+                                dR.data_ptr(), sp)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    words = dR.cpu().numpy()
+    ssj.result_error(words)
+    count = int(words[0])
+
+    eng.set_profiling(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    kernel_ms, launches = eng.kernel_time()
+    eng.set_profiling(False)
+    if world > 1:
+        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+        tot = torch.tensor([float(nC)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        total_pairs = float(tot.item()) * args.steps
+    else:
+        total_pairs = float(nC) * args.steps
+    value = total_pairs / (elapsed_ms / 1e3)
+    kernel_avg_ms = kernel_ms / max(launches, 1)
+    peak, peak_src = measured_peaks()
+    achieved_gbs = algo_bytes / (kernel_avg_ms / 1e3) / 1e9
+
+    # ---- end-to-end arm: C ABI with pinned host buffers ---------------------------------
+    pc = ssj.PinnedBuffer(4 * nC + 64)
+    pco = ssj.PinnedBuffer(4 * nCO + 64)
+    pf = ssj.PinnedBuffer(nC + 64)
+    hC = pc.view(np.uint32, nC)
+    hC[:] = chunk.C
+    hCO = pco.view(np.uint32, nCO)
+    hCO[:] = chunk.C_O
+    hF = pf.view(np.uint8, nC)
+    host_chunk = ssj.CandidateChunk.__new__(ssj.CandidateChunk)
+    host_chunk.C, host_chunk.C_O = hC, hCO
+    eng.verify_chunk(host_chunk, flags_out=hF)  # warm-up
+    if world > 1:
+        dist.barrier()
+    te = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        out = eng.verify_chunk(host_chunk, flags_out=hF)
+    e2e_s = time.perf_counter() - te
+    assert out.count == count, (out.count, count)
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = (total_pairs / args.steps) * args.e2e_steps / e2e_s
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            rate, cores, kind, sample, _ = cpu_reference_rate(coll, pred_t, chunk,
+                                                              int(args.cpu_sample))
+            cpu = {"value": rate, "unit": "pairs/s", "cores": cores, "kind": kind,
+                   "sample": f"first {sample} candidates (slice-aligned) of the step's batch, "
+                             f"VerificationEngine strategy A, best of 3"}
+        except Exception as e:  # reported, never fatal
+            cpu = {"value": None, "unit": "pairs/s", "cores": 0, "kind": "unavailable",
+                   "sample": str(e)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": "candidate pairs verified/sec", "value": value, "unit": "pairs/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {
+                "workload": desc, "n_sets": coll.size(),
+                "avg_set_size": round(coll.tokens.size / coll.size(), 2),
+                "threshold": f"{pred_t[0]}/{pred_t[1]}", "algorithm": algorithm,
+                "candidates_per_step_per_gpu": int(nC), "slices_per_step": int(nCO // 2),
+                "probe_windows": args.windows, "window_width": int(width),
+                "qualifying_per_step": count, "mode": "pairs (flags)",
+                "strategy": f"{resolved.kind.name}/{resolved.group_size}",
+                "l2": f"inputs larger than L2: C = {4 * nC / 2**30:.2f} GiB per step",
+                "parallelism": f"probe-window shards x{world}, no data-path collective",
+                "collection_broadcast_ms": bcast_ms,
+            },
+            "roofline": {
+                "bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+                "frac": achieved_gbs / peak, "traffic": ncu_traffic(args.workload),
+                "kernel": "tile_kernel (strategy A)" if resolved.kind.name == "A" else
+                          f"strategy {resolved.kind.name} kernel",
+                "algorithmic_bytes_per_launch": algo_bytes,
+                "kernel_ms_avg": kernel_avg_ms, "peak_source": peak_src,
+                "kernel_share_of_step": kernel_ms / elapsed_ms if elapsed_ms else None,
+            },
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "pairs/s",
+                    "h2d_bytes_per_step": int(4 * nC + 4 * nCO),
+                    "d2h_bytes_per_step": int(nC + 64), "steps": args.e2e_steps,
+                    "path": "ssj_verify_chunk (C ABI) from pinned host buffers, flags D2H"},
+            "gpu_launches": int(args.steps * eng.launches_per_chunk(nC, nCO)),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -159,7 +159,7 @@ int ssj_verify_chunk_results(ssj_engine* e, const uint32_t* C, uint64_t nC,
  * Device-resident variant (kernel-only path; the chunk is already in HBM):
  * d_C, d_C_O, d_flags (nullable) are device pointers; d_result is a device array of
  * SSJ_RESULT_WORDS uint64 that the call zeroes and fills asynchronously on `stream`
- * (a cudaStream_t, NULL = the engine's compute stream):
+ * (a cudaStream_t; NULL = the legacy default stream, as in the CUDA runtime):
  *   [0] count  [1] error bits  [2..4] stats (pairs_verified, prunes, violations)
  * No host synchronisation; read d_result after the stream completes.
  */
@@ -171,6 +171,19 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC,
                             const uint32_t* d_C_O, uint64_t nCO, uint8_t* d_flags,
                             uint64_t* d_result, void* stream);
 
+/* Kernel timing on the launching stream (benchmark instrumentation): when enabled,
+ * ssj_verify_chunk_device brackets its verification kernel with CUDA events recorded on the
+ * caller's stream; ssj_engine_kernel_time synchronises on them and returns the summed
+ * kernel milliseconds and launch count since the last call (then resets). */
+int ssj_engine_set_profiling(ssj_engine* e, int enabled);
+int ssj_engine_kernel_time(ssj_engine* e, double* total_ms, uint64_t* launches);
+
+/* Copy the engine's device collection into caller-owned device buffers of the same device
+ * (d_tokens: n_padded_tokens u32, d_sets: 2*n_sets u32) on `stream`, e.g. to hand it to an
+ * NCCL broadcast. NULL stream = the legacy default stream. */
+int ssj_engine_export_collection(const ssj_engine* e, uint32_t* d_tokens, uint32_t* d_sets,
+                                 void* stream);
+
 /* Number of kernels ssj_verify_chunk_device launches for a chunk of this shape
  * (for launch accounting in benchmarks). */
 int ssj_launches_per_chunk(const ssj_engine* e, uint64_t nC, uint64_t nCO);
@@ -179,11 +192,121 @@ int ssj_launches_per_chunk(const ssj_engine* e, uint64_t nC, uint64_t nCO);
  * Instrumentation: algorithmic bytes of a device-resident chunk under the reference's
  * early-exit loop: sum over pairs of 4 + 8 + 1 + 4*min(j_exit+1, |s|)
  * plus over slices 8 + 8 + 4*|r|. Runs a replay kernel; result written to *d_bytes
- * (device u64) on `stream`.
+ * (device u64) on `stream` (NULL = the legacy default stream).
  */
 int ssj_chunk_algorithmic_bytes_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC,
                                        const uint32_t* d_C_O, uint64_t nCO,
                                        uint64_t* d_bytes, void* stream);
+
+/* ---- candidate generation (role H0; joiners.hpp:47-183) ------------------------------ */
+/* pipeline.hpp:25 Algorithm */
+typedef enum { SSJ_ALG_ALLPAIRS = 0, SSJ_ALG_PPJOIN = 1, SSJ_ALG_GROUPJOIN = 2 } ssj_algorithm;
+
+typedef struct ssj_candidates ssj_candidates;
+/*
+ * The candidate stream of probes [probe_begin, probe_end) as one unbounded chunk (C, C_O),
+ * identical batch for batch to the reference generators (allpairs_generate
+ * joiners.hpp:47-71, ppjoin_generate :75-102, groupjoin_generate :111-183). threads > 1
+ * runs AllPairs / PPJoin on that many host threads (0 = all); threads == 1 and GroupJoin
+ * follow the reference's sequential control flow. GroupJoin's intra-group pairs
+ * (:175-179) are returned separately as (a, b) host pairs.
+ */
+int ssj_generate_candidates(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_sets,
+                            const ssj_predicate* pred, int32_t algorithm, uint32_t probe_begin,
+                            uint32_t probe_end, uint32_t threads, ssj_candidates** out);
+/* Several probe windows (windows[2k], windows[2k+1]) = [lo, hi) concatenated in the given
+ * order into one chunk, sharing one static index (AllPairs / PPJoin). */
+int ssj_generate_candidates_windows(const uint32_t* tokens, const uint32_t* offsets,
+                                    uint32_t n_sets, const ssj_predicate* pred, int32_t algorithm,
+                                    const uint32_t* windows, uint32_t n_windows, uint32_t threads,
+                                    ssj_candidates** out);
+int ssj_candidates_sizes(const ssj_candidates* c, uint64_t* nC, uint64_t* nCO, uint64_t* n_host);
+int ssj_candidates_copy(const ssj_candidates* c, uint32_t* C, uint32_t* C_O, uint32_t* host_pairs);
+void ssj_candidates_free(ssj_candidates* c);
+
+/* ---- collections: synthetic benchmark data + precoded preprocessing ------------------- */
+typedef struct ssj_collection ssj_collection;
+typedef struct {
+    uint64_t seed;
+    uint32_t n_sets;
+    uint32_t min_size, max_size;
+    int32_t zipf_sizes;
+    double size_skew;
+    uint32_t universe;
+    int32_t zipf_tokens;
+    double token_skew;
+    double duplicate_fraction; /* chance a record is a near-copy of an earlier one */
+    uint32_t max_edits;        /* tokens replaced in a near-copy: uniform in [0, max_edits] */
+    int32_t distinct_tokens;   /* 1: draw `size` distinct tokens (post-dedup size == size) */
+    uint32_t threads;          /* 0 = all host threads; output does not depend on it */
+} ssj_synth_config;
+/* Synthetic records (oracle.hpp:71-125 knobs + near-duplicates), then preprocess_precoded
+ * ordering (collection.hpp:134-168). */
+int ssj_synth_collection(const ssj_synth_config* cfg, ssj_collection** out);
+/* preprocess_precoded (collection.hpp:134-168) of records rec_tokens[rec_offsets[i]..[i+1]). */
+int ssj_preprocess_precoded(const uint32_t* rec_tokens, const uint64_t* rec_offsets,
+                            uint64_t n_records, ssj_collection** out);
+int ssj_collection_sizes(const ssj_collection* c, uint64_t* n_sets, uint64_t* n_tokens,
+                         uint64_t* dropped_empty);
+int ssj_collection_copy(const ssj_collection* c, uint32_t* tokens, uint32_t* offsets,
+                        uint32_t* original_id);
+void ssj_collection_free(ssj_collection* c);
+
+/* ---- the join driver (pipeline.hpp:150-361, run_join) ------------------------------------ */
+/* PipelineConfig::chunk_observer (pipeline.hpp:42-43): called on the dispatcher thread
+ * for every verified chunk; flags is NULL in Count mode. */
+typedef void (*ssj_chunk_observer)(void* user, const uint32_t* C, uint64_t nC,
+                                   const uint32_t* C_O, uint64_t nCO, const uint8_t* flags,
+                                   uint64_t count);
+
+/* PipelineConfig (pipeline.hpp:36-51) + device knobs. */
+typedef struct {
+    int32_t algorithm;        /* default SSJ_ALG_PPJOIN */
+    int32_t mode;             /* default SSJ_MODE_COUNT */
+    uint64_t chunk_budget;    /* M_c bytes, default 64 MiB; UINT64_MAX = one chunk */
+    ssj_strategy strategy;    /* default {Auto, 32} */
+    uint32_t workers;         /* validated >= 1 like the reference; the grid replaces the pool */
+    int32_t device;           /* CUDA device of the verification engine */
+    uint32_t filter_threads;  /* H0 generation threads; 1 = the reference's sequential loop */
+    uint32_t reserved;
+    ssj_chunk_observer observer;
+    void* observer_user;
+} ssj_join_config;
+
+/* JoinReport (pipeline.hpp:63-75) + PhaseTimings (:53-58) + ours. */
+typedef struct {
+    uint64_t count;
+    uint64_t chunk_count;
+    uint64_t candidate_count;
+    uint64_t host_verified_pairs;
+    uint64_t max_live_candidate_bytes;
+    uint64_t pairs_verified;
+    uint64_t early_exit_prunes;
+    uint64_t comparison_budget_violations;
+    uint64_t n_pairs;
+    ssj_strategy resolved_strategy;
+    double filtering_ms;
+    double serialization_ms;  /* includes hand-off back-pressure, as in the reference */
+    double verification_ms;   /* dispatcher busy time in verify_chunk */
+    double join_ms;
+    double handoff_wait_ms;   /* ours: the part of serialization_ms spent blocked in put() */
+    double setup_ms;          /* ours: engine creation incl. the one-time collection upload
+                                 (before join_ms starts, like pipeline.hpp:314) */
+} ssj_join_report;
+
+typedef struct ssj_join_result ssj_join_result;
+/* Fills the reference's PipelineConfig defaults. */
+void ssj_join_config_init(ssj_join_config* cfg);
+/* run_join(collection, pred, config): H0 = caller thread (generation + serialization into
+ * pinned chunk buffers), H1 = dispatcher (ssj_verify_chunk on the GPU), H2 = pair decoding.
+ * original_id may be NULL (identity). */
+int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_sets,
+                 const uint32_t* original_id, const ssj_predicate* pred,
+                 const ssj_join_config* cfg, ssj_join_result** out);
+int ssj_join_result_report(const ssj_join_result* r, ssj_join_report* report);
+/* Result pairs (r_id, s_id), r_id > s_id, original ids, unsorted (like JoinReport::pairs). */
+int ssj_join_result_pairs(const ssj_join_result* r, uint32_t* pairs /* 2 * n_pairs */);
+void ssj_join_result_free(ssj_join_result* r);
 
 /* ---- pinned host buffers (ChunkBuilder storage; double-buffered by the driver) ------- */
 void* ssj_host_alloc(size_t bytes);

@@ -39,6 +39,35 @@ class ssj_stats(C.Structure):
                 ("comparison_budget_violations", C.c_uint64)]
 
 
+class ssj_synth_config(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("n_sets", C.c_uint32), ("min_size", C.c_uint32),
+                ("max_size", C.c_uint32), ("zipf_sizes", C.c_int32), ("size_skew", C.c_double),
+                ("universe", C.c_uint32), ("zipf_tokens", C.c_int32), ("token_skew", C.c_double),
+                ("duplicate_fraction", C.c_double), ("max_edits", C.c_uint32),
+                ("distinct_tokens", C.c_int32), ("threads", C.c_uint32)]
+
+
+OBSERVER = C.CFUNCTYPE(None, C.c_void_p, u32p, C.c_uint64, u32p, C.c_uint64, u8p, C.c_uint64)
+
+
+class ssj_join_config(C.Structure):
+    _fields_ = [("algorithm", C.c_int32), ("mode", C.c_int32), ("chunk_budget", C.c_uint64),
+                ("strategy", ssj_strategy), ("workers", C.c_uint32), ("device", C.c_int32),
+                ("filter_threads", C.c_uint32), ("reserved", C.c_uint32),
+                ("observer", OBSERVER), ("observer_user", C.c_void_p)]
+
+
+class ssj_join_report(C.Structure):
+    _fields_ = [("count", C.c_uint64), ("chunk_count", C.c_uint64),
+                ("candidate_count", C.c_uint64), ("host_verified_pairs", C.c_uint64),
+                ("max_live_candidate_bytes", C.c_uint64), ("pairs_verified", C.c_uint64),
+                ("early_exit_prunes", C.c_uint64), ("comparison_budget_violations", C.c_uint64),
+                ("n_pairs", C.c_uint64), ("resolved_strategy", ssj_strategy),
+                ("filtering_ms", C.c_double), ("serialization_ms", C.c_double),
+                ("verification_ms", C.c_double), ("join_ms", C.c_double),
+                ("handoff_wait_ms", C.c_double), ("setup_ms", C.c_double)]
+
+
 # name -> (restype, argtypes); every symbol declared in include/ssjoin_b200.h
 SIGNATURES = {
     "ssj_abi_version": (C.c_int, []),
@@ -66,8 +95,31 @@ SIGNATURES = {
                                            C.c_uint64, u64p]),
     "ssj_verify_chunk_device": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, vp, vp, vp]),
     "ssj_launches_per_chunk": (C.c_int, [vp, C.c_uint64, C.c_uint64]),
+    "ssj_engine_set_profiling": (C.c_int, [vp, C.c_int]),
+    "ssj_engine_kernel_time": (C.c_int, [vp, C.POINTER(C.c_double), u64p]),
+    "ssj_engine_export_collection": (C.c_int, [vp, vp, vp, vp]),
     "ssj_chunk_algorithmic_bytes_device": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, vp,
                                                      vp]),
+    "ssj_generate_candidates": (C.c_int, [u32p, u32p, C.c_uint32, C.POINTER(ssj_predicate),
+                                          C.c_int32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                          C.POINTER(vp)]),
+    "ssj_generate_candidates_windows": (C.c_int, [u32p, u32p, C.c_uint32,
+                                                  C.POINTER(ssj_predicate), C.c_int32, u32p,
+                                                  C.c_uint32, C.c_uint32, C.POINTER(vp)]),
+    "ssj_candidates_sizes": (C.c_int, [vp, u64p, u64p, u64p]),
+    "ssj_candidates_copy": (C.c_int, [vp, vp, vp, vp]),
+    "ssj_candidates_free": (None, [vp]),
+    "ssj_synth_collection": (C.c_int, [C.POINTER(ssj_synth_config), C.POINTER(vp)]),
+    "ssj_preprocess_precoded": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(vp)]),
+    "ssj_collection_sizes": (C.c_int, [vp, u64p, u64p, u64p]),
+    "ssj_collection_copy": (C.c_int, [vp, vp, vp, vp]),
+    "ssj_collection_free": (None, [vp]),
+    "ssj_join_config_init": (None, [C.POINTER(ssj_join_config)]),
+    "ssj_run_join": (C.c_int, [u32p, u32p, C.c_uint32, u32p, C.POINTER(ssj_predicate),
+                               C.POINTER(ssj_join_config), C.POINTER(vp)]),
+    "ssj_join_result_report": (C.c_int, [vp, C.POINTER(ssj_join_report)]),
+    "ssj_join_result_pairs": (C.c_int, [vp, vp]),
+    "ssj_join_result_free": (None, [vp]),
     "ssj_host_alloc": (vp, [C.c_size_t]),
     "ssj_host_free": (None, [vp]),
 }

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/ssjoin_b200.h"
+#include "host_common.hpp"
 #include "verify_kernels.cuh"
 
 using ssjb::KParams;
@@ -120,6 +121,10 @@ struct ChunkSlot {
 
 }  // namespace
 
+namespace ssjh {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace ssjh
+
 struct ssj_engine {
     int device = 0;
     ssj_predicate hpred{};
@@ -132,6 +137,8 @@ struct ssj_engine {
     uint32_t* d_tokens = nullptr;
     uint2* d_sets = nullptr;
     bool owns_collection = true;
+    uint32_t* d_req_tab = nullptr;  // Jaccard/Dice required overlap by |r|+|s|
+    uint32_t req_tab_n = 0;
     cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
     ChunkSlot slot[2];
     uint64_t next_ticket = 0;
@@ -148,6 +155,10 @@ struct ssj_engine {
     size_t res_cap = 0;
     size_t res_cap2 = 0;
     unsigned long long* d_res_n = nullptr;
+    // kernel timing (ssj_engine_set_profiling)
+    bool profiling = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+    size_t prof_used = 0;
 };
 
 namespace {
@@ -189,7 +200,27 @@ KParams base_params(const ssj_engine& e) {
     p.sets = e.d_sets;
     p.n_sets = e.n_sets;
     p.pred = e.pred;
+    p.req_tab = e.d_req_tab;
+    p.req_tab_n = e.req_tab_n;
     return p;
+}
+
+// Jaccard and Dice: equivalent_overlap depends on |r| + |s| only (similarity.hpp:113-118),
+// so the kernels read it from a table built here with the exact u128 formula.
+int build_req_table(ssj_engine& e, uint32_t max_size) {
+    if (e.hpred.function != SSJ_JACCARD && e.hpred.function != SSJ_DICE) return SSJ_OK;
+    const uint64_t n = 2ull * max_size + 1;
+    if (n > (1ull << 22)) return SSJ_OK;  // formula path for huge sets
+    std::vector<uint32_t> tab(n);
+    for (uint64_t sum = 0; sum < n; ++sum) {
+        const uint64_t req = ssj_equivalent_overlap(&e.hpred, sum, 0);
+        if (req > 0xFFFFFFFFull) return SSJ_OK;
+        tab[sum] = (uint32_t)req;
+    }
+    SSJ_CK(cudaMalloc(&e.d_req_tab, n * sizeof(uint32_t)));
+    SSJ_CK(cudaMemcpy(e.d_req_tab, tab.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    e.req_tab_n = (uint32_t)n;
+    return SSJ_OK;
 }
 
 // Upload helper: host -> device on stream st. Pinned memory goes straight to the DMA
@@ -571,6 +602,9 @@ int ssj_engine_create(ssj_engine** out, int device, const uint32_t* tokens, cons
         cudaMemcpy(e->d_sets, sets.data(), sets.size() * sizeof(uint2), cudaMemcpyHostToDevice) !=
             cudaSuccess)
         return cleanup(fail(SSJ_ERR_CUDA, "collection upload failed"));
+    uint32_t max_size = 0;
+    for (uint32_t i = 0; i < n_sets; ++i) max_size = std::max(max_size, offsets[i + 1] - offsets[i]);
+    if ((rc = build_req_table(*e, max_size))) return cleanup(rc);
     *out = e;
     return SSJ_OK;
 }
@@ -605,6 +639,20 @@ int ssj_engine_create_from_device(ssj_engine** out, int device, const uint32_t* 
         ssj_engine_destroy(e);
         return rc;
     }
+    if (n_sets && (e->hpred.function == SSJ_JACCARD || e->hpred.function == SSJ_DICE)) {
+        std::vector<uint2> sets(n_sets);
+        if (cudaMemcpy(sets.data(), d_sets, n_sets * sizeof(uint2), cudaMemcpyDeviceToHost) !=
+            cudaSuccess) {
+            ssj_engine_destroy(e);
+            return fail(SSJ_ERR_CUDA, "reading set descriptors failed");
+        }
+        uint32_t max_size = 0;
+        for (const auto& sd : sets) max_size = std::max(max_size, sd.y);
+        if ((rc = build_req_table(*e, max_size))) {
+            ssj_engine_destroy(e);
+            return rc;
+        }
+    }
     *out = e;
     return SSJ_OK;
 }
@@ -634,9 +682,14 @@ void ssj_engine_destroy(ssj_engine* e) {
         cudaFree(e->d_sets);
     }
     cudaFree(e->dev_tile);
+    cudaFree(e->d_req_tab);
     cudaFree(e->d_res_slots);
     cudaFree(e->d_res_ov);
     cudaFree(e->d_res_n);
+    for (auto& pe : e->prof_events) {
+        cudaEventDestroy(pe.first);
+        cudaEventDestroy(pe.second);
+    }
     if (e->s_comp) cudaStreamDestroy(e->s_comp);
     if (e->s_h2d) cudaStreamDestroy(e->s_h2d);
     if (e->s_d2h) cudaStreamDestroy(e->s_d2h);
@@ -734,7 +787,7 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
     if (rc) return rc;
     if (!d_result) return fail(SSJ_ERR_INVALID_ARGUMENT, "null d_result");
     DeviceScope ds(e->device);
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : e->s_comp;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
     const uint32_t n_slices = (uint32_t)(nCO / 2);
     const uint32_t n_tiles = (uint32_t)((nC + ssjb::kTile - 1) / ssjb::kTile);
     if ((rc = ensure_device(&e->dev_tile, &e->dev_tile_cap, (size_t)n_tiles + 1))) return rc;
@@ -750,7 +803,56 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
     const int out = (e->mode == SSJ_MODE_PAIRS && d_flags) ? ssjb::kOutFlags : ssjb::kOutCount;
     SSJ_CK(cudaMemsetAsync(d_result, 0, SSJ_RESULT_WORDS * sizeof(uint64_t), st));
     SSJ_CK(ssjb::launch_prep(p, st));
+    cudaEvent_t k0 = nullptr, k1 = nullptr;
+    if (e->profiling) {
+        if (e->prof_used == e->prof_events.size()) {
+            cudaEvent_t a, b;
+            SSJ_CK(cudaEventCreate(&a));
+            SSJ_CK(cudaEventCreate(&b));
+            e->prof_events.push_back({a, b});
+        }
+        k0 = e->prof_events[e->prof_used].first;
+        k1 = e->prof_events[e->prof_used].second;
+        ++e->prof_used;
+        SSJ_CK(cudaEventRecord(k0, st));
+    }
     SSJ_CK(launch_strategy(*e, p, out, 0, n_tiles, st));
+    if (k1) SSJ_CK(cudaEventRecord(k1, st));
+    return SSJ_OK;
+}
+
+int ssj_engine_set_profiling(ssj_engine* e, int enabled) {
+    if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
+    e->profiling = enabled != 0;
+    e->prof_used = 0;
+    return SSJ_OK;
+}
+
+int ssj_engine_kernel_time(ssj_engine* e, double* total_ms, uint64_t* launches) {
+    if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
+    DeviceScope ds(e->device);
+    double sum = 0;
+    for (size_t i = 0; i < e->prof_used; ++i) {
+        float ms = 0;
+        SSJ_CK(cudaEventSynchronize(e->prof_events[i].second));
+        SSJ_CK(cudaEventElapsedTime(&ms, e->prof_events[i].first, e->prof_events[i].second));
+        sum += ms;
+    }
+    if (total_ms) *total_ms = sum;
+    if (launches) *launches = e->prof_used;
+    e->prof_used = 0;
+    return SSJ_OK;
+}
+
+int ssj_engine_export_collection(const ssj_engine* e, uint32_t* d_tokens, uint32_t* d_sets,
+                                 void* stream) {
+    if (!e || !d_tokens || !d_sets) return fail(SSJ_ERR_INVALID_ARGUMENT, "null argument");
+    DeviceScope ds(e->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+    SSJ_CK(cudaMemcpyAsync(d_tokens, e->d_tokens, e->n_padded * sizeof(uint32_t),
+                           cudaMemcpyDeviceToDevice, st));
+    SSJ_CK(cudaMemcpyAsync(d_sets, e->d_sets, (size_t)std::max<uint32_t>(e->n_sets, 1) * sizeof(uint2),
+                           cudaMemcpyDeviceToDevice, st));
     return SSJ_OK;
 }
 
@@ -767,7 +869,7 @@ int ssj_chunk_algorithmic_bytes_device(ssj_engine* e, const uint32_t* d_C, uint6
     int rc = check_chunk_args(e, d_C, nC, d_C_O, nCO);
     if (rc) return rc;
     DeviceScope ds(e->device);
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : e->s_comp;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
     KParams p = base_params(*e);
     p.C = d_C;
     p.nC = nC;

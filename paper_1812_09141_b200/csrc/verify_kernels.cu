@@ -84,16 +84,6 @@ __device__ __forceinline__ bool verify_pair(const KParams& p, const uint32_t* r,
     return merge_thread<kOut == kOutResults>(r, m, s4, n, (uint32_t)req, w0, w1, ov);
 }
 
-__device__ __forceinline__ uint32_t upper_bound_smem(const uint32_t* a, uint32_t n, uint64_t key) {
-    uint32_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if ((uint64_t)a[mid] <= key) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
 // First slice e in [lo, hi) whose end offset (C_O[2e+1]) is > key.
 __device__ __forceinline__ uint32_t upper_bound_ends(const uint32_t* __restrict__ C_O,
                                                      uint32_t lo, uint32_t hi, uint64_t key) {
@@ -124,16 +114,100 @@ __global__ void prep_kernel(const KParams p) {
 }
 
 // ---------------------------------------------------------------------------------------
+// Required overlap: table lookup by |r| + |s| for Jaccard / Dice (the value depends on the
+// sum only; the table is filled on the host with the exact u128 formula), else the formula.
+__device__ __forceinline__ uint64_t required_of(const KParams& p, uint32_t m, uint32_t n) {
+    const uint32_t sum = m + n;
+    if (p.req_tab && sum < p.req_tab_n) return __ldg(p.req_tab + sum);
+    return dev_required(p.pred, m, n);
+}
+
+// Membership-bitmap verification of one pair against a probe whose tokens are a bitmap in
+// shared memory: word k = {bits of tokens lo + 32k .. lo + 32k + 31, #probe tokens below}.
+// The candidate is walked in blocks of 8 tokens (registers t[]); after each block the merge
+// position is known exactly -- j = tokens of s consumed, i = #probe tokens <= last token
+// (rank) -- so the reference's bound (verify.hpp:58) is evaluated at (i, j): sound, and the
+// verdict is bit-exact. No dependent load chain between the 8 tokens of a block.
+template <bool kFull>
+__device__ __forceinline__ bool verify_bitmap(const uint2* __restrict__ bm, uint32_t lo,
+                                              uint32_t nbits, uint32_t m,
+                                              const uint4* __restrict__ s4, uint32_t n,
+                                              uint32_t req, uint4 w0, uint4 w1,
+                                              uint32_t* ov_out) {
+    const uint32_t slack_r = m - req, slack_s = n - req;
+    uint32_t ov = 0, j = 0;
+    for (;;) {
+        const uint32_t t[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        const uint32_t cnt = min(8u, n - j);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t d = t[q] - lo;
+            const bool in = (uint32_t)q < cnt && d < nbits;
+            const uint32_t word = in ? bm[d >> 5].x : 0u;
+            ov += (word >> (d & 31)) & 1u;
+        }
+        j += cnt;
+        if (j >= n) break;  // s exhausted: the verdict is ov >= req
+        const uint32_t tl = t[7];  // cnt == 8 here (s not exhausted)
+        const uint32_t d = tl - lo;
+        uint32_t i;
+        if (tl < lo) {
+            i = 0;
+        } else if (d >= nbits) {
+            i = m;
+        } else {
+            const uint2 w = bm[d >> 5];
+            i = w.y + __popc(w.x & ((2u << (d & 31)) - 1u));
+        }
+        if (!kFull && ov >= req) break;
+        if (ov < req && (i - ov > slack_r || j - ov > slack_s)) {
+            if (kFull) *ov_out = 0;
+            return false;
+        }
+        w0 = __ldg(s4 + (j >> 2));
+        w1 = __ldg(s4 + (j >> 2) + 1);
+    }
+    if (kFull) *ov_out = ov >= req ? ov : 0;
+    return ov >= req;
+}
+
+// ---------------------------------------------------------------------------------------
 // Strategy A: load-balanced thread-per-pair over fixed slot tiles.
+//
+// A CTA owns kTile consecutive slots; thread t owns the kItems consecutive slots
+// slot0 + t*kItems + [0, kItems) ("blocked"): its C ids arrive in 16-byte loads, its flags
+// leave in one 8-byte store. The slot -> slice map of the tile is a block-wide inclusive
+// scan over "a slice ends here" marks. Per slice of the tile the probe is prepared once in
+// shared memory:
+//   * slices with >= kBitmapMinCands candidates in the tile get a membership bitmap with
+//     per-word ranks over the probe's token range (verify_bitmap: O(1) per candidate token,
+//     no merge with the probe at all);
+//   * the others get the probe's tokens staged (merge_thread, the sequential merge).
+// All gathers of a thread (set descriptor, first 32-byte sector of each candidate) are
+// issued before any verification starts.
+struct TileSlice {
+    uint32_t end;     // cumulative end offset in C
+    uint32_t rpos8;   // probe set position (8-token units)
+    uint32_t rsize;   // |r|
+    uint32_t rofs;    // staged probe tokens in sh_r, or kNoStage
+    uint32_t bofs;    // bitmap words in sh_bm, or kNoStage
+    uint32_t lo;      // bitmap base token (multiple of 32)
+    uint32_t nwords;  // bitmap words (probe token range / 32)
+    uint32_t pad;
+};
+
 template <int kOut, bool kStats>
-__global__ void __launch_bounds__(kThreadsA) tile_kernel(const KParams p, const uint32_t tile_begin) {
+__global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const KParams p, const uint32_t tile_begin) {
+    constexpr int kItems = kTile / kThreadsA;
+    constexpr int kSliceItems = kMaxTileSlices / kThreadsA;
+    static_assert(kSliceItems >= 1, "kMaxTileSlices >= kThreadsA");
+    static_assert(kTileBitmapWords * 2 >= kTile, "marks alias the bitmap region");
     using Scan = cub::BlockScan<uint32_t, kThreadsA>;
-    __shared__ uint32_t sh_end[kMaxTileSlices];
-    __shared__ uint32_t sh_rsize[kMaxTileSlices];
-    __shared__ uint32_t sh_rpos8[kMaxTileSlices];
-    __shared__ uint32_t sh_rofs[kMaxTileSlices];
+    __shared__ TileSlice sh_sl[kMaxTileSlices];
+    __shared__ __align__(16) uint2 sh_bm[kTileBitmapWords];  // also the slice-end marks
     __shared__ __align__(16) uint32_t sh_r[kTileRCap];
     __shared__ typename Scan::TempStorage scan_tmp;
+    uint32_t* sh_mark = reinterpret_cast<uint32_t*>(sh_bm);
 
     const uint32_t tile = tile_begin + blockIdx.x;
     const uint64_t slot0 = (uint64_t)tile * kTile;
@@ -141,6 +215,28 @@ __global__ void __launch_bounds__(kThreadsA) tile_kernel(const KParams p, const 
     const uint64_t slot1 = min(slot0 + (uint64_t)kTile, p.nC);
     const uint32_t e0 = p.tile_first[tile];
     const uint32_t tid = threadIdx.x;
+    const uint64_t my0 = slot0 + (uint64_t)tid * kItems;
+
+    // 1. this thread's candidate ids and their set descriptors (independent of the slices)
+    uint32_t cand[kItems];
+    if (my0 + kItems <= slot1 && ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0)) {
+        const uint4* c4 = reinterpret_cast<const uint4*>(p.C + my0);
+#pragma unroll
+        for (int q = 0; q < kItems / 4; ++q) {
+            const uint4 v = __ldg(c4 + q);
+            cand[4 * q] = v.x;
+            cand[4 * q + 1] = v.y;
+            cand[4 * q + 2] = v.z;
+            cand[4 * q + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) cand[q] = my0 + q < slot1 ? __ldg(p.C + my0 + q) : 0u;
+    }
+    uint2 sd[kItems];
+#pragma unroll
+    for (int q = 0; q < kItems; ++q)
+        sd[q] = cand[q] < p.n_sets ? __ldg(p.sets + cand[q]) : make_uint2(0, 0);
 
     uint32_t ns = 0;
     bool fast = false;
@@ -151,62 +247,148 @@ __global__ void __launch_bounds__(kThreadsA) tile_kernel(const KParams p, const 
         fast = ns <= kMaxTileSlices;
     }
 
+    uint32_t li[kItems];  // tile-local slice of each item; ns = not covered
     if (fast) {
-        // Describe the tile's slices: end offset, probe size and position.
-        constexpr int kItems = kMaxTileSlices / kThreadsA;
-        uint32_t padded[kItems];
 #pragma unroll
-        for (int q = 0; q < kItems; ++q) {
-            const uint32_t k = tid * kItems + q;
+        for (int q = 0; q < kItems; ++q) sh_mark[tid * kItems + q] = 0;
+        __syncthreads();
+        uint32_t padded[kSliceItems], words[kSliceItems];
+#pragma unroll
+        for (int q = 0; q < kSliceItems; ++q) {
+            const uint32_t k = tid * kSliceItems + q;
             padded[q] = 0;
+            words[q] = 0;
             if (k < ns) {
                 const size_t e = (size_t)e0 + k;
                 const uint32_t probe = __ldg(p.C_O + 2 * e);
-                sh_end[k] = __ldg(p.C_O + 2 * e + 1);
+                const uint32_t end = __ldg(p.C_O + 2 * e + 1);
+                const uint32_t begin = e ? __ldg(p.C_O + 2 * e - 1) : 0u;
                 const uint2 rd = probe < p.n_sets ? __ldg(p.sets + probe) : make_uint2(0, 0);
-                sh_rsize[k] = rd.y;
-                sh_rpos8[k] = rd.x;
-                padded[q] = (rd.y + 7u) & ~7u;
+                TileSlice ts;
+                ts.end = end;
+                ts.rpos8 = rd.x;
+                ts.rsize = rd.y;
+                ts.lo = 0;
+                ts.nwords = 0;
+                const uint64_t cb = max((uint64_t)begin, slot0), ce = min((uint64_t)end, slot1);
+                const uint32_t cands = ce > cb ? (uint32_t)(ce - cb) : 0u;
+                if (rd.y && cands >= kBitmapMinCands) {
+                    const uint32_t* r = p.tokens + (size_t)rd.x * 8;
+                    const uint32_t first = __ldg(r), last = __ldg(r + rd.y - 1);
+                    ts.lo = first & ~31u;
+                    words[q] = ((last - ts.lo) >> 5) + 1;
+                    if (words[q] > kTileBitmapWords) words[q] = 0;
+                    ts.nwords = words[q];
+                }
+                if (!words[q]) padded[q] = (rd.y + 7u) & ~7u;
+                sh_sl[k] = ts;
+                if ((uint64_t)end > slot0 && (uint64_t)end < slot1) atomicAdd(&sh_mark[end - slot0], 1u);
             }
         }
-        uint32_t ofs[kItems];
-        Scan(scan_tmp).ExclusiveSum(padded, ofs);
+        uint32_t rofs[kSliceItems], bofs[kSliceItems];
+        Scan(scan_tmp).ExclusiveSum(padded, rofs);
+        __syncthreads();
+        Scan(scan_tmp).ExclusiveSum(words, bofs);
 #pragma unroll
-        for (int q = 0; q < kItems; ++q) {
-            const uint32_t k = tid * kItems + q;
-            if (k < ns) sh_rofs[k] = (ofs[q] + padded[q] <= kTileRCap) ? ofs[q] : kNoStage;
+        for (int q = 0; q < kSliceItems; ++q) {
+            const uint32_t k = tid * kSliceItems + q;
+            if (k < ns) {
+                sh_sl[k].rofs = (padded[q] && rofs[q] + padded[q] <= kTileRCap) ? rofs[q] : kNoStage;
+                sh_sl[k].bofs = (words[q] && bofs[q] + words[q] <= kTileBitmapWords) ? bofs[q] : kNoStage;
+            }
         }
         __syncthreads();
-        // Stage the probes that fit: one warp per slice, 16-byte vector copies.
+        uint32_t marks[kItems];
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) marks[q] = sh_mark[tid * kItems + q];
+        __syncthreads();  // scan_tmp reuse
+        Scan(scan_tmp).InclusiveSum(marks, li);
+        __syncthreads();  // marks consumed: the region becomes the bitmaps
+        for (uint32_t w = tid; w < kTileBitmapWords; w += kThreadsA) sh_bm[w] = make_uint2(0, 0);
+        // Stage probes that merge: one warp per slice, 16-byte vector copies.
         const uint32_t warp = tid >> 5, lane = tid & 31;
         for (uint32_t k = warp; k < ns; k += kThreadsA / 32) {
-            const uint32_t o = sh_rofs[k];
+            const uint32_t o = sh_sl[k].rofs;
             if (o == kNoStage) continue;
-            const uint4* src = reinterpret_cast<const uint4*>(p.tokens + (size_t)sh_rpos8[k] * 8);
+            const uint4* src = reinterpret_cast<const uint4*>(p.tokens + (size_t)sh_sl[k].rpos8 * 8);
             uint4* dst = reinterpret_cast<uint4*>(sh_r + o);
-            const uint32_t units = ((sh_rsize[k] + 7u) & ~7u) >> 2;
+            const uint32_t units = ((sh_sl[k].rsize + 7u) & ~7u) >> 2;
             for (uint32_t u = lane; u < units; u += 32) dst[u] = __ldg(src + u);
         }
         __syncthreads();
+        // Bitmaps: set the probe's bits ...
+        for (uint32_t k = 0; k < ns; ++k) {
+            const uint32_t bo = sh_sl[k].bofs;
+            if (bo == kNoStage) continue;
+            const uint32_t* r = p.tokens + (size_t)sh_sl[k].rpos8 * 8;
+            const uint32_t lo = sh_sl[k].lo;
+            for (uint32_t u = tid; u < sh_sl[k].rsize; u += kThreadsA) {
+                const uint32_t d = __ldg(r + u) - lo;
+                atomicOr(&sh_bm[bo + (d >> 5)].x, 1u << (d & 31));
+            }
+        }
+        __syncthreads();
+        // ... then the per-word ranks (one warp per bitmap slice, warp-wide scans)
+        for (uint32_t k = warp; k < ns; k += kThreadsA / 32) {
+            const uint32_t bo = sh_sl[k].bofs;
+            if (bo == kNoStage) continue;
+            const uint32_t nw = sh_sl[k].nwords;
+            uint32_t carry = 0;
+            for (uint32_t base = 0; base < nw; base += 32) {
+                const uint32_t w = base + lane;
+                const uint32_t c = w < nw ? __popc(sh_bm[bo + w].x) : 0u;
+                uint32_t incl = c;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+                    if (lane >= (uint32_t)off) incl += v;
+                }
+                if (w < nw) sh_bm[bo + w].y = carry + incl - c;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+        __syncthreads();
+    } else {
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) li[q] = 0;
     }
 
+    // 2. first 32-byte sector of the first candidate; the loop below prefetches item q+1's
+    //    sector before verifying item q
+    uint4 nw0, nw1;
+    {
+        const uint4* s4 = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[0].x * 8);
+        nw0 = __ldg(s4);
+        nw1 = __ldg(s4 + 1);
+    }
+
+    // 3. verification
     unsigned count = 0, prunes = 0, verified = 0;
-#pragma unroll 1
-    for (uint32_t it = 0; it < kTile / kThreadsA; ++it) {
-        const uint64_t slot = slot0 + (uint64_t)it * kThreadsA + tid;
+    uint32_t flag_bits[2] = {0, 0};
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+        const uint64_t slot = my0 + q;
+        const uint4 cw0 = nw0, cw1 = nw1;
+        if (q + 1 < kItems) {
+            const uint4* s4n = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[q + 1].x * 8);
+            nw0 = __ldg(s4n);
+            nw1 = __ldg(s4n + 1);
+        }
         bool met = false;
         uint32_t ov = 0;
         if (slot < slot1 && e0 < p.n_slices) {
             const uint32_t* r = nullptr;
-            uint32_t m = 0;
+            uint32_t m = 0, bofs = kNoStage, lo = 0, nbits = 0;
             bool covered;
             if (fast) {
-                const uint32_t li = upper_bound_smem(sh_end, ns, slot);
-                covered = li < ns;
+                covered = li[q] < ns;
                 if (covered) {
-                    m = sh_rsize[li];
-                    const uint32_t o = sh_rofs[li];
-                    r = o != kNoStage ? sh_r + o : p.tokens + (size_t)sh_rpos8[li] * 8;
+                    const TileSlice& ts = sh_sl[li[q]];
+                    m = ts.rsize;
+                    bofs = ts.bofs;
+                    lo = ts.lo;
+                    nbits = ts.nwords * 32;
+                    r = ts.rofs != kNoStage ? sh_r + ts.rofs : p.tokens + (size_t)ts.rpos8 * 8;
                 }
             } else {
                 const uint32_t e = upper_bound_ends(p.C_O, e0, p.n_slices, slot);
@@ -219,17 +401,45 @@ __global__ void __launch_bounds__(kThreadsA) tile_kernel(const KParams p, const 
                 }
             }
             if (covered) {
-                uint32_t n = 0;
-                met = verify_pair<kOut>(p, r, m, __ldg(p.C + slot), &ov, &n);
-                if (kStats) {
-                    ++verified;
-                    prunes += (!met && (m + n) > 0);
+                if (cand[q] >= p.n_sets) {
+                    flag_error(p.acc, kErrOutOfRange);
+                } else {
+                    const uint32_t n = sd[q].y;
+                    const uint4* s4 = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[q].x * 8);
+                    const uint64_t req = required_of(p, m, n);
+                    if (req == 0) {
+                        met = true;  // verify.hpp:57: no comparison, met = (0 >= 0)
+                        if (kOut == kOutResults)
+                            ov = full_overlap_seq(r, m, reinterpret_cast<const uint32_t*>(s4), n);
+                    } else if (req <= (uint64_t)min(m, n)) {
+                        if (bofs != kNoStage) {
+                            met = verify_bitmap<kOut == kOutResults>(sh_bm + bofs, lo, nbits, m, s4,
+                                                                     n, (uint32_t)req, cw0, cw1,
+                                                                     &ov);
+                        } else {
+                            met = merge_thread<kOut == kOutResults>(r, m, s4, n, (uint32_t)req,
+                                                                    cw0, cw1, &ov);
+                        }
+                    }
+                    if (kStats) {
+                        ++verified;
+                        prunes += (!met && (m + n) > 0);
+                    }
                 }
             }
-            if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
         }
         count += met;
+        flag_bits[q >> 2] |= (met ? 1u : 0u) << (8 * (q & 3));
         if (kOut == kOutResults) warp_append(p, met, slot, ov);
+    }
+    if (kOut == kOutFlags) {
+        if (my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 7) == 0) {
+            *reinterpret_cast<uint2*>(p.flags + my0) = make_uint2(flag_bits[0], flag_bits[1]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < kItems; ++q)
+                if (my0 + q < slot1) p.flags[my0 + q] = (flag_bits[q >> 2] >> (8 * (q & 3))) & 1u;
+        }
     }
     acc_add(p.acc, 0, count);
     if (kStats) {

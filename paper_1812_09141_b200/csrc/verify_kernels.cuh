@@ -9,10 +9,22 @@
 namespace ssjb {
 
 // Tile geometry of the load-balanced thread-per-pair kernel (strategy A).
-constexpr uint32_t kTile = 2048;           // candidate slots per CTA
-constexpr uint32_t kThreadsA = 256;        // threads per CTA (8 slots per thread)
+#ifndef SSJB_TILE_THREADS
+#define SSJB_TILE_THREADS 256
+#endif
+#ifndef SSJB_TILE_ITEMS
+#define SSJB_TILE_ITEMS 8
+#endif
+#ifndef SSJB_TILE_MIN_BLOCKS
+#define SSJB_TILE_MIN_BLOCKS 4
+#endif
+constexpr uint32_t kThreadsA = SSJB_TILE_THREADS;            // threads per CTA
+constexpr uint32_t kTile = SSJB_TILE_THREADS * SSJB_TILE_ITEMS;  // candidate slots per CTA
+constexpr int kTileMinBlocks = SSJB_TILE_MIN_BLOCKS;         // CTAs per SM (register cap)
 constexpr uint32_t kMaxTileSlices = 512;   // slices of one tile described in shared memory
-constexpr uint32_t kTileRCap = 4096;       // probe tokens staged in shared memory per tile
+constexpr uint32_t kTileRCap = 3072;       // probe tokens staged in shared memory per tile
+constexpr uint32_t kTileBitmapWords = 2048;  // {bits, rank} words of probe bitmaps per tile
+constexpr uint32_t kBitmapMinCands = 32;   // slices with fewer candidates in a tile merge
 
 // Everything a verification kernel needs. Device pointers only.
 struct KParams {
@@ -26,6 +38,8 @@ struct KParams {
     uint32_t* tile_first;        // [n_tiles + 1], first slice with end > t * kTile
     uint32_t n_tiles;
     PredDev pred;
+    const uint32_t* req_tab;        // Jaccard/Dice: required overlap by |r|+|s| (nullable)
+    uint32_t req_tab_n;
     uint8_t* flags;                 // Pairs mode (nullable)
     uint32_t* res_slots;            // results mode (nullable)
     uint32_t* res_ov;

@@ -209,6 +209,21 @@ class VerificationEngine:
                                                   C.c_void_p(d_result),
                                                   C.c_void_p(stream) if stream else None))
 
+    def set_profiling(self, enabled: bool) -> None:
+        N.check(self._lib.ssj_engine_set_profiling(self._h, int(enabled)))
+
+    def kernel_time(self) -> Tuple[float, int]:
+        """(summed verification-kernel ms, launches) since the last call (profiling on)."""
+        ms = C.c_double()
+        n = C.c_uint64()
+        N.check(self._lib.ssj_engine_kernel_time(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def export_collection(self, d_tokens: int, d_sets: int, stream: int = 0) -> None:
+        N.check(self._lib.ssj_engine_export_collection(
+            self._h, C.c_void_p(d_tokens), C.c_void_p(d_sets),
+            C.c_void_p(stream) if stream else None))
+
     def launches_per_chunk(self, nC: int, nCO: int) -> int:
         return self._lib.ssj_launches_per_chunk(self._h, nC, nCO)
 
