@@ -106,6 +106,12 @@ struct ChunkSlot {
     size_t capF = 0;
     uint32_t* dtile = nullptr;
     size_t capT = 0;
+    ssjb::SliceDesc* dslices = nullptr;
+    size_t capS = 0;
+    uint32_t* dbits = nullptr;
+    size_t capB = 0;
+    uint32_t* drank = nullptr;
+    size_t capR = 0;
     unsigned long long* dacc = nullptr;
     unsigned long long* hacc = nullptr;  // pinned mirror of dacc
     uint8_t* hflags = nullptr;           // pinned staging for pageable flag buffers
@@ -149,6 +155,12 @@ struct ssj_engine {
     // device-API scratch
     uint32_t* dev_tile = nullptr;
     size_t dev_tile_cap = 0;
+    ssjb::SliceDesc* dev_slices = nullptr;
+    size_t dev_slices_cap = 0;
+    uint32_t* dev_bits = nullptr;
+    size_t dev_bits_cap = 0;
+    uint32_t* dev_rank = nullptr;
+    size_t dev_rank_cap = 0;
     // results mode
     uint32_t* d_res_slots = nullptr;
     uint32_t* d_res_ov = nullptr;
@@ -249,6 +261,20 @@ int upload(ssj_engine& e, void* dst, const void* src, size_t bytes, cudaStream_t
     return SSJ_OK;
 }
 
+// Bitmap words reserved per chunk for strategy A's probe bitmaps (overflow falls back to
+// the merge path, so this only bounds memory, never correctness).
+uint64_t bitmap_words_for(uint64_t nC) { return std::max<uint64_t>(1ull << 20, nC / 8); }
+
+int ensure_tile_scratch(ssjb::SliceDesc** slices, size_t* capS, uint32_t** bits, size_t* capB,
+                        uint32_t** rank, size_t* capR, uint32_t n_slices, uint64_t nC) {
+    int rc;
+    if ((rc = ensure_device(slices, capS, std::max<size_t>(n_slices, 1)))) return rc;
+    const uint64_t words = bitmap_words_for(nC);
+    if ((rc = ensure_device(bits, capB, words))) return rc;
+    if ((rc = ensure_device(rank, capR, words))) return rc;
+    return SSJ_OK;
+}
+
 cudaError_t launch_strategy(const ssj_engine& e, const KParams& p, int out, uint32_t tile_begin,
                             uint32_t tile_end, cudaStream_t st) {
     const bool stats = e.strategy.kind != SSJ_STRATEGY_C;
@@ -287,6 +313,10 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
     if ((rc = ensure_device(&s.dCO, &s.capCO, (size_t)n_slices * 2))) return rc;
     if ((rc = ensure_device(&s.dtile, &s.capT, (size_t)n_tiles + 1))) return rc;
     if (out == ssjb::kOutFlags && (rc = ensure_device(&s.dflags, &s.capF, nC))) return rc;
+    const bool tiles = e.strategy.kind == SSJ_STRATEGY_A;
+    if (tiles && (rc = ensure_tile_scratch(&s.dslices, &s.capS, &s.dbits, &s.capB, &s.drank,
+                                           &s.capR, n_slices, nC)))
+        return rc;
     if (out == ssjb::kOutResults) {
         if ((rc = ensure_device(&e.d_res_slots, &e.res_cap, nC))) return rc;
         if ((rc = ensure_device(&e.d_res_ov, &e.res_cap2, nC))) return rc;
@@ -319,6 +349,12 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
     p.res_n = e.d_res_n;
     p.res_cap = nC;
     p.acc = s.dacc;
+    if (tiles) {
+        p.slices = s.dslices;
+        p.bm_bits = s.dbits;
+        p.bm_rank = s.drank;
+        p.bm_cap = bitmap_words_for(nC);
+    }
 
     int ev = 0;
     int turn = 0;
@@ -389,6 +425,9 @@ void destroy_slot(ChunkSlot& s) {
     cudaFree(s.dCO);
     cudaFree(s.dflags);
     cudaFree(s.dtile);
+    cudaFree(s.dslices);
+    cudaFree(s.dbits);
+    cudaFree(s.drank);
     cudaFree(s.dacc);
     cudaFreeHost(s.hacc);
     cudaFreeHost(s.hflags);
@@ -682,6 +721,9 @@ void ssj_engine_destroy(ssj_engine* e) {
         cudaFree(e->d_sets);
     }
     cudaFree(e->dev_tile);
+    cudaFree(e->dev_slices);
+    cudaFree(e->dev_bits);
+    cudaFree(e->dev_rank);
     cudaFree(e->d_req_tab);
     cudaFree(e->d_res_slots);
     cudaFree(e->d_res_ov);
@@ -791,6 +833,11 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
     const uint32_t n_slices = (uint32_t)(nCO / 2);
     const uint32_t n_tiles = (uint32_t)((nC + ssjb::kTile - 1) / ssjb::kTile);
     if ((rc = ensure_device(&e->dev_tile, &e->dev_tile_cap, (size_t)n_tiles + 1))) return rc;
+    const bool tiles = e->strategy.kind == SSJ_STRATEGY_A;
+    if (tiles && (rc = ensure_tile_scratch(&e->dev_slices, &e->dev_slices_cap, &e->dev_bits,
+                                           &e->dev_bits_cap, &e->dev_rank, &e->dev_rank_cap,
+                                           n_slices, nC)))
+        return rc;
     KParams p = base_params(*e);
     p.C = d_C;
     p.nC = nC;
@@ -800,6 +847,12 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
     p.n_tiles = n_tiles;
     p.flags = d_flags;
     p.acc = reinterpret_cast<unsigned long long*>(d_result);
+    if (tiles) {
+        p.slices = e->dev_slices;
+        p.bm_bits = e->dev_bits;
+        p.bm_rank = e->dev_rank;
+        p.bm_cap = bitmap_words_for(nC);
+    }
     const int out = (e->mode == SSJ_MODE_PAIRS && d_flags) ? ssjb::kOutFlags : ssjb::kOutCount;
     SSJ_CK(cudaMemsetAsync(d_result, 0, SSJ_RESULT_WORDS * sizeof(uint64_t), st));
     SSJ_CK(ssjb::launch_prep(p, st));
@@ -857,10 +910,11 @@ int ssj_engine_export_collection(const ssj_engine* e, uint32_t* d_tokens, uint32
 }
 
 int ssj_launches_per_chunk(const ssj_engine* e, uint64_t nC, uint64_t nCO) {
-    (void)e;
     (void)nC;
-    (void)nCO;
-    return 2;  // prep + one verification kernel (the memset is not a kernel of ours)
+    // prep (+ probe bitmaps for strategy A when there are slices) + one verification kernel;
+    // the memset of the result block is not a kernel of ours
+    if (e && e->strategy.kind == SSJ_STRATEGY_A && nCO >= 2) return 3;
+    return 2;
 }
 
 int ssj_chunk_algorithmic_bytes_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC,

@@ -25,7 +25,6 @@ namespace ssjb {
 
 namespace {
 
-constexpr uint32_t kNoStage = 0xFFFFFFFFu;
 
 __device__ __forceinline__ void acc_add(unsigned long long* acc, int word, unsigned v) {
     const unsigned w = __reduce_add_sync(0xffffffffu, v);
@@ -96,20 +95,86 @@ __device__ __forceinline__ uint32_t upper_bound_ends(const uint32_t* __restrict_
 }
 
 // ---------------------------------------------------------------------------------------
-// Prep: validate C_O (chunk.hpp:36-48 decode assumptions) and compute the first slice of
-// every tile. Thread idx handles slice idx and tile idx.
+// Prep: validate C_O (chunk.hpp:36-48 decode assumptions), compute the first slice of every
+// tile and -- for strategy A -- one descriptor per slice: probe position/size and, for slices
+// with >= kSliceBitmapMinCands candidates, a probe-bitmap allocation (global atomic bump).
+// Thread idx handles slice idx and tile idx.
 __global__ void prep_kernel(const KParams p) {
     const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx < p.n_slices) {
         const uint32_t end = p.C_O[2 * idx + 1];
         const uint32_t begin = idx ? p.C_O[2 * idx - 1] : 0;
+        const uint32_t probe = p.C_O[2 * idx];
         if (end < begin || (uint64_t)end > p.nC) flag_error(p.acc, kErrBadOffsets);
-        if (end > begin && p.C_O[2 * idx] >= p.n_sets) flag_error(p.acc, kErrOutOfRange);
+        if (end > begin && probe >= p.n_sets) flag_error(p.acc, kErrOutOfRange);
+        if (p.slices) {
+            uint4 d0 = make_uint4(end, 0, 0, kNone);
+            uint4 d1 = make_uint4(0, 0, 0, 0);
+            if (probe < p.n_sets) {
+                const uint2 rd = p.sets[probe];
+                d0.y = rd.x;
+                d0.z = rd.y;
+                if (p.bm_cap && rd.y && end >= begin && end - begin >= kSliceBitmapMinCands) {
+                    const uint32_t* r = p.tokens + (size_t)rd.x * 8;
+                    const uint32_t lo = r[0] & ~31u;
+                    const uint32_t nw = ((r[rd.y - 1] - lo) >> 5) + 1;
+                    if (nw <= kMaxBitmapWords) {
+                        const unsigned long long off = atomicAdd(p.acc + kAccBitmapWords, (unsigned long long)nw);
+                        if (off + nw <= p.bm_cap) {
+                            d0.w = (uint32_t)off;
+                            d1.x = lo;
+                            d1.y = nw;
+                        }
+                    }
+                }
+            }
+            uint4* dst = reinterpret_cast<uint4*>(p.slices + idx);
+            dst[0] = d0;
+            dst[1] = d1;
+        }
     }
     if (idx <= p.n_tiles) {
         p.tile_first[idx] = idx == p.n_tiles
                                 ? p.n_slices
                                 : upper_bound_ends(p.C_O, 0, p.n_slices, idx * (uint64_t)kTile);
+    }
+}
+
+// Probe bitmaps (one warp per slice): bits of the probe's tokens relative to `lo`, then the
+// number of probe tokens below every word (warp-wide exclusive scan).
+__global__ void bitmap_kernel(const KParams p) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t e = warp; e < p.n_slices; e += n_warps) {
+        const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(p.slices + e));
+        if (d0.w == kNone) continue;
+        const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(p.slices + e) + 1);
+        uint32_t* bits = p.bm_bits + d0.w;
+        uint32_t* rank = p.bm_rank + d0.w;
+        const uint32_t lo = d1.x, nw = d1.y;
+        for (uint32_t w = lane; w < nw; w += 32) bits[w] = 0;
+        __syncwarp();
+        const uint32_t* r = p.tokens + (size_t)d0.y * 8;
+        for (uint32_t u = lane; u < d0.z; u += 32) {
+            const uint32_t dd = __ldg(r + u) - lo;
+            atomicOr(bits + (dd >> 5), 1u << (dd & 31));
+        }
+        __threadfence_block();
+        __syncwarp();
+        uint32_t carry = 0;
+        for (uint32_t base = 0; base < nw; base += 32) {
+            const uint32_t w = base + lane;
+            const uint32_t c = w < nw ? __popc(__ldcg(bits + w)) : 0u;
+            uint32_t incl = c;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= (uint32_t)off) incl += v;
+            }
+            if (w < nw) rank[w] = carry + incl - c;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
     }
 }
 
@@ -122,14 +187,15 @@ __device__ __forceinline__ uint64_t required_of(const KParams& p, uint32_t m, ui
     return dev_required(p.pred, m, n);
 }
 
-// Membership-bitmap verification of one pair against a probe whose tokens are a bitmap in
-// shared memory: word k = {bits of tokens lo + 32k .. lo + 32k + 31, #probe tokens below}.
-// The candidate is walked in blocks of 8 tokens (registers t[]); after each block the merge
-// position is known exactly -- j = tokens of s consumed, i = #probe tokens <= last token
-// (rank) -- so the reference's bound (verify.hpp:58) is evaluated at (i, j): sound, and the
-// verdict is bit-exact. No dependent load chain between the 8 tokens of a block.
+// Membership-bitmap verification of one pair: bits[k] holds probe tokens lo+32k..lo+32k+31,
+// rank[k] the number of probe tokens below lo+32k (shared or global memory). The candidate
+// is walked in blocks of 8 tokens (registers); after each block the merge position is known
+// exactly -- j = candidate tokens consumed, i = #probe tokens <= the block's last token -- so
+// the reference's bound (verify.hpp:58) is evaluated at (i, j): sound, and the verdict is
+// bit-exact. The 8 lookups of a block are independent (no dependent load chain).
 template <bool kFull>
-__device__ __forceinline__ bool verify_bitmap(const uint2* __restrict__ bm, uint32_t lo,
+__device__ __forceinline__ bool verify_bitmap(const uint32_t* __restrict__ bits,
+                                              const uint32_t* __restrict__ rank, uint32_t lo,
                                               uint32_t nbits, uint32_t m,
                                               const uint4* __restrict__ s4, uint32_t n,
                                               uint32_t req, uint4 w0, uint4 w1,
@@ -143,26 +209,27 @@ __device__ __forceinline__ bool verify_bitmap(const uint2* __restrict__ bm, uint
         for (int q = 0; q < 8; ++q) {
             const uint32_t d = t[q] - lo;
             const bool in = (uint32_t)q < cnt && d < nbits;
-            const uint32_t word = in ? bm[d >> 5].x : 0u;
+            const uint32_t word = in ? bits[d >> 5] : 0u;
             ov += (word >> (d & 31)) & 1u;
         }
         j += cnt;
         if (j >= n) break;  // s exhausted: the verdict is ov >= req
-        const uint32_t tl = t[7];  // cnt == 8 here (s not exhausted)
-        const uint32_t d = tl - lo;
-        uint32_t i;
-        if (tl < lo) {
-            i = 0;
-        } else if (d >= nbits) {
-            i = m;
-        } else {
-            const uint2 w = bm[d >> 5];
-            i = w.y + __popc(w.x & ((2u << (d & 31)) - 1u));
-        }
         if (!kFull && ov >= req) break;
-        if (ov < req && (i - ov > slack_r || j - ov > slack_s)) {
-            if (kFull) *ov_out = 0;
-            return false;
+        if (ov < req) {
+            const uint32_t tl = t[7];  // cnt == 8 here (s not exhausted)
+            const uint32_t d = tl - lo;
+            uint32_t i;
+            if (tl < lo) {
+                i = 0;
+            } else if (d >= nbits) {
+                i = m;
+            } else {
+                i = rank[d >> 5] + __popc(bits[d >> 5] & ((2u << (d & 31)) - 1u));
+            }
+            if (i - ov > slack_r || j - ov > slack_s) {
+                if (kFull) *ov_out = 0;
+                return false;
+            }
         }
         w0 = __ldg(s4 + (j >> 2));
         w1 = __ldg(s4 + (j >> 2) + 1);
@@ -177,23 +244,22 @@ __device__ __forceinline__ bool verify_bitmap(const uint2* __restrict__ bm, uint
 // A CTA owns kTile consecutive slots; thread t owns the kItems consecutive slots
 // slot0 + t*kItems + [0, kItems) ("blocked"): its C ids arrive in 16-byte loads, its flags
 // leave in one 8-byte store. The slot -> slice map of the tile is a block-wide inclusive
-// scan over "a slice ends here" marks. Per slice of the tile the probe is prepared once in
-// shared memory:
-//   * slices with >= kBitmapMinCands candidates in the tile get a membership bitmap with
-//     per-word ranks over the probe's token range (verify_bitmap: O(1) per candidate token,
-//     no merge with the probe at all);
-//   * the others get the probe's tokens staged (merge_thread, the sequential merge).
-// All gathers of a thread (set descriptor, first 32-byte sector of each candidate) are
-// issued before any verification starts.
+// scan over "a slice ends here" marks. Per slice of the tile:
+//   * a probe bitmap built once per chunk (bitmap_kernel) is used when the slice is long;
+//     with >= kTileBitmapMinCands candidates in this tile it is copied to shared memory,
+//     otherwise read through L1 -- O(1) per candidate token, no merge with the probe;
+//   * short slices get the probe's tokens staged in shared memory for the sequential merge.
+// Each thread's candidate descriptors are loaded up front and the first 32-byte sector of
+// candidate q+1 is in flight while candidate q is verified.
 struct TileSlice {
     uint32_t end;     // cumulative end offset in C
     uint32_t rpos8;   // probe set position (8-token units)
     uint32_t rsize;   // |r|
-    uint32_t rofs;    // staged probe tokens in sh_r, or kNoStage
-    uint32_t bofs;    // bitmap words in sh_bm, or kNoStage
-    uint32_t lo;      // bitmap base token (multiple of 32)
-    uint32_t nwords;  // bitmap words (probe token range / 32)
-    uint32_t pad;
+    uint32_t rofs;    // staged probe tokens in sh_r, or kNone
+    uint32_t gbofs;   // probe bitmap in global memory, or kNone
+    uint32_t lo;      // bitmap base token
+    uint32_t nwords;  // bitmap words
+    uint32_t sofs;    // bitmap copy in shared memory, or kNone
 };
 
 template <int kOut, bool kStats>
@@ -204,10 +270,11 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
     static_assert(kTileBitmapWords * 2 >= kTile, "marks alias the bitmap region");
     using Scan = cub::BlockScan<uint32_t, kThreadsA>;
     __shared__ TileSlice sh_sl[kMaxTileSlices];
-    __shared__ __align__(16) uint2 sh_bm[kTileBitmapWords];  // also the slice-end marks
+    __shared__ __align__(16) uint32_t sh_bits[kTileBitmapWords];
+    __shared__ __align__(16) uint32_t sh_rank[kTileBitmapWords];
     __shared__ __align__(16) uint32_t sh_r[kTileRCap];
     __shared__ typename Scan::TempStorage scan_tmp;
-    uint32_t* sh_mark = reinterpret_cast<uint32_t*>(sh_bm);
+    uint32_t* sh_mark = sh_bits;  // [kTile] marks alias bits+rank (consumed before the copy)
 
     const uint32_t tile = tile_begin + blockIdx.x;
     const uint64_t slot0 = (uint64_t)tile * kTile;
@@ -260,91 +327,59 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
             words[q] = 0;
             if (k < ns) {
                 const size_t e = (size_t)e0 + k;
-                const uint32_t probe = __ldg(p.C_O + 2 * e);
-                const uint32_t end = __ldg(p.C_O + 2 * e + 1);
+                const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(p.slices + e));
+                const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(p.slices + e) + 1);
                 const uint32_t begin = e ? __ldg(p.C_O + 2 * e - 1) : 0u;
-                const uint2 rd = probe < p.n_sets ? __ldg(p.sets + probe) : make_uint2(0, 0);
                 TileSlice ts;
-                ts.end = end;
-                ts.rpos8 = rd.x;
-                ts.rsize = rd.y;
-                ts.lo = 0;
-                ts.nwords = 0;
-                const uint64_t cb = max((uint64_t)begin, slot0), ce = min((uint64_t)end, slot1);
+                ts.end = d0.x;
+                ts.rpos8 = d0.y;
+                ts.rsize = d0.z;
+                ts.gbofs = d0.w;
+                ts.lo = d1.x;
+                ts.nwords = d1.y;
+                const uint64_t cb = max((uint64_t)begin, slot0), ce = min((uint64_t)d0.x, slot1);
                 const uint32_t cands = ce > cb ? (uint32_t)(ce - cb) : 0u;
-                if (rd.y && cands >= kBitmapMinCands) {
-                    const uint32_t* r = p.tokens + (size_t)rd.x * 8;
-                    const uint32_t first = __ldg(r), last = __ldg(r + rd.y - 1);
-                    ts.lo = first & ~31u;
-                    words[q] = ((last - ts.lo) >> 5) + 1;
-                    if (words[q] > kTileBitmapWords) words[q] = 0;
-                    ts.nwords = words[q];
+                if (d0.w != kNone) {
+                    if (cands >= kTileBitmapMinCands) words[q] = d1.y;
+                } else {
+                    padded[q] = (d0.z + 7u) & ~7u;
                 }
-                if (!words[q]) padded[q] = (rd.y + 7u) & ~7u;
                 sh_sl[k] = ts;
-                if ((uint64_t)end > slot0 && (uint64_t)end < slot1) atomicAdd(&sh_mark[end - slot0], 1u);
+                if ((uint64_t)d0.x > slot0 && (uint64_t)d0.x < slot1) atomicAdd(&sh_mark[d0.x - slot0], 1u);
             }
         }
-        uint32_t rofs[kSliceItems], bofs[kSliceItems];
+        uint32_t rofs[kSliceItems], sofs[kSliceItems];
         Scan(scan_tmp).ExclusiveSum(padded, rofs);
         __syncthreads();
-        Scan(scan_tmp).ExclusiveSum(words, bofs);
+        Scan(scan_tmp).ExclusiveSum(words, sofs);
 #pragma unroll
         for (int q = 0; q < kSliceItems; ++q) {
             const uint32_t k = tid * kSliceItems + q;
             if (k < ns) {
-                sh_sl[k].rofs = (padded[q] && rofs[q] + padded[q] <= kTileRCap) ? rofs[q] : kNoStage;
-                sh_sl[k].bofs = (words[q] && bofs[q] + words[q] <= kTileBitmapWords) ? bofs[q] : kNoStage;
+                sh_sl[k].rofs = (padded[q] && rofs[q] + padded[q] <= kTileRCap) ? rofs[q] : kNone;
+                sh_sl[k].sofs = (words[q] && sofs[q] + words[q] <= kTileBitmapWords) ? sofs[q] : kNone;
             }
         }
         __syncthreads();
         uint32_t marks[kItems];
 #pragma unroll
         for (int q = 0; q < kItems; ++q) marks[q] = sh_mark[tid * kItems + q];
-        __syncthreads();  // scan_tmp reuse
+        __syncthreads();  // scan_tmp reuse; marks consumed
         Scan(scan_tmp).InclusiveSum(marks, li);
-        __syncthreads();  // marks consumed: the region becomes the bitmaps
-        for (uint32_t w = tid; w < kTileBitmapWords; w += kThreadsA) sh_bm[w] = make_uint2(0, 0);
-        // Stage probes that merge: one warp per slice, 16-byte vector copies.
+        // Copy long slices' bitmaps and stage short slices' probes: one warp per slice.
         const uint32_t warp = tid >> 5, lane = tid & 31;
         for (uint32_t k = warp; k < ns; k += kThreadsA / 32) {
-            const uint32_t o = sh_sl[k].rofs;
-            if (o == kNoStage) continue;
-            const uint4* src = reinterpret_cast<const uint4*>(p.tokens + (size_t)sh_sl[k].rpos8 * 8);
-            uint4* dst = reinterpret_cast<uint4*>(sh_r + o);
-            const uint32_t units = ((sh_sl[k].rsize + 7u) & ~7u) >> 2;
-            for (uint32_t u = lane; u < units; u += 32) dst[u] = __ldg(src + u);
-        }
-        __syncthreads();
-        // Bitmaps: set the probe's bits ...
-        for (uint32_t k = 0; k < ns; ++k) {
-            const uint32_t bo = sh_sl[k].bofs;
-            if (bo == kNoStage) continue;
-            const uint32_t* r = p.tokens + (size_t)sh_sl[k].rpos8 * 8;
-            const uint32_t lo = sh_sl[k].lo;
-            for (uint32_t u = tid; u < sh_sl[k].rsize; u += kThreadsA) {
-                const uint32_t d = __ldg(r + u) - lo;
-                atomicOr(&sh_bm[bo + (d >> 5)].x, 1u << (d & 31));
-            }
-        }
-        __syncthreads();
-        // ... then the per-word ranks (one warp per bitmap slice, warp-wide scans)
-        for (uint32_t k = warp; k < ns; k += kThreadsA / 32) {
-            const uint32_t bo = sh_sl[k].bofs;
-            if (bo == kNoStage) continue;
-            const uint32_t nw = sh_sl[k].nwords;
-            uint32_t carry = 0;
-            for (uint32_t base = 0; base < nw; base += 32) {
-                const uint32_t w = base + lane;
-                const uint32_t c = w < nw ? __popc(sh_bm[bo + w].x) : 0u;
-                uint32_t incl = c;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
-                    if (lane >= (uint32_t)off) incl += v;
+            const TileSlice ts = sh_sl[k];
+            if (ts.sofs != kNone) {
+                for (uint32_t w = lane; w < ts.nwords; w += 32) {
+                    sh_bits[ts.sofs + w] = __ldg(p.bm_bits + ts.gbofs + w);
+                    sh_rank[ts.sofs + w] = __ldg(p.bm_rank + ts.gbofs + w);
                 }
-                if (w < nw) sh_bm[bo + w].y = carry + incl - c;
-                carry += __shfl_sync(0xffffffffu, incl, 31);
+            } else if (ts.rofs != kNone) {
+                const uint4* src = reinterpret_cast<const uint4*>(p.tokens + (size_t)ts.rpos8 * 8);
+                uint4* dst = reinterpret_cast<uint4*>(sh_r + ts.rofs);
+                const uint32_t units = ((ts.rsize + 7u) & ~7u) >> 2;
+                for (uint32_t u = lane; u < units; u += 32) dst[u] = __ldg(src + u);
             }
         }
         __syncthreads();
@@ -378,17 +413,25 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
         uint32_t ov = 0;
         if (slot < slot1 && e0 < p.n_slices) {
             const uint32_t* r = nullptr;
-            uint32_t m = 0, bofs = kNoStage, lo = 0, nbits = 0;
+            const uint32_t* bits = nullptr;
+            const uint32_t* rank = nullptr;
+            uint32_t m = 0, lo = 0, nbits = 0;
             bool covered;
             if (fast) {
                 covered = li[q] < ns;
                 if (covered) {
                     const TileSlice& ts = sh_sl[li[q]];
                     m = ts.rsize;
-                    bofs = ts.bofs;
+                    if (ts.sofs != kNone) {
+                        bits = sh_bits + ts.sofs;
+                        rank = sh_rank + ts.sofs;
+                    } else if (ts.gbofs != kNone) {
+                        bits = p.bm_bits + ts.gbofs;
+                        rank = p.bm_rank + ts.gbofs;
+                    }
                     lo = ts.lo;
                     nbits = ts.nwords * 32;
-                    r = ts.rofs != kNoStage ? sh_r + ts.rofs : p.tokens + (size_t)ts.rpos8 * 8;
+                    r = ts.rofs != kNone ? sh_r + ts.rofs : p.tokens + (size_t)ts.rpos8 * 8;
                 }
             } else {
                 const uint32_t e = upper_bound_ends(p.C_O, e0, p.n_slices, slot);
@@ -412,10 +455,9 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
                         if (kOut == kOutResults)
                             ov = full_overlap_seq(r, m, reinterpret_cast<const uint32_t*>(s4), n);
                     } else if (req <= (uint64_t)min(m, n)) {
-                        if (bofs != kNoStage) {
-                            met = verify_bitmap<kOut == kOutResults>(sh_bm + bofs, lo, nbits, m, s4,
-                                                                     n, (uint32_t)req, cw0, cw1,
-                                                                     &ov);
+                        if (bits) {
+                            met = verify_bitmap<kOut == kOutResults>(bits, rank, lo, nbits, m, s4, n,
+                                                                     (uint32_t)req, cw0, cw1, &ov);
                         } else {
                             met = merge_thread<kOut == kOutResults>(r, m, s4, n, (uint32_t)req,
                                                                     cw0, cw1, &ov);
@@ -667,11 +709,18 @@ constexpr uint32_t kSliceRCap = 12288;  // tokens staged per CTA in strategies B
 
 }  // namespace
 
-cudaError_t launch_prep(const KParams& p, cudaStream_t st) {
+cudaError_t launch_prep(const KParams& p, cudaStream_t st, int* launches) {
     const uint64_t work = (uint64_t)max(p.n_slices, p.n_tiles + 1);
     const uint32_t threads = 256;
     const uint32_t grid = (uint32_t)((work + threads - 1) / threads);
     prep_kernel<<<grid ? grid : 1, threads, 0, st>>>(p);
+    int n = 1;
+    if (p.slices && p.bm_cap && p.n_slices) {
+        const uint64_t warps = p.n_slices < 148ull * 64 ? p.n_slices : 148ull * 64;
+        bitmap_kernel<<<(uint32_t)((warps * 32 + 255) / 256), 256, 0, st>>>(p);
+        ++n;
+    }
+    if (launches) *launches = n;
     return cudaGetLastError();
 }
 

@@ -16,15 +16,33 @@ namespace ssjb {
 #define SSJB_TILE_ITEMS 8
 #endif
 #ifndef SSJB_TILE_MIN_BLOCKS
-#define SSJB_TILE_MIN_BLOCKS 4
+#define SSJB_TILE_MIN_BLOCKS 3
 #endif
 constexpr uint32_t kThreadsA = SSJB_TILE_THREADS;            // threads per CTA
 constexpr uint32_t kTile = SSJB_TILE_THREADS * SSJB_TILE_ITEMS;  // candidate slots per CTA
 constexpr int kTileMinBlocks = SSJB_TILE_MIN_BLOCKS;         // CTAs per SM (register cap)
 constexpr uint32_t kMaxTileSlices = 512;   // slices of one tile described in shared memory
-constexpr uint32_t kTileRCap = 3072;       // probe tokens staged in shared memory per tile
-constexpr uint32_t kTileBitmapWords = 2048;  // {bits, rank} words of probe bitmaps per tile
-constexpr uint32_t kBitmapMinCands = 32;   // slices with fewer candidates in a tile merge
+constexpr uint32_t kTileRCap = 2048;       // probe tokens staged in shared memory per tile
+constexpr uint32_t kTileBitmapWords = 2048;  // bitmap words (bits + rank) copied to smem per tile
+constexpr uint32_t kSliceBitmapMinCands = 64;  // slices this long get a probe bitmap per chunk
+constexpr uint32_t kTileBitmapMinCands = 64;   // ... copied to smem when a tile has this many
+constexpr uint32_t kMaxBitmapWords = 8192;     // probe token range cap (256K tokens)
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+// Per-slice descriptor built once per chunk by prep_kernel (32 bytes, one sector).
+struct SliceDesc {
+    uint32_t end;     // cumulative end offset in C
+    uint32_t rpos8;   // probe set position (8-token units)
+    uint32_t rsize;   // |r|
+    uint32_t bofs;    // probe bitmap (bm_bits / bm_rank word offset) or kNone
+    uint32_t lo;      // bitmap base token (multiple of 32)
+    uint32_t nwords;  // bitmap words
+    uint32_t pad0, pad1;
+};
+
+// Result-block words (SSJ_RESULT_WORDS = 8): 0 count, 1 error bits, 2..4 stats,
+// 5 bitmap words allocated in this chunk.
+constexpr int kAccBitmapWords = 5;
 
 // Everything a verification kernel needs. Device pointers only.
 struct KParams {
@@ -40,6 +58,10 @@ struct KParams {
     PredDev pred;
     const uint32_t* req_tab;        // Jaccard/Dice: required overlap by |r|+|s| (nullable)
     uint32_t req_tab_n;
+    SliceDesc* slices;              // strategy A: per-slice descriptors (nullable otherwise)
+    uint32_t* bm_bits;              // probe membership bitmaps (word = 32 tokens)
+    uint32_t* bm_rank;              // probe tokens below each bitmap word
+    uint64_t bm_cap;                // bitmap words available (0 = no bitmaps)
     uint8_t* flags;                 // Pairs mode (nullable)
     uint32_t* res_slots;            // results mode (nullable)
     uint32_t* res_ov;
@@ -51,7 +73,9 @@ struct KParams {
 enum OutKind : int { kOutCount = 0, kOutFlags = 1, kOutResults = 2 };
 
 // Launchers (stream-ordered, no synchronisation). Return cudaGetLastError().
-cudaError_t launch_prep(const KParams& p, cudaStream_t st);
+// prep_kernel (+ bitmap_kernel when p.slices && p.bm_cap): validation, tile index, slice
+// descriptors and probe bitmaps. Returns the number of kernels launched through *launches.
+cudaError_t launch_prep(const KParams& p, cudaStream_t st, int* launches = nullptr);
 // Strategy A: tiles [tile_begin, tile_end)
 cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_begin,
                          uint32_t tile_end, cudaStream_t st);
