@@ -49,6 +49,20 @@ WORKLOADS = {
                   duplicate_fraction=0.10, max_edits=1, distinct_tokens=True),
              (9, 10), "allpairs",
              "uniform self-join, 100K sets, avg 10 tokens, 10K-token universe, Jaccard 0.9"),
+    "cfg3": (dict(sets=1_000_000, min_size=2, max_size=2500, zipf_sizes=True, size_skew=1.9,
+                  universe=41_000, zipf_tokens=True, token_skew=0.6, duplicate_fraction=0.05,
+                  max_edits=2),
+             (3, 4), "allpairs",
+             "KOSARAK-like sparse self-join, 1M sets, avg ~8 tokens, long tail, Jaccard 0.75"),
+    "cfg4": (dict(sets=250_000, min_size=1, max_size=20_000, zipf_sizes=True, size_skew=1.3,
+                  universe=200_000, zipf_tokens=True, token_skew=1.0, duplicate_fraction=0.02,
+                  max_edits=3),
+             (3, 5), "allpairs",
+             "ENRON/ORKUT-like long-set self-join, 250K sets, avg ~180 tokens, max >10K, Jaccard 0.6"),
+    "cfg5": (dict(sets=550_000, min_size=40, max_size=120, universe=7200, zipf_tokens=True,
+                  token_skew=1.0, duplicate_fraction=0.01, max_edits=2, distinct_tokens=True),
+             (4, 5), "allpairs",
+             "~1B-candidate DBLP-like Zipf join, 550K sets, Jaccard 0.8 (probe-sharded)"),
 }
 
 
@@ -65,6 +79,11 @@ def build_batch(ssj, coll, pred, algorithm, rank, world, target, windows, thread
     """Stratified probe windows over the collection; rank r takes window offset r."""
     n = coll.size()
     alg = ssj.Algorithm.AllPairs if algorithm == "allpairs" else ssj.Algorithm.PPJoin
+    if target <= 0:  # the whole join's candidate stream
+        chunk = ssj.generate_candidates_windows(coll, pred, alg,
+                                                shard_probe_windows(n, world, n, rank, world)
+                                                if world > 1 else [(0, n)], threads)
+        return chunk, n
     # calibrate the window width on a small probe sample
     stride = n // windows
     sample_w = max(1, min(64, stride // max(world, 1)))
@@ -123,6 +142,25 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.samples)}
+
+
+def measure_l2_read_gbs(dev, mib=48, reps=50):
+    """L2-resident read bandwidth: a float32 reduction over a 48 MiB buffer (fits the 126 MB
+    L2), repeated; bytes read / CUDA-event time. The reference figure for working sets that
+    stay in L2."""
+    import torch
+    x = torch.ones(mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
+    for _ in range(5):
+        x.sum()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        x.sum()
+    e1.record()
+    torch.cuda.synchronize()
+    return x.numel() * 4 * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
 
 
 def measured_peaks():
@@ -223,7 +261,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
-    ap.add_argument("--candidates", type=float, default=256e6, help="candidates per step")
+    ap.add_argument("--candidates", type=float, default=None,
+                    help="candidates per step (default: 256M for cfg2/cfg5, the whole join "
+                         "for the smaller configs)")
     ap.add_argument("--windows", type=int, default=64)
     ap.add_argument("--seed", type=int, default=1812)
     ap.add_argument("--threads", type=int, default=0, help="host generator threads (0 = all)")
@@ -235,6 +275,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.ref_sample = int(args.ref_sample)
+    if args.candidates is None:
+        args.candidates = 256e6 if args.workload in ("cfg2", "cfg5") else 0
 
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -328,6 +370,7 @@ def main():
     kernel_avg_ms = kernel_ms / max(launches, 1)
     peak, peak_src = measured_peaks()
     achieved_gbs = algo_bytes / (kernel_avg_ms / 1e3) / 1e9
+    l2_gbs = measure_l2_read_gbs(dev)
 
     # ---- end-to-end arm: C ABI with pinned host buffers ---------------------------------
     pc = ssj.PinnedBuffer(4 * nC + 64)
@@ -393,6 +436,9 @@ def main():
                 "algorithmic_bytes_per_launch": algo_bytes,
                 "kernel_ms_avg": kernel_avg_ms, "peak_source": peak_src,
                 "kernel_share_of_step": kernel_ms / elapsed_ms if elapsed_ms else None,
+                "l2": {"peak": l2_gbs, "unit": "GB/s", "frac": achieved_gbs / l2_gbs,
+                       "source": "measured in this run: float32 reduction over a 48 MiB "
+                                 "L2-resident buffer"},
             },
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "pairs/s",

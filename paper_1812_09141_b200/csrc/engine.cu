@@ -112,6 +112,9 @@ struct ChunkSlot {
     size_t capB = 0;
     uint32_t* drank = nullptr;
     size_t capR = 0;
+    uint32_t* ddefer = nullptr;          // long-pair slots (strategy A)
+    size_t capDf = 0;
+    unsigned long long* ddefer_n = nullptr;  // one counter per piece
     unsigned long long* dacc = nullptr;
     unsigned long long* hacc = nullptr;  // pinned mirror of dacc
     uint8_t* hflags = nullptr;           // pinned staging for pageable flag buffers
@@ -161,6 +164,9 @@ struct ssj_engine {
     size_t dev_bits_cap = 0;
     uint32_t* dev_rank = nullptr;
     size_t dev_rank_cap = 0;
+    uint32_t* dev_defer = nullptr;
+    size_t dev_defer_cap = 0;
+    unsigned long long* dev_defer_n = nullptr;
     // results mode
     uint32_t* d_res_slots = nullptr;
     uint32_t* d_res_ov = nullptr;
@@ -281,7 +287,11 @@ cudaError_t launch_strategy(const ssj_engine& e, const KParams& p, int out, uint
     switch (e.strategy.kind) {
         case SSJ_STRATEGY_B: return ssjb::launch_block(p, out, stats, e.strategy.group_size, st);
         case SSJ_STRATEGY_C: return ssjb::launch_path(p, out, e.strategy.group_size, st);
-        default: return ssjb::launch_tiles(p, out, stats, tile_begin, tile_end, st);
+        default: {
+            cudaError_t err = ssjb::launch_tiles(p, out, stats, tile_begin, tile_end, st);
+            if (err != cudaSuccess) return err;
+            return ssjb::launch_long(p, out, stats, st);
+        }
     }
 }
 
@@ -317,6 +327,7 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
     if (tiles && (rc = ensure_tile_scratch(&s.dslices, &s.capS, &s.dbits, &s.capB, &s.drank,
                                            &s.capR, n_slices, nC)))
         return rc;
+    if (tiles && (rc = ensure_device(&s.ddefer, &s.capDf, std::max<size_t>(nC, 1)))) return rc;
     if (out == ssjb::kOutResults) {
         if ((rc = ensure_device(&e.d_res_slots, &e.res_cap, nC))) return rc;
         if ((rc = ensure_device(&e.d_res_ov, &e.res_cap2, nC))) return rc;
@@ -359,6 +370,7 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
     int ev = 0;
     int turn = 0;
     SSJ_CK(cudaMemsetAsync(s.dacc, 0, SSJ_RESULT_WORDS * sizeof(unsigned long long), e.s_comp));
+    if (tiles) SSJ_CK(cudaMemsetAsync(s.ddefer_n, 0, kMaxPieces * sizeof(unsigned long long), e.s_comp));
     if (out == ssjb::kOutResults)
         SSJ_CK(cudaMemsetAsync(e.d_res_n, 0, sizeof(unsigned long long), e.s_comp));
     if ((rc = upload(e, s.dCO, C_O, (size_t)n_slices * 2 * sizeof(uint32_t), e.s_comp, co_pinned,
@@ -386,6 +398,12 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
         }
         const uint32_t t0 = (uint32_t)(lo / ssjb::kTile);
         const uint32_t t1 = (uint32_t)((hi + ssjb::kTile - 1) / ssjb::kTile);
+        if (tiles) {  // this piece's long pairs: their own segment and counter
+            const int pc = (int)(lo / piece);
+            p.defer = s.ddefer + lo;
+            p.defer_n = s.ddefer_n + pc;
+            p.defer_cap = hi - lo;
+        }
         SSJ_CK(launch_strategy(e, p, out, t0, t1, e.s_comp));
         if (out == ssjb::kOutFlags && hi > lo) {
             SSJ_CK(cudaEventRecord(s.ev[ev], e.s_comp));
@@ -428,6 +446,8 @@ void destroy_slot(ChunkSlot& s) {
     cudaFree(s.dslices);
     cudaFree(s.dbits);
     cudaFree(s.drank);
+    cudaFree(s.ddefer);
+    cudaFree(s.ddefer_n);
     cudaFree(s.dacc);
     cudaFreeHost(s.hacc);
     cudaFreeHost(s.hflags);
@@ -444,6 +464,7 @@ int init_engine_runtime(ssj_engine& e) {
         for (auto& ev : s.ev) SSJ_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         SSJ_CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
         SSJ_CK(cudaMalloc(&s.dacc, SSJ_RESULT_WORDS * sizeof(unsigned long long)));
+        SSJ_CK(cudaMalloc(&s.ddefer_n, kMaxPieces * sizeof(unsigned long long)));
         SSJ_CK(cudaHostAlloc(&s.hacc, SSJ_RESULT_WORDS * sizeof(unsigned long long),
                              cudaHostAllocDefault));
     }
@@ -724,6 +745,8 @@ void ssj_engine_destroy(ssj_engine* e) {
     cudaFree(e->dev_slices);
     cudaFree(e->dev_bits);
     cudaFree(e->dev_rank);
+    cudaFree(e->dev_defer);
+    cudaFree(e->dev_defer_n);
     cudaFree(e->d_req_tab);
     cudaFree(e->d_res_slots);
     cudaFree(e->d_res_ov);
@@ -838,6 +861,9 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
                                            &e->dev_bits_cap, &e->dev_rank, &e->dev_rank_cap,
                                            n_slices, nC)))
         return rc;
+    if (tiles && (rc = ensure_device(&e->dev_defer, &e->dev_defer_cap, std::max<size_t>(nC, 1))))
+        return rc;
+    if (tiles && !e->dev_defer_n) SSJ_CK(cudaMalloc(&e->dev_defer_n, sizeof(unsigned long long)));
     KParams p = base_params(*e);
     p.C = d_C;
     p.nC = nC;
@@ -852,9 +878,13 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
         p.bm_bits = e->dev_bits;
         p.bm_rank = e->dev_rank;
         p.bm_cap = bitmap_words_for(nC);
+        p.defer = e->dev_defer;
+        p.defer_n = e->dev_defer_n;
+        p.defer_cap = nC;
     }
     const int out = (e->mode == SSJ_MODE_PAIRS && d_flags) ? ssjb::kOutFlags : ssjb::kOutCount;
     SSJ_CK(cudaMemsetAsync(d_result, 0, SSJ_RESULT_WORDS * sizeof(uint64_t), st));
+    if (tiles) SSJ_CK(cudaMemsetAsync(e->dev_defer_n, 0, sizeof(unsigned long long), st));
     SSJ_CK(ssjb::launch_prep(p, st));
     cudaEvent_t k0 = nullptr, k1 = nullptr;
     if (e->profiling) {
@@ -913,7 +943,8 @@ int ssj_launches_per_chunk(const ssj_engine* e, uint64_t nC, uint64_t nCO) {
     (void)nC;
     // prep (+ probe bitmaps for strategy A when there are slices) + one verification kernel;
     // the memset of the result block is not a kernel of ours
-    if (e && e->strategy.kind == SSJ_STRATEGY_A && nCO >= 2) return 3;
+    // strategy A: prep, probe bitmaps (when there are slices), tiles, long pairs
+    if (e && e->strategy.kind == SSJ_STRATEGY_A) return nCO >= 2 ? 4 : 3;
     return 2;
 }
 

@@ -305,6 +305,15 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
     for (int q = 0; q < kItems; ++q)
         sd[q] = cand[q] < p.n_sets ? __ldg(p.sets + cand[q]) : make_uint2(0, 0);
 
+    // 2. (issued before the slice setup) first 32-byte sector of the first candidate; the loop below prefetches item q+1's
+    //    sector before verifying item q
+    uint4 nw0, nw1;
+    {
+        const uint4* s4 = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[0].x * 8);
+        nw0 = __ldg(s4);
+        nw1 = __ldg(s4 + 1);
+    }
+
     uint32_t ns = 0;
     bool fast = false;
     if (e0 < p.n_slices) {
@@ -388,15 +397,6 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
         for (int q = 0; q < kItems; ++q) li[q] = 0;
     }
 
-    // 2. first 32-byte sector of the first candidate; the loop below prefetches item q+1's
-    //    sector before verifying item q
-    uint4 nw0, nw1;
-    {
-        const uint4* s4 = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[0].x * 8);
-        nw0 = __ldg(s4);
-        nw1 = __ldg(s4 + 1);
-    }
-
     // 3. verification
     unsigned count = 0, prunes = 0, verified = 0;
     uint32_t flag_bits[2] = {0, 0};
@@ -450,7 +450,18 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
                     const uint32_t n = sd[q].y;
                     const uint4* s4 = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[q].x * 8);
                     const uint64_t req = required_of(p, m, n);
-                    if (req == 0) {
+                    bool deferred = false;
+                    if (p.defer && n > kLongPair && req >= 1 && req <= (uint64_t)min(m, n)) {
+                        // long pair: hand it to long_kernel (one warp per pair)
+                        const unsigned long long idx = atomicAdd(p.defer_n, 1ull);
+                        if (idx < p.defer_cap) {
+                            p.defer[idx] = (uint32_t)slot;
+                            deferred = true;
+                        }
+                    }
+                    if (deferred) {
+                        // verdict, flag and stats come from long_kernel
+                    } else if (req == 0) {
                         met = true;  // verify.hpp:57: no comparison, met = (0 >= 0)
                         if (kOut == kOutResults)
                             ov = full_overlap_seq(r, m, reinterpret_cast<const uint32_t*>(s4), n);
@@ -463,7 +474,7 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
                                                                     cw0, cw1, &ov);
                         }
                     }
-                    if (kStats) {
+                    if (kStats && !deferred) {
                         ++verified;
                         prunes += (!met && (m + n) > 0);
                     }
@@ -541,6 +552,63 @@ __global__ void block_kernel(const KParams p, const uint32_t rcap) {
 // Strategy C: G lanes per pair over merge-path partitions, round-level early exit.
 constexpr uint32_t kHops = 16;
 
+// One pair walked by a group of G lanes (group-uniform control flow; gmask = the group's
+// lanes). Each round the lanes take consecutive segments of kHops merge-path hops starting
+// at the reference's diagonal split (verify.hpp:86-103) and count matches at their r-side
+// hop (verify.hpp:157-163); counts are shuffle-reduced. After each round the merge position
+// (iD, jD) at the round's last diagonal is exact, so the reference's bound
+// overlap + min(m - iD, n - jD) < required (verify.hpp:58) is evaluated there. With kFull
+// the path is walked to the end for qualifying pairs (ov = |r ∩ s|).
+template <int G, bool kFull>
+__device__ __forceinline__ bool path_pair(const uint32_t* r, uint32_t m, const uint32_t* s,
+                                          uint32_t n, uint64_t req, uint32_t lane,
+                                          unsigned gmask, uint32_t* ov_out) {
+    if (req > (uint64_t)min(m, n)) {
+        *ov_out = 0;
+        return false;
+    }
+    if (req == 0 && !kFull) return true;
+    const uint32_t total = m + n;
+    uint32_t D = 0, ov = 0;
+    while (D < total) {
+        const uint32_t d = D + lane * kHops;
+        uint32_t cnt = 0, ie = m, je = n;
+        if (d < total) {
+            uint32_t i = dev_merge_path_split(r, m, s, n, d);
+            uint32_t j = d - i;
+            const uint32_t hops = min(kHops, total - d);
+            for (uint32_t h = 0; h < hops && (i < m || j < n); ++h) {
+                if (j >= n || (i < m && r[i] <= s[j])) {
+                    if (j < n && r[i] == s[j]) ++cnt;
+                    ++i;
+                } else {
+                    ++j;
+                }
+            }
+            ie = i;
+            je = j;
+        }
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) cnt += __shfl_xor_sync(gmask, cnt, off, G);
+        ov += cnt;
+        const uint32_t Dn = min(D + G * kHops, total);
+        const uint32_t lb = (Dn - D - 1) / kHops;  // last lane with work
+        const uint32_t iD = __shfl_sync(gmask, ie, lb, G);
+        const uint32_t jD = __shfl_sync(gmask, je, lb, G);
+        D = Dn;
+        if (!kFull && ov >= req) {
+            *ov_out = ov;
+            return true;
+        }
+        if (ov < req && (uint64_t)ov + min(m - iD, n - jD) < req) {
+            *ov_out = 0;
+            return false;
+        }
+    }
+    *ov_out = ov;  // full path walked: ov = |r ∩ s|
+    return ov >= req;
+}
+
 template <int G, int kOut>
 __global__ void path_kernel(const KParams p, const uint32_t rcap) {
     extern __shared__ __align__(16) uint32_t dsh[];
@@ -577,54 +645,9 @@ __global__ void path_kernel(const KParams p, const uint32_t rcap) {
                     if (lane == 0) flag_error(p.acc, kErrOutOfRange);
                 } else {
                     const uint2 sd = __ldg(p.sets + cand);
-                    const uint32_t n = sd.y;
-                    const uint32_t* s = p.tokens + (size_t)sd.x * 8;
-                    const uint64_t req = dev_required(p.pred, m, n);
-                    const uint32_t total = m + n;
-                    bool decided = false;
-                    if (req > (uint64_t)min(m, n)) {
-                        decided = true;  // met = false
-                    } else if (req == 0 && kOut != kOutResults) {
-                        decided = true;
-                        met = true;
-                    }
-                    uint32_t D = 0;
-                    while (!decided && D < total) {
-                        const uint32_t d = D + lane * kHops;
-                        uint32_t cnt = 0, ie = m, je = n;
-                        if (d < total) {
-                            uint32_t i = dev_merge_path_split(r, m, s, n, d);
-                            uint32_t j = d - i;
-                            const uint32_t hops = min(kHops, total - d);
-                            for (uint32_t h = 0; h < hops && (i < m || j < n); ++h) {
-                                // verify.hpp:157-163: a common value counts at its r-side hop
-                                if (j >= n || (i < m && r[i] <= s[j])) {
-                                    if (j < n && r[i] == s[j]) ++cnt;
-                                    ++i;
-                                } else {
-                                    ++j;
-                                }
-                            }
-                            ie = i;
-                            je = j;
-                        }
-#pragma unroll
-                        for (int off = G / 2; off > 0; off >>= 1)
-                            cnt += __shfl_xor_sync(gmask, cnt, off, G);
-                        ov += cnt;
-                        const uint32_t Dn = min(D + G * kHops, total);
-                        const uint32_t lb = (Dn - D - 1) / kHops;  // last lane with work
-                        const uint32_t iD = __shfl_sync(gmask, ie, lb, G);
-                        const uint32_t jD = __shfl_sync(gmask, je, lb, G);
-                        D = Dn;
-                        if (kOut != kOutResults && ov >= req) {
-                            met = true;
-                            decided = true;
-                        } else if ((uint64_t)ov + min(m - iD, n - jD) < req) {
-                            decided = true;  // the bound of verify.hpp:58 at diagonal D
-                        }
-                    }
-                    if (!decided) met = ov >= req;  // full path walked: ov = |r ∩ s|
+                    met = path_pair<G, kOut == kOutResults>(
+                        r, m, p.tokens + (size_t)sd.x * 8, sd.y, required_of(p, m, sd.y), lane,
+                        gmask, &ov);
                 }
                 if (kOut == kOutFlags && lane == 0) p.flags[slot] = met ? 1 : 0;
             }
@@ -634,6 +657,90 @@ __global__ void path_kernel(const KParams p, const uint32_t rcap) {
         }
     }
     acc_add(p.acc, 0, count);
+}
+
+// ---------------------------------------------------------------------------------------
+// Long pairs deferred by tile_kernel (candidate longer than kLongPair tokens): one warp per
+// pair. With a probe bitmap the warp reads 32 consecutive candidate tokens per step
+// (one coalesced 128-byte load), tests membership in parallel, adds popc(ballot) to the
+// overlap and evaluates the reference's bound at the exact merge position after the step's
+// last token (rank lookup). Without a bitmap it walks the merge path (path_pair, G = 32).
+template <int kOut, bool kStats>
+__global__ void long_kernel(const KParams p) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t n_items = min((uint64_t)*p.defer_n, p.defer_cap);
+    unsigned count = 0, prunes = 0, verified = 0;
+    for (uint64_t w = gw; w < n_items; w += n_warps) {
+        const uint64_t slot = __ldg(p.defer + w);
+        const uint32_t e = upper_bound_ends(p.C_O, 0, p.n_slices, slot);
+        const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(p.slices + e));
+        const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(p.slices + e) + 1);
+        const uint32_t m = d0.z;
+        const uint32_t* r = p.tokens + (size_t)d0.y * 8;
+        const uint32_t cand = __ldg(p.C + slot);  // < n_sets: checked by tile_kernel
+        const uint2 sd = __ldg(p.sets + cand);
+        const uint32_t n = sd.y;
+        const uint32_t* s = p.tokens + (size_t)sd.x * 8;
+        const uint64_t req = required_of(p, m, n);
+        bool met;
+        uint32_t ov = 0;
+        if (d0.w != kNone && req >= 1 && req <= (uint64_t)min(m, n)) {
+            const uint32_t* bits = p.bm_bits + d0.w;
+            const uint32_t* rank = p.bm_rank + d0.w;
+            const uint32_t lo = d1.x, nbits = d1.y * 32;
+            const uint32_t slack_r = m - (uint32_t)req, slack_s = n - (uint32_t)req;
+            uint32_t j = 0;
+            bool decided = false;
+            met = false;
+            while (j < n) {
+                const uint32_t cnt = min(32u, n - j);
+                const uint32_t tok = lane < cnt ? __ldg(s + j + lane) : 0u;
+                const uint32_t d = tok - lo;
+                const bool in = lane < cnt && d < nbits;
+                const uint32_t bit = in ? (__ldg(bits + (d >> 5)) >> (d & 31)) & 1u : 0u;
+                ov += __popc(__ballot_sync(0xffffffffu, bit));
+                j += cnt;
+                if (j >= n) break;
+                if (kOut != kOutResults && ov >= req) {
+                    met = true;
+                    decided = true;
+                    break;
+                }
+                if (ov < req) {
+                    const uint32_t tl = __shfl_sync(0xffffffffu, tok, 31);
+                    const uint32_t dl = tl - lo;
+                    uint32_t i;
+                    if (tl < lo) i = 0;
+                    else if (dl >= nbits) i = m;
+                    else i = __ldg(rank + (dl >> 5)) + __popc(__ldg(bits + (dl >> 5)) & ((2u << (dl & 31)) - 1u));
+                    if (i - ov > slack_r || j - ov > slack_s) {
+                        decided = true;
+                        break;
+                    }
+                }
+            }
+            if (!decided) met = ov >= req;
+            if (!met) ov = 0;
+        } else {
+            met = path_pair<32, kOut == kOutResults>(r, m, s, n, req, lane, 0xffffffffu, &ov);
+        }
+        if (lane == 0) {
+            if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
+            count += met;
+            if (kStats) {
+                ++verified;
+                prunes += (!met && (m + n) > 0);
+            }
+        }
+        if (kOut == kOutResults) warp_append(p, met && lane == 0, slot, ov);
+    }
+    acc_add(p.acc, 0, count);
+    if (kStats) {
+        acc_add(p.acc, 2, verified);
+        acc_add(p.acc, 3, prunes);
+    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -735,6 +842,20 @@ cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_be
         case 3: tile_kernel<kOutFlags, true><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
         case 4: tile_kernel<kOutResults, false><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
         default: tile_kernel<kOutResults, true><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_long(const KParams& p, int out, bool stats, cudaStream_t st) {
+    if (!p.defer) return cudaSuccess;
+    const uint32_t grid = 148 * 8, threads = 256;
+    switch (out * 2 + (stats ? 1 : 0)) {
+        case 0: long_kernel<kOutCount, false><<<grid, threads, 0, st>>>(p); break;
+        case 1: long_kernel<kOutCount, true><<<grid, threads, 0, st>>>(p); break;
+        case 2: long_kernel<kOutFlags, false><<<grid, threads, 0, st>>>(p); break;
+        case 3: long_kernel<kOutFlags, true><<<grid, threads, 0, st>>>(p); break;
+        case 4: long_kernel<kOutResults, false><<<grid, threads, 0, st>>>(p); break;
+        default: long_kernel<kOutResults, true><<<grid, threads, 0, st>>>(p); break;
     }
     return cudaGetLastError();
 }

@@ -13,21 +13,25 @@ namespace ssjb {
 #define SSJB_TILE_THREADS 256
 #endif
 #ifndef SSJB_TILE_ITEMS
-#define SSJB_TILE_ITEMS 8
+#define SSJB_TILE_ITEMS 2
 #endif
 #ifndef SSJB_TILE_MIN_BLOCKS
-#define SSJB_TILE_MIN_BLOCKS 3
+#define SSJB_TILE_MIN_BLOCKS 4
 #endif
 constexpr uint32_t kThreadsA = SSJB_TILE_THREADS;            // threads per CTA
 constexpr uint32_t kTile = SSJB_TILE_THREADS * SSJB_TILE_ITEMS;  // candidate slots per CTA
 constexpr int kTileMinBlocks = SSJB_TILE_MIN_BLOCKS;         // CTAs per SM (register cap)
-constexpr uint32_t kMaxTileSlices = 512;   // slices of one tile described in shared memory
+constexpr uint32_t kMaxTileSlices = kTile / 2 < 512 ? kTile / 2 : 512;  // slices described in smem per tile
 constexpr uint32_t kTileRCap = 2048;       // probe tokens staged in shared memory per tile
 constexpr uint32_t kTileBitmapWords = 2048;  // bitmap words (bits + rank) copied to smem per tile
 constexpr uint32_t kSliceBitmapMinCands = 64;  // slices this long get a probe bitmap per chunk
-constexpr uint32_t kTileBitmapMinCands = 64;   // ... copied to smem when a tile has this many
+#ifndef SSJB_TILE_BM_COPY_MIN
+#define SSJB_TILE_BM_COPY_MIN 64
+#endif
+constexpr uint32_t kTileBitmapMinCands = SSJB_TILE_BM_COPY_MIN;  // ... copied to smem when a tile has this many
 constexpr uint32_t kMaxBitmapWords = 8192;     // probe token range cap (256K tokens)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kLongPair = 256;            // candidates longer than this go to long_kernel
 
 // Per-slice descriptor built once per chunk by prep_kernel (32 bytes, one sector).
 struct SliceDesc {
@@ -62,6 +66,9 @@ struct KParams {
     uint32_t* bm_bits;              // probe membership bitmaps (word = 32 tokens)
     uint32_t* bm_rank;              // probe tokens below each bitmap word
     uint64_t bm_cap;                // bitmap words available (0 = no bitmaps)
+    uint32_t* defer;                // strategy A: slots of long pairs for long_kernel
+    unsigned long long* defer_n;    // their count (this launch's segment)
+    uint64_t defer_cap;
     uint8_t* flags;                 // Pairs mode (nullable)
     uint32_t* res_slots;            // results mode (nullable)
     uint32_t* res_ov;
@@ -79,6 +86,8 @@ cudaError_t launch_prep(const KParams& p, cudaStream_t st, int* launches = nullp
 // Strategy A: tiles [tile_begin, tile_end)
 cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_begin,
                          uint32_t tile_end, cudaStream_t st);
+// Strategy A, second pass: the long pairs tile_kernel deferred (one warp per pair)
+cudaError_t launch_long(const KParams& p, int out, bool stats, cudaStream_t st);
 // Strategy B: block of `threads` per probe slice
 cudaError_t launch_block(const KParams& p, int out, bool stats, uint32_t threads,
                          cudaStream_t st);

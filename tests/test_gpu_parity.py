@@ -355,3 +355,29 @@ def test_auto_resolution_never_auto(ssj, gpu):
     big = ssj.Collection.from_sets([list(range(1000)), list(range(3, 1003))])
     with engine(ssj, big, ssj.jaccard(1, 2), "Auto", 32) as eng:
         assert eng.strategy().kind == ssj.StrategyKind.C and eng.strategy().group_size >= 32
+
+
+def test_long_sets_bitmaps_and_deferral(ssj, gpu, oracle):
+    """ENRON-like long sets: probe bitmaps (slices >= 64 candidates), long pairs deferred to
+    the warp-per-pair kernel, plus short slices on the merge path -- all strategies, flags,
+    results mode overlaps and stats against the oracle."""
+    coll = ssj.synth_collection(2019, ssj.SynthConfig(
+        sets=6000, min_size=1, max_size=6000, zipf_sizes=True, size_skew=1.3, universe=60000,
+        zipf_tokens=True, token_skew=1.0, duplicate_fraction=0.05, max_edits=3))
+    for num, den in ((3, 5), (4, 5)):
+        pred = ssj.jaccard(num, den)
+        chunk, _ = ssj.generate_candidates(coll, pred, ssj.Algorithm.AllPairs, threads=4)
+        assert chunk.C.size > 10_000
+        ref = oracle.verify_chunk(coll.tokens, coll.offsets, chunk.C, chunk.C_O,
+                                  oracle.pred(J, num, den), want_overlaps=True)
+        for kind, group in (("A", 1), ("B", 256), ("C", 32), ("C", 8)):
+            with engine(ssj, coll, pred, kind, group) as eng:
+                st = ssj.VerifyStats()
+                out = eng.verify_chunk(chunk, None, st)
+                assert out.count == ref["count"], (num, kind, group)
+                assert np.array_equal(out.flags, ref["flags"]), (num, kind, group)
+                if kind != "C":
+                    assert (st.pairs_verified, st.early_exit_prunes) == tuple(ref["stats"][:2])
+                slots, ovs = eng.verify_chunk_results(chunk)
+                want = np.nonzero(ref["flags"])[0]
+                assert np.array_equal(slots, want) and np.array_equal(ovs, ref["overlaps"][want])

@@ -1,0 +1,84 @@
+#!/usr/bin/env python
+"""End-to-end join time (BASELINE metric part 2): the GPU run_join
+(H0 CPU filtering -> pinned chunks -> GPU verification -> pairs) against the reference's
+own CPU run_join on the same collection, same algorithm, same M_c, same output mode.
+
+    python tools/join_e2e.py [--workload cfg5] [--mode count]
+
+Prints one JSON line with both reports' phase timings (pipeline.hpp:53-58) and whether
+verification was hidden behind filtering (join_ms ~= filtering_ms + serialization_ms).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1812_09141_b200 as ssj  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="cfg5", choices=sorted(bench.WORKLOADS))
+    ap.add_argument("--mode", default="count", choices=["count", "pairs"])
+    ap.add_argument("--budget", type=int, default=64 << 20)
+    ap.add_argument("--seed", type=int, default=1812)
+    ap.add_argument("--skip-reference", action="store_true")
+    args = ap.parse_args()
+
+    synth_kw, pred_t, algorithm, desc = bench.WORKLOADS[args.workload]
+    coll = ssj.synth_collection(args.seed, ssj.SynthConfig(**synth_kw))
+    pred = ssj.jaccard(*pred_t)
+    alg = ssj.Algorithm.AllPairs if algorithm == "allpairs" else ssj.Algorithm.PPJoin
+    mode = ssj.OutputMode.Pairs if args.mode == "pairs" else ssj.OutputMode.Count
+    out = {"workload": desc, "n_sets": coll.size(), "threshold": f"{pred_t[0]}/{pred_t[1]}",
+           "algorithm": algorithm, "mode": args.mode, "chunk_budget": args.budget}
+
+    def ours(filter_threads):
+        t0 = time.perf_counter()
+        rep = ssj.run_join(coll, pred, ssj.PipelineConfig(
+            algorithm=alg, chunk_budget=args.budget, mode=mode,
+            strategy=ssj.Strategy(ssj.StrategyKind.Auto, 32), filter_threads=filter_threads))
+        wall = 1e3 * (time.perf_counter() - t0)
+        t = rep.timings
+        return {"count": rep.count, "candidates": rep.candidate_count, "chunks": rep.chunk_count,
+                "join_ms": t.join_ms, "filtering_ms": t.filtering_ms,
+                "serialization_ms": t.serialization_ms, "handoff_wait_ms": t.handoff_wait_ms,
+                "verification_ms": t.verification_ms, "setup_ms": t.setup_ms, "wall_ms": wall,
+                "filter_threads": filter_threads,
+                "verification_hidden": t.join_ms <= 1.1 * (t.filtering_ms + t.serialization_ms
+                                                           - t.handoff_wait_ms) + 50}
+
+    ssj.run_join(ssj.Collection.from_sets([[1, 2], [1, 2]]), pred)  # warm the CUDA context
+    out["gpu_join_parallel_filter"] = ours(0)
+    out["gpu_join_reference_filter"] = ours(1)
+    if not args.skip_reference:
+        from oracle import pyoracle as po
+        if po.ref_available():
+            R = po.Ref()
+            h = R.coll(coll.tokens, coll.offsets, coll.original_id)
+            workers = R.L.ref_hardware_concurrency()
+            t0 = time.perf_counter()
+            rep, pairs, _ = R.run_join(h, 0, pred_t[0], pred_t[1], 1,
+                                       algorithm=0 if algorithm == "allpairs" else 1,
+                                       budget=args.budget, kind=0, group=1,
+                                       pairs_mode=args.mode == "pairs", workers=workers)
+            out["cpu_reference_join"] = {
+                "count": rep["count"], "candidates": rep["candidate_count"],
+                "chunks": rep["chunk_count"], "join_ms": rep["join_ms"],
+                "filtering_ms": rep["filtering_ms"], "serialization_ms": rep["serialization_ms"],
+                "verification_ms": rep["verification_ms"], "workers": int(workers),
+                "strategy": "A", "wall_ms": 1e3 * (time.perf_counter() - t0)}
+            assert rep["count"] == out["gpu_join_parallel_filter"]["count"], "count mismatch"
+            out["speedup_join"] = rep["join_ms"] / out["gpu_join_parallel_filter"]["join_ms"]
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

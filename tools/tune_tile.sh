@@ -6,9 +6,10 @@ shift
 OUT=gpurun_out; mkdir -p $OUT
 cp paper_1812_09141_b200/libssjoin_b200.so /tmp/lib_default.so
 for v in $VARIANTS; do
-  IFS=: read T I B <<< "$v"
+  IFS=: read T I B CP <<< "$v"
+  CP=${CP:-64}
   rm -rf build/obj
-  make -s -j16 NVFLAGS_EXTRA="-DSSJB_TILE_THREADS=$T -DSSJB_TILE_ITEMS=$I -DSSJB_TILE_MIN_BLOCKS=$B" \
+  make -s -j16 NVFLAGS_EXTRA="-DSSJB_TILE_THREADS=$T -DSSJB_TILE_ITEMS=$I -DSSJB_TILE_MIN_BLOCKS=$B -DSSJB_TILE_BM_COPY_MIN=$CP" \
        paper_1812_09141_b200/libssjoin_b200.so > /dev/null 2>&1 || { echo "build $v failed"; continue; }
   timeout 300 python bench.py --steps 10 --warmup 3 --e2e-steps 1 --no-cpu-baseline "$@" \
       > $OUT/tune_$v.json 2> $OUT/tune_$v.err
