@@ -144,23 +144,11 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def measure_l2_read_gbs(dev, mib=48, reps=50):
-    """L2-resident read bandwidth: a float32 reduction over a 48 MiB buffer (fits the 126 MB
-    L2), repeated; bytes read / CUDA-event time. The reference figure for working sets that
-    stay in L2."""
-    import torch
-    x = torch.ones(mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
-    for _ in range(5):
-        x.sum()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        x.sum()
-    e1.record()
-    torch.cuda.synchronize()
-    return x.numel() * 4 * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+def measure_read_gbs(local):
+    """Streaming-read bandwidth of an L2-resident (48 MiB) and an HBM-sized (4 GiB) buffer,
+    measured in this run by the library's diagnostic kernel (16-byte loads, grid-stride)."""
+    from paper_1812_09141_b200.verify import measure_read_bandwidth
+    return (measure_read_bandwidth(local, 48 << 20, 50), measure_read_bandwidth(local, 4 << 30, 5))
 
 
 def measured_peaks():
@@ -370,7 +358,7 @@ def main():
     kernel_avg_ms = kernel_ms / max(launches, 1)
     peak, peak_src = measured_peaks()
     achieved_gbs = algo_bytes / (kernel_avg_ms / 1e3) / 1e9
-    l2_gbs = measure_l2_read_gbs(dev)
+    l2_gbs, hbm_read_gbs = measure_read_gbs(local)
 
     # ---- end-to-end arm: C ABI with pinned host buffers ---------------------------------
     pc = ssj.PinnedBuffer(4 * nC + 64)
@@ -383,7 +371,8 @@ def main():
     hF = pf.view(np.uint8, nC)
     host_chunk = ssj.CandidateChunk.__new__(ssj.CandidateChunk)
     host_chunk.C, host_chunk.C_O = hC, hCO
-    eng.verify_chunk(host_chunk, flags_out=hF)  # warm-up
+    for _ in range(2):  # warm-up: both chunk slots of the engine (double buffering)
+        eng.verify_chunk(host_chunk, flags_out=hF)
     if world > 1:
         dist.barrier()
     te = time.perf_counter()
@@ -399,13 +388,18 @@ def main():
 
     # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------------------
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            rate, cores, kind, sample, _ = cpu_reference_rate(coll, pred_t, chunk,
-                                                              int(args.cpu_sample))
+            rate, cores, kind, sample, ref_count = cpu_reference_rate(coll, pred_t, chunk,
+                                                                      int(args.cpu_sample))
             cpu = {"value": rate, "unit": "pairs/s", "cores": cores, "kind": kind,
                    "sample": f"first {sample} candidates (slice-aligned) of the step's batch, "
                              f"VerificationEngine strategy A, best of 3"}
+            # the same sample's qualifying count from the GPU flags of the timed steps
+            gpu_count = int(dF[:sample].sum().item()) if sample else 0
+            parity = {"candidates": int(sample), "gpu_count": gpu_count,
+                      "reference_count": int(ref_count), "match": gpu_count == int(ref_count)}
         except Exception as e:  # reported, never fatal
             cpu = {"value": None, "unit": "pairs/s", "cores": 0, "kind": "unavailable",
                    "sample": str(e)[:200]}
@@ -437,10 +431,12 @@ def main():
                 "kernel_ms_avg": kernel_avg_ms, "peak_source": peak_src,
                 "kernel_share_of_step": kernel_ms / elapsed_ms if elapsed_ms else None,
                 "l2": {"peak": l2_gbs, "unit": "GB/s", "frac": achieved_gbs / l2_gbs,
-                       "source": "measured in this run: float32 reduction over a 48 MiB "
-                                 "L2-resident buffer"},
+                       "source": "measured in this run: streaming 16-byte reads of a 48 MiB "
+                                 "L2-resident buffer (ssj_measure_read_bandwidth)"},
+                "hbm_read_measured_gbs": hbm_read_gbs,
             },
             "cpu_baseline": cpu,
+            "parity_sample": parity,
             "e2e": {"value": e2e_value, "unit": "pairs/s",
                     "h2d_bytes_per_step": int(4 * nC + 4 * nCO),
                     "d2h_bytes_per_step": int(nC + 64), "steps": args.e2e_steps,

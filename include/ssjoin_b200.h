@@ -156,6 +156,19 @@ int ssj_verify_chunk_results(ssj_engine* e, const uint32_t* C, uint64_t nC,
                              uint32_t* overlaps_out, uint64_t cap, uint64_t* n_out);
 
 /*
+ * H2 on the GPU (decode_pairs, pipeline.hpp:79-92, and write_pairs order, report.hpp:39-42):
+ * verifies the chunk and returns the qualifying pairs as original input ids
+ * (r_id, s_id) with r_id > s_id, two uint32 per pair, plus their true overlaps (nullable).
+ * sorted != 0 sorts them on the device (radix sort on r_id << 32 | s_id). Original ids come
+ * from ssj_engine_set_original_ids (identity if never set). Only the qualifying pairs cross
+ * PCIe (no per-candidate flags). stats: nullable, as in ssj_verify_chunk.
+ */
+int ssj_engine_set_original_ids(ssj_engine* e, const uint32_t* original_id /* n_sets; NULL = identity */);
+int ssj_verify_chunk_pairs(ssj_engine* e, const uint32_t* C, uint64_t nC, const uint32_t* C_O,
+                           uint64_t nCO, uint32_t* pairs_out, uint32_t* overlaps_out,
+                           uint64_t cap, uint64_t* n_out, int sorted, ssj_stats* stats);
+
+/*
  * Device-resident variant (kernel-only path; the chunk is already in HBM):
  * d_C, d_C_O, d_flags (nullable) are device pointers; d_result is a device array of
  * SSJ_RESULT_WORDS uint64 that the call zeroes and fills asynchronously on `stream`
@@ -307,6 +320,12 @@ int ssj_join_result_report(const ssj_join_result* r, ssj_join_report* report);
 /* Result pairs (r_id, s_id), r_id > s_id, original ids, unsorted (like JoinReport::pairs). */
 int ssj_join_result_pairs(const ssj_join_result* r, uint32_t* pairs /* 2 * n_pairs */);
 void ssj_join_result_free(ssj_join_result* r);
+
+/* ---- diagnostics -------------------------------------------------------------------- */
+/* Streaming read bandwidth (GB/s) of a `bytes` device buffer read `reps` times with 16-byte
+ * loads: with bytes < L2 (126 MB) it measures L2-resident reads, with bytes >> L2 HBM reads.
+ * Used by bench.py for the roofline denominators of L2-resident working sets. */
+int ssj_measure_read_bandwidth(int device, uint64_t bytes, uint32_t reps, double* gbs);
 
 /* ---- pinned host buffers (ChunkBuilder storage; double-buffered by the driver) ------- */
 void* ssj_host_alloc(size_t bytes);

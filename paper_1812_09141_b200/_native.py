@@ -93,6 +93,9 @@ SIGNATURES = {
     "ssj_wait_chunk": (C.c_int, [vp, C.c_uint64, u64p, C.POINTER(ssj_stats)]),
     "ssj_verify_chunk_results": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, vp, vp,
                                            C.c_uint64, u64p]),
+    "ssj_engine_set_original_ids": (C.c_int, [vp, vp]),
+    "ssj_verify_chunk_pairs": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, vp, vp, C.c_uint64,
+                                         u64p, C.c_int, C.POINTER(ssj_stats)]),
     "ssj_verify_chunk_device": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, vp, vp, vp]),
     "ssj_launches_per_chunk": (C.c_int, [vp, C.c_uint64, C.c_uint64]),
     "ssj_engine_set_profiling": (C.c_int, [vp, C.c_int]),
@@ -120,6 +123,8 @@ SIGNATURES = {
     "ssj_join_result_report": (C.c_int, [vp, C.POINTER(ssj_join_report)]),
     "ssj_join_result_pairs": (C.c_int, [vp, vp]),
     "ssj_join_result_free": (None, [vp]),
+    "ssj_measure_read_bandwidth": (C.c_int, [C.c_int, C.c_uint64, C.c_uint32,
+                                             C.POINTER(C.c_double)]),
     "ssj_host_alloc": (vp, [C.c_size_t]),
     "ssj_host_free": (None, [vp]),
 }

@@ -18,6 +18,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "../../include/ssjoin_b200.h"
 #include "host_common.hpp"
 #include "verify_kernels.cuh"
@@ -173,6 +175,16 @@ struct ssj_engine {
     size_t res_cap = 0;
     size_t res_cap2 = 0;
     unsigned long long* d_res_n = nullptr;
+    // GPU pair decoding (ssj_verify_chunk_pairs)
+    uint32_t* d_oid = nullptr;
+    unsigned long long* d_keys = nullptr;
+    size_t keys_cap = 0;
+    unsigned long long* d_keys_alt = nullptr;
+    size_t keys_alt_cap = 0;
+    uint32_t* d_ov_alt = nullptr;
+    size_t ov_alt_cap = 0;
+    void* d_sort_tmp = nullptr;
+    size_t sort_tmp_cap = 0;
     // kernel timing (ssj_engine_set_profiling)
     bool profiling = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
@@ -181,15 +193,14 @@ struct ssj_engine {
 
 namespace {
 
-// verify.hpp:249-253 resolves Auto on the CPU (B for avg <= 10, else C with B >= 128).
-// The B200 policy keeps the reference's input (the integer average set size,
-// collection.hpp:91-93) but maps to the GPU kernels: the load-balanced thread-per-pair
-// tiles (A) for short sets, warp-cooperative merge paths (C, 32 lanes) for long ones.
+// verify.hpp:249-253 resolves Auto on the CPU (B for avg <= 10, else C with B >= 128): a
+// worker-pool policy. On the B200 one kernel family covers both regimes: the load-balanced
+// tile kernel (A) verifies short pairs thread-per-pair and defers long candidates to a
+// warp-per-pair pass (the cooperative scheme of C), so Auto resolves to A for every input.
 ssj_strategy resolve_strategy(const ssj_engine& e, ssj_strategy s) {
+    (void)e;
     if (s.kind != SSJ_STRATEGY_AUTO) return s;
-    const uint64_t avg = e.n_sets ? e.n_tokens / e.n_sets : 0;
-    if (avg <= 256) return {SSJ_STRATEGY_A, s.group_size};
-    return {SSJ_STRATEGY_C, std::max<uint32_t>(s.group_size, 32)};
+    return {SSJ_STRATEGY_A, s.group_size};
 }
 
 int make_pred_dev(const ssj_predicate& p, PredDev* out) {
@@ -751,6 +762,11 @@ void ssj_engine_destroy(ssj_engine* e) {
     cudaFree(e->d_res_slots);
     cudaFree(e->d_res_ov);
     cudaFree(e->d_res_n);
+    cudaFree(e->d_oid);
+    cudaFree(e->d_keys);
+    cudaFree(e->d_keys_alt);
+    cudaFree(e->d_ov_alt);
+    cudaFree(e->d_sort_tmp);
     for (auto& pe : e->prof_events) {
         cudaEventDestroy(pe.first);
         cudaEventDestroy(pe.second);
@@ -841,6 +857,85 @@ int ssj_verify_chunk_results(ssj_engine* e, const uint32_t* C, uint64_t nC, cons
     for (uint64_t i = 0; i < w; ++i) {
         slots_out[i] = (uint32_t)(key[i] >> 32);
         overlaps_out[i] = (uint32_t)key[i];
+    }
+    if (n > cap) return fail(SSJ_ERR_RUNTIME, "result capacity exceeded");
+    return SSJ_OK;
+}
+
+int ssj_engine_set_original_ids(ssj_engine* e, const uint32_t* original_id) {
+    if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
+    DeviceScope ds(e->device);
+    if (!e->d_oid) SSJ_CK(cudaMalloc(&e->d_oid, (size_t)std::max<uint32_t>(e->n_sets, 1) * 4));
+    if (original_id) {
+        SSJ_CK(cudaMemcpy(e->d_oid, original_id, (size_t)e->n_sets * 4, cudaMemcpyHostToDevice));
+    } else {
+        std::vector<uint32_t> id(e->n_sets);
+        for (uint32_t i = 0; i < e->n_sets; ++i) id[i] = i;
+        SSJ_CK(cudaMemcpy(e->d_oid, id.data(), (size_t)e->n_sets * 4, cudaMemcpyHostToDevice));
+    }
+    return SSJ_OK;
+}
+
+int ssj_verify_chunk_pairs(ssj_engine* e, const uint32_t* C, uint64_t nC, const uint32_t* C_O,
+                           uint64_t nCO, uint32_t* pairs_out, uint32_t* overlaps_out,
+                           uint64_t cap, uint64_t* n_out, int sorted, ssj_stats* stats) {
+    int rc = check_chunk_args(e, C, nC, C_O, nCO);
+    if (rc) return rc;
+    if (!n_out || (cap && !pairs_out)) return fail(SSJ_ERR_INVALID_ARGUMENT, "null output");
+    DeviceScope ds(e->device);
+    if (!e->d_oid && (rc = ssj_engine_set_original_ids(e, nullptr))) return rc;
+    ChunkSlot& s = e->slot[e->next_ticket & 1];
+    if (s.busy) return fail(SSJ_ERR_RUNTIME, "a chunk is in flight on this slot: wait first");
+    if ((rc = enqueue_chunk(*e, s, C, nC, C_O, nCO, nullptr, ssjb::kOutResults))) {
+        cudaDeviceSynchronize();
+        return rc;
+    }
+    if ((rc = finish_chunk(*e, s, nullptr, stats))) return rc;
+    unsigned long long n = 0;
+    SSJ_CK(cudaMemcpy(&n, e->d_res_n, sizeof(n), cudaMemcpyDeviceToHost));
+    *n_out = n;
+    if (n) {
+        if ((rc = ensure_device(&e->d_keys, &e->keys_cap, n))) return rc;
+        KParams p = base_params(*e);
+        p.C = s.dC;
+        p.nC = nC;
+        p.C_O = s.dCO;
+        p.n_slices = (uint32_t)(nCO / 2);
+        p.res_slots = e->d_res_slots;
+        SSJ_CK(ssjb::launch_pairs(p, e->d_oid, n, e->d_keys, e->s_comp));
+        unsigned long long* keys = e->d_keys;
+        uint32_t* ovs = e->d_res_ov;
+        if (sorted) {  // write_pairs order (report.hpp:39-42) by a device radix sort
+            if ((rc = ensure_device(&e->d_keys_alt, &e->keys_alt_cap, n))) return rc;
+            if ((rc = ensure_device(&e->d_ov_alt, &e->ov_alt_cap, n))) return rc;
+            size_t tmp = 0;
+            SSJ_CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, e->d_keys, e->d_keys_alt,
+                                                   e->d_res_ov, e->d_ov_alt, (int)n, 0, 64,
+                                                   e->s_comp));
+            if (tmp > e->sort_tmp_cap) {
+                cudaFree(e->d_sort_tmp);
+                e->d_sort_tmp = nullptr;
+                e->sort_tmp_cap = 0;
+                SSJ_CK(cudaMalloc(&e->d_sort_tmp, tmp));
+                e->sort_tmp_cap = tmp;
+            }
+            SSJ_CK(cub::DeviceRadixSort::SortPairs(e->d_sort_tmp, tmp, e->d_keys, e->d_keys_alt,
+                                                   e->d_res_ov, e->d_ov_alt, (int)n, 0, 64,
+                                                   e->s_comp));
+            keys = e->d_keys_alt;
+            ovs = e->d_ov_alt;
+        }
+        SSJ_CK(cudaStreamSynchronize(e->s_comp));
+        const uint64_t w = std::min<uint64_t>(n, cap);
+        std::vector<unsigned long long> hk(w);
+        if (w) {
+            SSJ_CK(cudaMemcpy(hk.data(), keys, w * 8, cudaMemcpyDeviceToHost));
+            if (overlaps_out) SSJ_CK(cudaMemcpy(overlaps_out, ovs, w * 4, cudaMemcpyDeviceToHost));
+        }
+        for (uint64_t i = 0; i < w; ++i) {
+            pairs_out[2 * i] = (uint32_t)(hk[i] >> 32);
+            pairs_out[2 * i + 1] = (uint32_t)hk[i];
+        }
     }
     if (n > cap) return fail(SSJ_ERR_RUNTIME, "result capacity exceeded");
     return SSJ_OK;
@@ -962,6 +1057,39 @@ int ssj_chunk_algorithmic_bytes_device(ssj_engine* e, const uint32_t* d_C, uint6
     p.n_slices = (uint32_t)(nCO / 2);
     SSJ_CK(cudaMemsetAsync(d_bytes, 0, sizeof(uint64_t), st));
     SSJ_CK(ssjb::launch_bytes(p, reinterpret_cast<unsigned long long*>(d_bytes), st));
+    return SSJ_OK;
+}
+
+int ssj_measure_read_bandwidth(int device, uint64_t bytes, uint32_t reps, double* gbs) {
+    int rc = check_device(device);
+    if (rc) return rc;
+    if (!gbs || bytes < 16 || !reps) return fail(SSJ_ERR_INVALID_ARGUMENT, "bad arguments");
+    DeviceScope ds(device);
+    void* buf = nullptr;
+    unsigned* sink = nullptr;
+    cudaEvent_t a = nullptr, b = nullptr;
+    auto cleanup = [&]() {
+        cudaFree(buf);
+        cudaFree(sink);
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    };
+    if (cudaMalloc(&buf, bytes) != cudaSuccess || cudaMalloc(&sink, 4) != cudaSuccess ||
+        cudaMemset(buf, 1, bytes) != cudaSuccess || cudaEventCreate(&a) != cudaSuccess ||
+        cudaEventCreate(&b) != cudaSuccess) {
+        cleanup();
+        return fail(SSJ_ERR_CUDA, "bandwidth probe setup failed");
+    }
+    ssjb::launch_read_bw(buf, bytes, 2, sink, 0);  // warm-up (and L2 fill)
+    cudaEventRecord(a, 0);
+    ssjb::launch_read_bw(buf, bytes, reps, sink, 0);
+    cudaEventRecord(b, 0);
+    float ms = 0;
+    const cudaError_t err = cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    cleanup();
+    if (err != cudaSuccess) return fail(SSJ_ERR_CUDA, cudaGetErrorString(err));
+    *gbs = (double)bytes * reps / (ms / 1e3) / 1e9;
     return SSJ_OK;
 }
 

@@ -78,8 +78,14 @@ struct PinnedVec {
 struct Chunk {
     PinnedVec<uint32_t> C, CO;
     PinnedVec<uint8_t> flags;
+    std::vector<uint32_t> pairs;  // pairs decoded on the GPU (pairs mode without observer)
+    bool decoded = false;
     uint64_t byte_size() const { return 4ull * (C.n + CO.n); }  // chunk.hpp:25-27
-    void clear() { C.n = CO.n = 0; }
+    void clear() {
+        C.n = CO.n = 0;
+        pairs.clear();
+        decoded = false;
+    }
 };
 
 class ChunkPool {
@@ -213,6 +219,7 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
                                 &cfg->strategy)))
         return rc;
     ssj_engine_strategy(engine.e, &report.resolved_strategy);
+    if (pairs_mode && (rc = ssj_engine_set_original_ids(engine.e, original_id))) return rc;
     report.setup_ms = ms_since(setup_start);
 
     ChunkPool pool(3);
@@ -256,7 +263,9 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
                 h2_slot = nullptr;
                 lk.unlock();
                 uint64_t prev = 0;
-                for (size_t e = 0; e + 1 < ch->CO.n; e += 2) {
+                if (ch->decoded)
+                    engine_pairs.insert(engine_pairs.end(), ch->pairs.begin(), ch->pairs.end());
+                for (size_t e = 0; !ch->decoded && e + 1 < ch->CO.n; e += 2) {
                     const uint32_t pid = original_id[ch->CO.p[e]];
                     const uint64_t end = ch->CO.p[e + 1];
                     for (uint64_t s = prev; s < end; ++s) {
@@ -291,11 +300,21 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
                 }
                 Chunk* ch = to_dispatcher.take();
                 if (!ch) break;
-                if (pairs_mode) ch->flags.reserve(ch->C.n + 1);
                 uint64_t count = 0;
                 const auto t0 = Clock::now();
-                ck(ssj_verify_chunk(engine.e, ch->C.p, ch->C.n, ch->CO.p, ch->CO.n,
-                                    pairs_mode ? ch->flags.p : nullptr, &count, &stats));
+                if (pairs_mode && !cfg->observer) {
+                    // H2 on the GPU: only the qualifying pairs (original ids) cross PCIe
+                    ch->pairs.resize(2 * (ch->C.n + 1));
+                    ck(ssj_verify_chunk_pairs(engine.e, ch->C.p, ch->C.n, ch->CO.p, ch->CO.n,
+                                              ch->pairs.data(), nullptr, ch->C.n + 1, &count,
+                                              0, &stats));
+                    ch->pairs.resize(2 * count);
+                    ch->decoded = true;
+                } else {
+                    if (pairs_mode) ch->flags.reserve(ch->C.n + 1);
+                    ck(ssj_verify_chunk(engine.e, ch->C.p, ch->C.n, ch->CO.p, ch->CO.n,
+                                        pairs_mode ? ch->flags.p : nullptr, &count, &stats));
+                }
                 verification_ms += ms_since(t0);
                 ++verified_chunks;
                 verified_candidates += ch->C.n;

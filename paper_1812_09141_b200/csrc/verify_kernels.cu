@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
 
     // 1. this thread's candidate ids and their set descriptors (independent of the slices)
     uint32_t cand[kItems];
-    if (my0 + kItems <= slot1 && ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0)) {
+    if (kItems % 4 == 0 && my0 + kItems <= slot1 &&
+        ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0)) {
         const uint4* c4 = reinterpret_cast<const uint4*>(p.C + my0);
 #pragma unroll
         for (int q = 0; q < kItems / 4; ++q) {
@@ -295,6 +296,15 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
             cand[4 * q + 1] = v.y;
             cand[4 * q + 2] = v.z;
             cand[4 * q + 3] = v.w;
+        }
+    } else if (kItems % 2 == 0 && my0 + kItems <= slot1 &&
+               ((reinterpret_cast<uintptr_t>(p.C) & 7) == 0)) {
+        const uint2* c2 = reinterpret_cast<const uint2*>(p.C + my0);
+#pragma unroll
+        for (int q = 0; q < kItems / 2; ++q) {
+            const uint2 v = __ldg(c2 + q);
+            cand[2 * q] = v.x;
+            cand[2 * q + 1] = v.y;
         }
     } else {
 #pragma unroll
@@ -305,6 +315,7 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
     for (int q = 0; q < kItems; ++q)
         sd[q] = cand[q] < p.n_sets ? __ldg(p.sets + cand[q]) : make_uint2(0, 0);
 
+#if SSJB_EARLY_SECTOR
     // 2. (issued before the slice setup) first 32-byte sector of the first candidate; the loop below prefetches item q+1's
     //    sector before verifying item q
     uint4 nw0, nw1;
@@ -314,6 +325,7 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
         nw1 = __ldg(s4 + 1);
     }
 
+#endif
     uint32_t ns = 0;
     bool fast = false;
     if (e0 < p.n_slices) {
@@ -397,9 +409,18 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
         for (int q = 0; q < kItems; ++q) li[q] = 0;
     }
 
+#if !SSJB_EARLY_SECTOR
+    uint4 nw0, nw1;
+    {
+        const uint4* s4 = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[0].x * 8);
+        nw0 = __ldg(s4);
+        nw1 = __ldg(s4 + 1);
+    }
+#endif
+
     // 3. verification
     unsigned count = 0, prunes = 0, verified = 0;
-    uint32_t flag_bits[2] = {0, 0};
+    uint32_t flag_bits[(kItems + 3) / 4] = {};
 #pragma unroll
     for (int q = 0; q < kItems; ++q) {
         const uint64_t slot = my0 + q;
@@ -486,8 +507,12 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
         if (kOut == kOutResults) warp_append(p, met, slot, ov);
     }
     if (kOut == kOutFlags) {
-        if (my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 7) == 0) {
+        if (kItems == 8 && my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 7) == 0) {
             *reinterpret_cast<uint2*>(p.flags + my0) = make_uint2(flag_bits[0], flag_bits[1]);
+        } else if (kItems == 4 && my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 3) == 0) {
+            *reinterpret_cast<uint32_t*>(p.flags + my0) = flag_bits[0];
+        } else if (kItems == 2 && my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 1) == 0) {
+            *reinterpret_cast<uint16_t*>(p.flags + my0) = (uint16_t)flag_bits[0];
         } else {
 #pragma unroll
             for (int q = 0; q < kItems; ++q)
@@ -744,6 +769,37 @@ __global__ void long_kernel(const KParams p) {
 }
 
 // ---------------------------------------------------------------------------------------
+// Diagnostic: streaming read bandwidth of a device buffer (16-byte loads, grid-stride),
+// used by the benchmark for the L2-resident and HBM roofline denominators.
+__global__ void read_bw_kernel(const uint4* __restrict__ a, uint64_t n, uint32_t reps,
+                               unsigned* __restrict__ sink) {
+    uint32_t x = 0;
+    for (uint32_t r = 0; r < reps; ++r) {
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+             i += (uint64_t)gridDim.x * blockDim.x) {
+            const uint4 v = __ldcg(a + i);
+            x ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+    }
+    if (x == 0x9E3779B9u) sink[0] = x;  // keeps the loads alive
+}
+
+// ---------------------------------------------------------------------------------------
+// H2 on the GPU (pipeline.hpp:79-92 decode_pairs): qualifying slot -> (max(orig), min(orig))
+// original input ids, packed as a 64-bit key (r_id << 32 | s_id) so that a radix sort gives
+// write_pairs order (report.hpp:39-42).
+__global__ void pairs_kernel(const KParams p, const uint32_t* __restrict__ oid, uint64_t n,
+                             unsigned long long* __restrict__ keys) {
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t slot = p.res_slots[k];
+    const uint32_t e = upper_bound_ends(p.C_O, 0, p.n_slices, slot);
+    const uint32_t a = __ldg(oid + __ldg(p.C_O + 2 * (size_t)e));
+    const uint32_t b = __ldg(oid + __ldg(p.C + slot));
+    keys[k] = ((unsigned long long)max(a, b) << 32) | min(a, b);
+}
+
+// ---------------------------------------------------------------------------------------
 // Instrumentation: algorithmic bytes under the reference loop
 // verify.hpp:56-69, replayed exactly per pair.
 __global__ void bytes_kernel(const KParams p, unsigned long long* out) {
@@ -894,6 +950,19 @@ cudaError_t launch_path(const KParams& p, int out, uint32_t group, cudaStream_t 
     if (group >= 4) return launch_path_out<4>(p, out, grid, rcap, smem, st);
     if (group >= 2) return launch_path_out<2>(p, out, grid, rcap, smem, st);
     return launch_path_out<1>(p, out, grid, rcap, smem, st);
+}
+
+cudaError_t launch_read_bw(const void* buf, uint64_t bytes, uint32_t reps, unsigned* sink,
+                           cudaStream_t st) {
+    read_bw_kernel<<<148 * 8, 512, 0, st>>>(static_cast<const uint4*>(buf), bytes / 16, reps, sink);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pairs(const KParams& p, const uint32_t* oid, uint64_t n,
+                         unsigned long long* keys, cudaStream_t st) {
+    if (!n) return cudaSuccess;
+    pairs_kernel<<<(uint32_t)((n + 255) / 256), 256, 0, st>>>(p, oid, n, keys);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_bytes(const KParams& p, unsigned long long* d_bytes, cudaStream_t st) {

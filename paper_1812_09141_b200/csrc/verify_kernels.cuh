@@ -25,6 +25,9 @@ constexpr uint32_t kMaxTileSlices = kTile / 2 < 512 ? kTile / 2 : 512;  // slice
 constexpr uint32_t kTileRCap = 2048;       // probe tokens staged in shared memory per tile
 constexpr uint32_t kTileBitmapWords = 2048;  // bitmap words (bits + rank) copied to smem per tile
 constexpr uint32_t kSliceBitmapMinCands = 64;  // slices this long get a probe bitmap per chunk
+#ifndef SSJB_EARLY_SECTOR
+#define SSJB_EARLY_SECTOR 0
+#endif
 #ifndef SSJB_TILE_BM_COPY_MIN
 #define SSJB_TILE_BM_COPY_MIN 64
 #endif
@@ -93,6 +96,12 @@ cudaError_t launch_block(const KParams& p, int out, bool stats, uint32_t threads
                          cudaStream_t st);
 // Strategy C: groups of G lanes per pair, merge-path partitions with round-level exits
 cudaError_t launch_path(const KParams& p, int out, uint32_t group, cudaStream_t st);
+// Diagnostic streaming-read kernel (bandwidth probe)
+cudaError_t launch_read_bw(const void* buf, uint64_t bytes, uint32_t reps, unsigned* sink,
+                           cudaStream_t st);
+// H2 on the GPU: qualifying slots (p.res_slots[0..n)) -> (r_id << 32 | s_id) original ids
+cudaError_t launch_pairs(const KParams& p, const uint32_t* oid, uint64_t n,
+                         unsigned long long* keys, cudaStream_t st);
 // Instrumentation: algorithmic bytes under the reference loop
 cudaError_t launch_bytes(const KParams& p, unsigned long long* d_bytes, cudaStream_t st);
 

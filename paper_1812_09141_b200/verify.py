@@ -198,6 +198,29 @@ class VerificationEngine:
                                                    C.byref(n)))
         return slots[: n.value], ovs[: n.value]
 
+    def set_original_ids(self, original_id: Optional[np.ndarray] = None) -> None:
+        """Original input ids for verify_chunk_pairs (identity when None)."""
+        oid = None if original_id is None else np.ascontiguousarray(original_id, np.uint32)
+        N.check(self._lib.ssj_engine_set_original_ids(self._h, _vp(oid)))
+
+    def verify_chunk_pairs(self, chunk: CandidateChunk, sorted_: bool = True,
+                           stats: Optional[VerifyStats] = None) -> Tuple[np.ndarray, np.ndarray]:
+        """Qualifying pairs decoded on the GPU: ((k, 2) uint32 (r_id, s_id) with r_id > s_id,
+        in write_pairs order when sorted_), and their true overlaps."""
+        nC = chunk.candidate_count()
+        pairs = np.zeros(2 * max(nC, 1), np.uint32)
+        ovs = np.zeros(max(nC, 1), np.uint32)
+        n = C.c_uint64()
+        st = N.ssj_stats()
+        N.check(self._lib.ssj_verify_chunk_pairs(self._h, _vp(chunk.C), nC, _vp(chunk.C_O),
+                                                 chunk.C_O.size, _vp(pairs), _vp(ovs), nC,
+                                                 C.byref(n), int(sorted_), C.byref(st)))
+        if stats is not None:
+            stats.pairs_verified += st.pairs_verified
+            stats.early_exit_prunes += st.early_exit_prunes
+            stats.comparison_budget_violations += st.comparison_budget_violations
+        return pairs[: 2 * n.value].reshape(-1, 2), ovs[: n.value]
+
     # -- device-resident (kernel-only) path --------------------------------------------
     def verify_chunk_device(self, d_C: int, nC: int, d_C_O: int, nCO: int, d_flags: int,
                             d_result: int, stream: int = 0) -> None:
@@ -241,6 +264,13 @@ def result_error(words) -> None:
         raise IndexError("set index out of range")
     if bits & 2:
         raise ValueError("malformed C_O: end offsets decreasing or beyond C")
+
+
+def measure_read_bandwidth(device: int, nbytes: int, reps: int = 20) -> float:
+    """Streaming read GB/s of an nbytes device buffer (diagnostic, see the C ABI)."""
+    g = C.c_double()
+    N.check(N.lib().ssj_measure_read_bandwidth(device, nbytes, reps, C.byref(g)))
+    return g.value
 
 
 def device_count() -> int:

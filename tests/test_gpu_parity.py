@@ -354,7 +354,10 @@ def test_auto_resolution_never_auto(ssj, gpu):
         assert eng.strategy().kind != ssj.StrategyKind.Auto
     big = ssj.Collection.from_sets([list(range(1000)), list(range(3, 1003))])
     with engine(ssj, big, ssj.jaccard(1, 2), "Auto", 32) as eng:
-        assert eng.strategy().kind == ssj.StrategyKind.C and eng.strategy().group_size >= 32
+        # B200 policy: the tile kernel (A) with long pairs deferred to warp-per-pair
+        assert eng.strategy().kind == ssj.StrategyKind.A and eng.strategy().group_size == 32
+        out = eng.verify_chunk(ssj.CandidateChunk([0], [1, 1]))
+        assert out.count == 1
 
 
 def test_long_sets_bitmaps_and_deferral(ssj, gpu, oracle):
@@ -381,3 +384,30 @@ def test_long_sets_bitmaps_and_deferral(ssj, gpu, oracle):
                 slots, ovs = eng.verify_chunk_results(chunk)
                 want = np.nonzero(ref["flags"])[0]
                 assert np.array_equal(slots, want) and np.array_equal(ovs, ref["overlaps"][want])
+
+
+@pytest.mark.parametrize("name", ["medium_s101", "sweep_s1002", "verify_s43"])
+def test_gpu_pair_decoding(ssj, gpu, oracle, name):
+    """H2 on the GPU (decode_pairs pipeline.hpp:79-92 + write_pairs order report.hpp:39-42):
+    qualifying slots -> (max, min) original ids, radix-sorted on the device, with overlaps."""
+    g = golden(name)
+    coll = coll_of(ssj, g)
+    for key in chunk_keys(g):
+        fn, num, den = (int(x) for x in key.split("_")[:3])
+        chunk = ssj.CandidateChunk(g["C_" + key], g["CO_" + key])
+        ref = oracle.verify_chunk(g["tokens"], g["offsets"], chunk.C, chunk.C_O,
+                                  oracle.pred(fn, num, den), want_overlaps=True)
+        slots = np.nonzero(ref["flags"])[0]
+        probe = chunk.C_O[0::2][np.searchsorted(chunk.C_O[1::2].astype(np.int64), slots,
+                                                side="right")]
+        a = coll.original_id[probe]
+        b = coll.original_id[chunk.C[slots]]
+        want = np.stack([np.maximum(a, b), np.minimum(a, b)], 1).astype(np.uint32)
+        order = np.lexsort((want[:, 1], want[:, 0]))
+        with engine(ssj, coll, make_pred(ssj, fn, num, den)) as eng:
+            eng.set_original_ids(coll.original_id)
+            st = ssj.VerifyStats()
+            pairs, ovs = eng.verify_chunk_pairs(chunk, True, st)
+            assert np.array_equal(pairs, want[order]), key
+            assert np.array_equal(ovs, ref["overlaps"][slots][order]), key
+            assert st.pairs_verified == chunk.C.size
