@@ -54,11 +54,11 @@ WORKLOADS = {
                   max_edits=2),
              (3, 4), "allpairs",
              "KOSARAK-like sparse self-join, 1M sets, avg ~8 tokens, long tail, Jaccard 0.75"),
-    "cfg4": (dict(sets=250_000, min_size=1, max_size=20_000, zipf_sizes=True, size_skew=1.3,
+    "cfg4": (dict(sets=100_000, min_size=1, max_size=20_000, zipf_sizes=True, size_skew=1.3,
                   universe=200_000, zipf_tokens=True, token_skew=1.0, duplicate_fraction=0.02,
                   max_edits=3),
              (3, 5), "allpairs",
-             "ENRON/ORKUT-like long-set self-join, 250K sets, avg ~180 tokens, max >10K, Jaccard 0.6"),
+             "ENRON/ORKUT-like long-set self-join, 100K sets, avg ~180 tokens, max >10K, Jaccard 0.6"),
     "cfg5": (dict(sets=550_000, min_size=40, max_size=120, universe=7200, zipf_tokens=True,
                   token_skew=1.0, duplicate_fraction=0.01, max_edits=2, distinct_tokens=True),
              (4, 5), "allpairs",
@@ -172,16 +172,34 @@ def ncu_traffic(workload):
         return None
 
 
+def stratified_sample(chunk, sample):
+    """Every k-th slice of the batch (k chosen so that ~`sample` candidates are picked), so the
+    CPU sample has the batch's mix of probe sizes (slices are in probe = size order).
+    Returns (C_sub, C_O_sub, slot_index_of_sub) as numpy arrays."""
+    CO = chunk.C_O.reshape(-1, 2).astype(np.int64)
+    n_sl = CO.shape[0]
+    if n_sl == 0:
+        return np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.int64)
+    ends = CO[:, 1]
+    begins = np.concatenate([[0], ends[:-1]])
+    total = int(ends[-1])
+    k = max(1, int(np.ceil(total / max(sample, 1))))
+    pick = np.arange(0, n_sl, k)
+    lens = ends[pick] - begins[pick]
+    idx = np.concatenate([np.arange(b, e) for b, e in zip(begins[pick], ends[pick])]) \
+        if lens.sum() else np.zeros(0, np.int64)
+    sub_C = chunk.C[idx]
+    sub_CO = np.stack([CO[pick, 0], np.cumsum(lens)], 1).reshape(-1).astype(np.uint32)
+    return sub_C, sub_CO, idx
+
+
 def cpu_reference_rate(coll, pred_t, chunk, sample, reps=3):
-    """The reference's verify_chunk (strategy A, all host threads) on the first `sample`
-    candidates (slice-aligned) of the batch. Returns (pairs/s, cores, kind, sample)."""
+    """The reference's verify_chunk (strategy A, all host threads) on a stratified sample of
+    ~`sample` candidates of the batch (every k-th slice). Returns
+    (pairs/s, cores, kind, n_sample, count, slot_index)."""
     from oracle import pyoracle as po
-    CO = chunk.C_O.reshape(-1, 2)
-    k = int(np.searchsorted(CO[:, 1].astype(np.int64), sample, side="left")) + 1
-    k = min(k, CO.shape[0])
-    sub_CO = CO[:k].reshape(-1).copy()
-    nC = int(CO[k - 1, 1]) if k else 0
-    sub_C = chunk.C[:nC]
+    sub_C, sub_CO, idx = stratified_sample(chunk, sample)
+    nC = int(sub_C.size)
     if po.ref_available():
         R = po.Ref()
         h = R.coll(coll.tokens, coll.offsets, coll.original_id)
@@ -189,11 +207,11 @@ def cpu_reference_rate(coll, pred_t, chunk, sample, reps=3):
         pool = R.pool(workers)
         sec, cnt = R.time_verify_chunk(h, pool, 0, pred_t[0], pred_t[1], 1, 0, 1, True, sub_C,
                                        sub_CO, reps=reps)
-        return nC / sec, int(workers), "reference", nC, cnt
+        return nC / sec, int(workers), "reference", nC, cnt, idx
     t0 = time.perf_counter()
     res = po.verify_chunk(coll.tokens, coll.offsets, sub_C, sub_CO, po.pred(0, *pred_t))
     sec = time.perf_counter() - t0
-    return nC / sec, 1, "port", nC, res["count"]
+    return nC / sec, 1, "port", nC, res["count"], idx
 
 
 def run_reference_arm(args):
@@ -204,8 +222,11 @@ def run_reference_arm(args):
     synth_kw, pred_t, algorithm, desc = WORKLOADS[args.workload]
     coll = ssj.synth_collection(args.seed, ssj.SynthConfig(**synth_kw))
     pred = ssj.jaccard(*pred_t)
-    chunk, width = build_batch(ssj, coll, pred, algorithm, 0, 1, args.ref_sample, args.windows,
+    chunk, width = build_batch(ssj, coll, pred, algorithm, 0, 1,
+                               256e6 if args.workload in ("cfg2", "cfg5") else 0, args.windows,
                                args.threads)
+    sub_C, sub_CO, _ = stratified_sample(chunk, args.ref_sample)
+    chunk = ssj.CandidateChunk(sub_C, sub_CO)
     from oracle import pyoracle as po
     if not po.ref_available():
         print(json.dumps({"impl": "reference",
@@ -231,6 +252,7 @@ def run_reference_arm(args):
         "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": desc, "sample_candidates_per_step": int(chunk.C.size),
+                   "sample": "every k-th slice of the GPU arm's batch (stratified)",
                    "strategy": "A", "workers": int(workers)},
         "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": int(workers),
                          "kind": "reference",
@@ -391,13 +413,14 @@ def main():
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            rate, cores, kind, sample, ref_count = cpu_reference_rate(coll, pred_t, chunk,
-                                                                      int(args.cpu_sample))
+            rate, cores, kind, sample, ref_count, idx = cpu_reference_rate(
+                coll, pred_t, chunk, int(args.cpu_sample))
             cpu = {"value": rate, "unit": "pairs/s", "cores": cores, "kind": kind,
-                   "sample": f"first {sample} candidates (slice-aligned) of the step's batch, "
-                             f"VerificationEngine strategy A, best of 3"}
+                   "sample": f"{sample} candidates: every k-th slice of the step's batch "
+                             f"(stratified over probe sizes), VerificationEngine strategy A, "
+                             f"best of 3"}
             # the same sample's qualifying count from the GPU flags of the timed steps
-            gpu_count = int(dF[:sample].sum().item()) if sample else 0
+            gpu_count = int(dF.cpu().numpy()[idx].sum()) if sample else 0
             parity = {"candidates": int(sample), "gpu_count": gpu_count,
                       "reference_count": int(ref_count), "match": gpu_count == int(ref_count)}
         except Exception as e:  # reported, never fatal

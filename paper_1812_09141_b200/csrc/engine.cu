@@ -280,7 +280,7 @@ int upload(ssj_engine& e, void* dst, const void* src, size_t bytes, cudaStream_t
 
 // Bitmap words reserved per chunk for strategy A's probe bitmaps (overflow falls back to
 // the merge path, so this only bounds memory, never correctness).
-uint64_t bitmap_words_for(uint64_t nC) { return std::max<uint64_t>(1ull << 20, nC / 8); }
+uint64_t bitmap_words_for(uint64_t nC) { return std::max<uint64_t>(4ull << 20, nC / 8); }
 
 int ensure_tile_scratch(ssjb::SliceDesc** slices, size_t* capS, uint32_t** bits, size_t* capB,
                         uint32_t** rank, size_t* capR, uint32_t n_slices, uint64_t nC) {

@@ -114,7 +114,10 @@ __global__ void prep_kernel(const KParams p) {
                 const uint2 rd = p.sets[probe];
                 d0.y = rd.x;
                 d0.z = rd.y;
-                if (p.bm_cap && rd.y && end >= begin && end - begin >= kSliceBitmapMinCands) {
+                // a probe bitmap pays off for long slices, and for long probes (their long
+                // candidates are verified 32 tokens per step by long_kernel)
+                if (p.bm_cap && rd.y && end > begin &&
+                    (end - begin >= kSliceBitmapMinCands || rd.y > kLongPair)) {
                     const uint32_t* r = p.tokens + (size_t)rd.x * 8;
                     const uint32_t lo = r[0] & ~31u;
                     const uint32_t nw = ((r[rd.y - 1] - lo) >> 5) + 1;
@@ -251,6 +254,7 @@ __device__ __forceinline__ bool verify_bitmap(const uint32_t* __restrict__ bits,
 //   * short slices get the probe's tokens staged in shared memory for the sequential merge.
 // Each thread's candidate descriptors are loaded up front and the first 32-byte sector of
 // candidate q+1 is in flight while candidate q is verified.
+#if !SSJB_WARP_TILES
 struct TileSlice {
     uint32_t end;     // cumulative end offset in C
     uint32_t rpos8;   // probe set position (8-token units)
@@ -513,6 +517,155 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
             *reinterpret_cast<uint32_t*>(p.flags + my0) = flag_bits[0];
         } else if (kItems == 2 && my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 1) == 0) {
             *reinterpret_cast<uint16_t*>(p.flags + my0) = (uint16_t)flag_bits[0];
+        } else {
+#pragma unroll
+            for (int q = 0; q < kItems; ++q)
+                if (my0 + q < slot1) p.flags[my0 + q] = (flag_bits[q >> 2] >> (8 * (q & 3))) & 1u;
+        }
+    }
+    acc_add(p.acc, 0, count);
+    if (kStats) {
+        acc_add(p.acc, 2, verified);
+        acc_add(p.acc, 3, prunes);
+    }
+}
+
+#endif  // !SSJB_WARP_TILES
+
+// ---------------------------------------------------------------------------------------
+// Strategy A, warp-tile form: every warp owns kTile = 32 * kItems consecutive slots and works
+// alone -- no shared memory, no CTA barriers. Lane l owns slots slot0 + l*kItems + [0, kItems)
+// (C ids in one vector load, flags in one vector store). The slices of the warp tile (first
+// one from the prep kernel's index) are read one per lane; a slot's slice is found by a
+// 5-step shuffle binary search over those ends. Slice descriptors, probe bitmaps and probe
+// tokens are read through L1 (lanes of a tile share them). Long candidates are deferred to
+// long_kernel exactly as in tile_kernel.
+template <int kOut, bool kStats>
+__global__ void __launch_bounds__(kThreadsA, kTileMinBlocks)
+    warp_tile_kernel(const KParams p, const uint32_t tile_begin, const uint32_t tile_end) {
+    constexpr int kItems = SSJB_TILE_ITEMS;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t tile = tile_begin + blockIdx.x * (kThreadsA / 32) + (threadIdx.x >> 5);
+    if (tile >= tile_end) return;  // warp-uniform
+    const uint64_t slot0 = (uint64_t)tile * kTile;
+    if (slot0 >= p.nC) return;
+    const uint64_t slot1 = min(slot0 + (uint64_t)kTile, p.nC);
+    const uint64_t my0 = slot0 + (uint64_t)lane * kItems;
+
+    uint32_t cand[kItems];
+    if (kItems % 4 == 0 && my0 + kItems <= slot1 && ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0)) {
+        const uint4* c4 = reinterpret_cast<const uint4*>(p.C + my0);
+#pragma unroll
+        for (int q = 0; q < kItems / 4; ++q) {
+            const uint4 v = __ldg(c4 + q);
+            cand[4 * q] = v.x;
+            cand[4 * q + 1] = v.y;
+            cand[4 * q + 2] = v.z;
+            cand[4 * q + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) cand[q] = my0 + q < slot1 ? __ldg(p.C + my0 + q) : 0u;
+    }
+    uint2 sd[kItems];
+#pragma unroll
+    for (int q = 0; q < kItems; ++q)
+        sd[q] = cand[q] < p.n_sets ? __ldg(p.sets + cand[q]) : make_uint2(0, 0);
+
+    const uint32_t e0 = __ldg(p.tile_first + tile);
+    uint32_t ns = 0;
+    if (e0 < p.n_slices) {
+        uint32_t e_hi = __ldg(p.tile_first + tile + 1);
+        if (e_hi >= p.n_slices) e_hi = p.n_slices - 1;
+        ns = e_hi - e0 + 1;
+    }
+    const bool small = ns <= 32;  // warp-uniform
+    const uint32_t my_end = lane < ns ? __ldg(p.C_O + 2 * ((size_t)e0 + lane) + 1) : 0xFFFFFFFFu;
+
+    uint4 nw0, nw1;
+    {
+        const uint4* s4 = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[0].x * 8);
+        nw0 = __ldg(s4);
+        nw1 = __ldg(s4 + 1);
+    }
+    unsigned count = 0, prunes = 0, verified = 0;
+    uint32_t flag_bits[(kItems + 3) / 4] = {};
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+        const uint64_t slot = my0 + q;
+        const uint4 cw0 = nw0, cw1 = nw1;
+        if (q + 1 < kItems) {
+            const uint4* s4n = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[q + 1].x * 8);
+            nw0 = __ldg(s4n);
+            nw1 = __ldg(s4n + 1);
+        }
+        // slice of this slot: number of the tile's slice ends <= slot (all lanes shuffle)
+        uint32_t li = 0;
+        if (small) {
+            const uint32_t key = (uint32_t)min(slot, (uint64_t)0xFFFFFFFEu);
+#pragma unroll
+            for (uint32_t step = 16; step > 0; step >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, my_end, li + step - 1);
+                if (v <= key) li += step;
+            }
+            const uint32_t v = __shfl_sync(0xffffffffu, my_end, li & 31);
+            if (li < 32 && v <= key) ++li;
+        }
+        bool met = false;
+        uint32_t ov = 0;
+        if (slot < slot1 && ns) {
+            const uint32_t e = small ? e0 + li : upper_bound_ends(p.C_O, e0, p.n_slices, slot);
+            if (e < p.n_slices && (!small || li < ns)) {
+                const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(p.slices + e));
+                const uint32_t m = d0.z;
+                const uint32_t* r = p.tokens + (size_t)d0.y * 8;
+                if (cand[q] >= p.n_sets) {
+                    flag_error(p.acc, kErrOutOfRange);
+                } else {
+                    const uint32_t n = sd[q].y;
+                    const uint4* s4 = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[q].x * 8);
+                    const uint64_t req = required_of(p, m, n);
+                    bool deferred = false;
+                    if (p.defer && n > kLongPair && req >= 1 && req <= (uint64_t)min(m, n)) {
+                        const unsigned long long idx = atomicAdd(p.defer_n, 1ull);
+                        if (idx < p.defer_cap) {
+                            p.defer[idx] = (uint32_t)slot;
+                            deferred = true;
+                        }
+                    }
+                    if (deferred) {
+                        // verdict, flag and stats come from long_kernel
+                    } else if (req == 0) {
+                        met = true;  // verify.hpp:57: no comparison, met = (0 >= 0)
+                        if (kOut == kOutResults)
+                            ov = full_overlap_seq(r, m, reinterpret_cast<const uint32_t*>(s4), n);
+                    } else if (req <= (uint64_t)min(m, n)) {
+                        if (d0.w != kNone) {
+                            const uint2 d1 = __ldg(reinterpret_cast<const uint2*>(p.slices + e) + 2);
+                            met = verify_bitmap<kOut == kOutResults>(
+                                p.bm_bits + d0.w, p.bm_rank + d0.w, d1.x, d1.y * 32, m, s4, n,
+                                (uint32_t)req, cw0, cw1, &ov);
+                        } else {
+                            met = merge_thread<kOut == kOutResults>(r, m, s4, n, (uint32_t)req,
+                                                                    cw0, cw1, &ov);
+                        }
+                    }
+                    if (kStats && !deferred) {
+                        ++verified;
+                        prunes += (!met && (m + n) > 0);
+                    }
+                }
+            }
+        }
+        count += met;
+        flag_bits[q >> 2] |= (met ? 1u : 0u) << (8 * (q & 3));
+        if (kOut == kOutResults) warp_append(p, met, slot, ov);
+    }
+    if (kOut == kOutFlags) {
+        if (kItems == 8 && my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 7) == 0) {
+            *reinterpret_cast<uint2*>(p.flags + my0) = make_uint2(flag_bits[0], flag_bits[1 % ((kItems + 3) / 4)]);
+        } else if (kItems == 4 && my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 3) == 0) {
+            *reinterpret_cast<uint32_t*>(p.flags + my0) = flag_bits[0];
         } else {
 #pragma unroll
             for (int q = 0; q < kItems; ++q)
@@ -890,6 +1043,21 @@ cudaError_t launch_prep(const KParams& p, cudaStream_t st, int* launches) {
 cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_begin,
                          uint32_t tile_end, cudaStream_t st) {
     if (tile_end <= tile_begin) return cudaSuccess;
+#if SSJB_WARP_TILES
+    {
+        constexpr uint32_t wpb = kThreadsA / 32;
+        const uint32_t g = (tile_end - tile_begin + wpb - 1) / wpb;
+        switch (out * 2 + (stats ? 1 : 0)) {
+            case 0: warp_tile_kernel<kOutCount, false><<<g, kThreadsA, 0, st>>>(p, tile_begin, tile_end); break;
+            case 1: warp_tile_kernel<kOutCount, true><<<g, kThreadsA, 0, st>>>(p, tile_begin, tile_end); break;
+            case 2: warp_tile_kernel<kOutFlags, false><<<g, kThreadsA, 0, st>>>(p, tile_begin, tile_end); break;
+            case 3: warp_tile_kernel<kOutFlags, true><<<g, kThreadsA, 0, st>>>(p, tile_begin, tile_end); break;
+            case 4: warp_tile_kernel<kOutResults, false><<<g, kThreadsA, 0, st>>>(p, tile_begin, tile_end); break;
+            default: warp_tile_kernel<kOutResults, true><<<g, kThreadsA, 0, st>>>(p, tile_begin, tile_end); break;
+        }
+        return cudaGetLastError();
+    }
+#else
     const uint32_t grid = tile_end - tile_begin;
     switch (out * 2 + (stats ? 1 : 0)) {
         case 0: tile_kernel<kOutCount, false><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
@@ -900,6 +1068,7 @@ cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_be
         default: tile_kernel<kOutResults, true><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
     }
     return cudaGetLastError();
+#endif
 }
 
 cudaError_t launch_long(const KParams& p, int out, bool stats, cudaStream_t st) {

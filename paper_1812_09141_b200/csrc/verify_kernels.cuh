@@ -10,16 +10,24 @@ namespace ssjb {
 
 // Tile geometry of the load-balanced thread-per-pair kernel (strategy A).
 #ifndef SSJB_TILE_THREADS
-#define SSJB_TILE_THREADS 256
+#define SSJB_TILE_THREADS 128
 #endif
 #ifndef SSJB_TILE_ITEMS
 #define SSJB_TILE_ITEMS 2
 #endif
 #ifndef SSJB_TILE_MIN_BLOCKS
-#define SSJB_TILE_MIN_BLOCKS 4
+#define SSJB_TILE_MIN_BLOCKS 8
+#endif
+#ifndef SSJB_WARP_TILES
+#define SSJB_WARP_TILES 1
 #endif
 constexpr uint32_t kThreadsA = SSJB_TILE_THREADS;            // threads per CTA
+#if SSJB_WARP_TILES
+// warp tiles: every warp owns 32 * kItems consecutive slots (no CTA-level cooperation)
+constexpr uint32_t kTile = 32 * SSJB_TILE_ITEMS;
+#else
 constexpr uint32_t kTile = SSJB_TILE_THREADS * SSJB_TILE_ITEMS;  // candidate slots per CTA
+#endif
 constexpr int kTileMinBlocks = SSJB_TILE_MIN_BLOCKS;         // CTAs per SM (register cap)
 constexpr uint32_t kMaxTileSlices = kTile / 2 < 512 ? kTile / 2 : 512;  // slices described in smem per tile
 constexpr uint32_t kTileRCap = 2048;       // probe tokens staged in shared memory per tile

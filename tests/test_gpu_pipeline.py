@@ -196,3 +196,42 @@ def test_oracle_sweep_subset(ssj, gpu, oracle, name):
                                            chunk_budget=256 << 10))
                     assert rep.count == len(truth)
                     assert np.array_equal(ssj.sorted_pairs(rep.pairs), truth)
+
+
+SHAPES = {
+    # the five BASELINE configs at oracle-sized n (same generator knobs as bench.py)
+    "cfg1": (dict(sets=3000, min_size=5, max_size=15, universe=1000, duplicate_fraction=0.10,
+                  max_edits=1, distinct_tokens=True), (9, 10)),
+    "cfg2": (dict(sets=3000, min_size=40, max_size=120, universe=7200, zipf_tokens=True,
+                  token_skew=1.0, duplicate_fraction=0.05, max_edits=2, distinct_tokens=True),
+             (4, 5)),
+    "cfg3": (dict(sets=3000, min_size=2, max_size=2500, zipf_sizes=True, size_skew=1.9,
+                  universe=41_000, zipf_tokens=True, token_skew=0.6, duplicate_fraction=0.05,
+                  max_edits=2), (3, 4)),
+    "cfg4": (dict(sets=2500, min_size=1, max_size=12_000, zipf_sizes=True, size_skew=1.3,
+                  universe=200_000, zipf_tokens=True, token_skew=1.0, duplicate_fraction=0.05,
+                  max_edits=3), (3, 5)),
+    "cfg5": (dict(sets=3000, min_size=40, max_size=120, universe=7200, zipf_tokens=True,
+                  token_skew=1.0, duplicate_fraction=0.05, max_edits=2, distinct_tokens=True),
+             (17, 20)),
+}
+
+
+@pytest.mark.parametrize("shape", sorted(SHAPES))
+def test_config_shapes_join_vs_oracle(ssj, gpu, oracle, shape):
+    """run_join over every config shape (small n) equals the brute-force oracle for every
+    algorithm, in Pairs mode (GPU pair decoding) and Count mode, several budgets."""
+    kw, (num, den) = SHAPES[shape]
+    coll = ssj.synth_collection(1234, ssj.SynthConfig(**kw))
+    tri = oracle.brute_force_join(coll.tokens, coll.offsets, oracle.pred(J, num, den))
+    truth = oracle.oracle_pairs(coll.original_id, tri)
+    for alg in ssj.Algorithm:
+        for budget, ft in ((64 << 10, 1), (ssj.KUNBOUNDED_BUDGET, 0)):
+            rep = ssj.run_join(coll, ssj.jaccard(num, den),
+                               cfg(ssj, algorithm=alg, mode=ssj.OutputMode.Pairs,
+                                   chunk_budget=budget, filter_threads=ft))
+            assert rep.count == len(truth), (shape, alg, budget)
+            assert np.array_equal(ssj.sorted_pairs(rep.pairs), truth), (shape, alg, budget)
+        rep = ssj.run_join(coll, ssj.jaccard(num, den),
+                           cfg(ssj, algorithm=alg, mode=ssj.OutputMode.Count))
+        assert rep.count == len(truth)

@@ -6,11 +6,12 @@ shift
 OUT=gpurun_out; mkdir -p $OUT
 cp paper_1812_09141_b200/libssjoin_b200.so /tmp/lib_default.so
 for v in $VARIANTS; do
-  IFS=: read T I B CP ES <<< "$v"
+  IFS=: read T I B CP ES WT <<< "$v"
   CP=${CP:-64}
   ES=${ES:-0}
+  WT=${WT:-1}
   rm -rf build/obj
-  make -s -j16 NVFLAGS_EXTRA="-DSSJB_TILE_THREADS=$T -DSSJB_TILE_ITEMS=$I -DSSJB_TILE_MIN_BLOCKS=$B -DSSJB_TILE_BM_COPY_MIN=$CP -DSSJB_EARLY_SECTOR=$ES" \
+  make -s -j16 NVFLAGS_EXTRA="-DSSJB_TILE_THREADS=$T -DSSJB_TILE_ITEMS=$I -DSSJB_TILE_MIN_BLOCKS=$B -DSSJB_TILE_BM_COPY_MIN=$CP -DSSJB_EARLY_SECTOR=$ES -DSSJB_WARP_TILES=$WT" \
        paper_1812_09141_b200/libssjoin_b200.so > /dev/null 2>&1 || { echo "build $v failed"; continue; }
   timeout 300 python bench.py --steps 10 --warmup 3 --e2e-steps 1 --cpu-sample 4e6 "$@" \
       > $OUT/tune_$v.json 2> $OUT/tune_$v.err
