@@ -48,6 +48,11 @@ METRICS = [
 ]
 
 
+SCALE = {"byte": (1, "byte"), "Kbyte": (1e3, "byte"), "Mbyte": (1e6, "byte"),
+         "Gbyte": (1e9, "byte"), "ns": (1, "ns"), "us": (1e3, "ns"), "usecond": (1e3, "ns"),
+         "ms": (1e6, "ns"), "msecond": (1e6, "ns"), "nsecond": (1, "ns")}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("report")
@@ -63,12 +68,16 @@ def main():
         for m in METRICS:
             if m in hdr:
                 v = row[hdr.index(m)]
+                u = units[hdr.index(m)]
                 try:
                     d[m] = float(v.replace(",", ""))
+                    if u in SCALE:  # normalise bytes to byte and time to ns
+                        d[m] *= SCALE[u][0]
+                        u = SCALE[u][1]
                 except ValueError:
                     d[m] = v
-                if units[hdr.index(m)]:
-                    d[m + " [unit]"] = units[hdr.index(m)]
+                if u:
+                    d[m + " [unit]"] = u
         if args.algo_bytes and "dram__bytes_read.sum" in d:
             dram = d["dram__bytes_read.sum"] + d.get("dram__bytes_write.sum", 0)
             d["dram_over_algorithmic"] = dram / args.algo_bytes
