@@ -63,6 +63,7 @@ struct DeviceScope {
 constexpr int kEventsPerSlot = 96;
 constexpr uint64_t kPieceMinSlots = 1ull << 22;  // 4M candidates = 16 MB of C per piece
 constexpr int kMaxPieces = 32;
+constexpr int kCounters = 3;  // per piece: deferred long pairs, runs, short tiles
 
 template <typename T>
 int ensure_device(T** ptr, size_t* cap, size_t need) {
@@ -116,7 +117,11 @@ struct ChunkSlot {
     size_t capR = 0;
     uint32_t* ddefer = nullptr;          // long-pair slots (strategy A)
     size_t capDf = 0;
-    unsigned long long* ddefer_n = nullptr;  // one counter per piece
+    unsigned long long* ddefer_n = nullptr;  // kCounters counters per piece
+    ssjb::RunDesc* druns = nullptr;      // runs of long slices (strategy A)
+    size_t capRu = 0;
+    uint32_t* dshort = nullptr;          // short tiles (strategy A)
+    size_t capSh = 0;
     unsigned long long* dacc = nullptr;
     unsigned long long* hacc = nullptr;  // pinned mirror of dacc
     uint8_t* hflags = nullptr;           // pinned staging for pageable flag buffers
@@ -168,7 +173,11 @@ struct ssj_engine {
     size_t dev_rank_cap = 0;
     uint32_t* dev_defer = nullptr;
     size_t dev_defer_cap = 0;
-    unsigned long long* dev_defer_n = nullptr;
+    unsigned long long* dev_defer_n = nullptr;  // kCounters
+    ssjb::RunDesc* dev_runs = nullptr;
+    size_t dev_runs_cap = 0;
+    uint32_t* dev_short = nullptr;
+    size_t dev_short_cap = 0;
     // results mode
     uint32_t* d_res_slots = nullptr;
     uint32_t* d_res_ov = nullptr;
@@ -339,6 +348,8 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
                                            &s.capR, n_slices, nC)))
         return rc;
     if (tiles && (rc = ensure_device(&s.ddefer, &s.capDf, std::max<size_t>(nC, 1)))) return rc;
+    if (tiles && (rc = ensure_device(&s.druns, &s.capRu, 2 * (size_t)n_tiles + 2))) return rc;
+    if (tiles && (rc = ensure_device(&s.dshort, &s.capSh, (size_t)n_tiles + 1))) return rc;
     if (out == ssjb::kOutResults) {
         if ((rc = ensure_device(&e.d_res_slots, &e.res_cap, nC))) return rc;
         if ((rc = ensure_device(&e.d_res_ov, &e.res_cap2, nC))) return rc;
@@ -381,7 +392,9 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
     int ev = 0;
     int turn = 0;
     SSJ_CK(cudaMemsetAsync(s.dacc, 0, SSJ_RESULT_WORDS * sizeof(unsigned long long), e.s_comp));
-    if (tiles) SSJ_CK(cudaMemsetAsync(s.ddefer_n, 0, kMaxPieces * sizeof(unsigned long long), e.s_comp));
+    if (tiles)
+        SSJ_CK(cudaMemsetAsync(s.ddefer_n, 0, kCounters * kMaxPieces * sizeof(unsigned long long),
+                               e.s_comp));
     if (out == ssjb::kOutResults)
         SSJ_CK(cudaMemsetAsync(e.d_res_n, 0, sizeof(unsigned long long), e.s_comp));
     if ((rc = upload(e, s.dCO, C_O, (size_t)n_slices * 2 * sizeof(uint32_t), e.s_comp, co_pinned,
@@ -394,7 +407,7 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
     uint64_t piece = nC;
     if (e.strategy.kind == SSJ_STRATEGY_A) {
         piece = std::max<uint64_t>(kPieceMinSlots, (nC + kMaxPieces - 1) / kMaxPieces);
-        piece = (piece + ssjb::kTile - 1) / ssjb::kTile * ssjb::kTile;
+        piece = (piece + ssjb::kRun - 1) / ssjb::kRun * ssjb::kRun;  // runs never straddle pieces
     }
     if (piece == 0) piece = 1;
     for (uint64_t lo = 0; lo < nC || (lo == 0 && nC == 0); lo += piece) {
@@ -412,8 +425,14 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
         if (tiles) {  // this piece's long pairs: their own segment and counter
             const int pc = (int)(lo / piece);
             p.defer = s.ddefer + lo;
-            p.defer_n = s.ddefer_n + pc;
+            p.defer_n = s.ddefer_n + kCounters * pc;
             p.defer_cap = hi - lo;
+            p.runs = s.druns + 2 * (size_t)t0;
+            p.runs_n = s.ddefer_n + kCounters * pc + 1;
+            p.runs_cap = 2 * (uint64_t)(t1 - t0);
+            p.short_tiles = s.dshort + t0;
+            p.short_n = s.ddefer_n + kCounters * pc + 2;
+            p.short_cap = t1 - t0;
         }
         SSJ_CK(launch_strategy(e, p, out, t0, t1, e.s_comp));
         if (out == ssjb::kOutFlags && hi > lo) {
@@ -459,6 +478,8 @@ void destroy_slot(ChunkSlot& s) {
     cudaFree(s.drank);
     cudaFree(s.ddefer);
     cudaFree(s.ddefer_n);
+    cudaFree(s.druns);
+    cudaFree(s.dshort);
     cudaFree(s.dacc);
     cudaFreeHost(s.hacc);
     cudaFreeHost(s.hflags);
@@ -475,7 +496,7 @@ int init_engine_runtime(ssj_engine& e) {
         for (auto& ev : s.ev) SSJ_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         SSJ_CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
         SSJ_CK(cudaMalloc(&s.dacc, SSJ_RESULT_WORDS * sizeof(unsigned long long)));
-        SSJ_CK(cudaMalloc(&s.ddefer_n, kMaxPieces * sizeof(unsigned long long)));
+        SSJ_CK(cudaMalloc(&s.ddefer_n, kCounters * kMaxPieces * sizeof(unsigned long long)));
         SSJ_CK(cudaHostAlloc(&s.hacc, SSJ_RESULT_WORDS * sizeof(unsigned long long),
                              cudaHostAllocDefault));
     }
@@ -758,6 +779,8 @@ void ssj_engine_destroy(ssj_engine* e) {
     cudaFree(e->dev_rank);
     cudaFree(e->dev_defer);
     cudaFree(e->dev_defer_n);
+    cudaFree(e->dev_runs);
+    cudaFree(e->dev_short);
     cudaFree(e->d_req_tab);
     cudaFree(e->d_res_slots);
     cudaFree(e->d_res_ov);
@@ -958,7 +981,12 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
         return rc;
     if (tiles && (rc = ensure_device(&e->dev_defer, &e->dev_defer_cap, std::max<size_t>(nC, 1))))
         return rc;
-    if (tiles && !e->dev_defer_n) SSJ_CK(cudaMalloc(&e->dev_defer_n, sizeof(unsigned long long)));
+    if (tiles && !e->dev_defer_n)
+        SSJ_CK(cudaMalloc(&e->dev_defer_n, kCounters * sizeof(unsigned long long)));
+    if (tiles && (rc = ensure_device(&e->dev_runs, &e->dev_runs_cap, 2 * (size_t)n_tiles + 2)))
+        return rc;
+    if (tiles && (rc = ensure_device(&e->dev_short, &e->dev_short_cap, (size_t)n_tiles + 1)))
+        return rc;
     KParams p = base_params(*e);
     p.C = d_C;
     p.nC = nC;
@@ -976,10 +1004,16 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
         p.defer = e->dev_defer;
         p.defer_n = e->dev_defer_n;
         p.defer_cap = nC;
+        p.runs = e->dev_runs;
+        p.runs_n = e->dev_defer_n + 1;
+        p.runs_cap = 2 * (uint64_t)n_tiles;
+        p.short_tiles = e->dev_short;
+        p.short_n = e->dev_defer_n + 2;
+        p.short_cap = n_tiles;
     }
     const int out = (e->mode == SSJ_MODE_PAIRS && d_flags) ? ssjb::kOutFlags : ssjb::kOutCount;
     SSJ_CK(cudaMemsetAsync(d_result, 0, SSJ_RESULT_WORDS * sizeof(uint64_t), st));
-    if (tiles) SSJ_CK(cudaMemsetAsync(e->dev_defer_n, 0, sizeof(unsigned long long), st));
+    if (tiles) SSJ_CK(cudaMemsetAsync(e->dev_defer_n, 0, kCounters * sizeof(unsigned long long), st));
     SSJ_CK(ssjb::launch_prep(p, st));
     cudaEvent_t k0 = nullptr, k1 = nullptr;
     if (e->profiling) {
@@ -1035,11 +1069,10 @@ int ssj_engine_export_collection(const ssj_engine* e, uint32_t* d_tokens, uint32
 }
 
 int ssj_launches_per_chunk(const ssj_engine* e, uint64_t nC, uint64_t nCO) {
-    (void)nC;
-    // prep (+ probe bitmaps for strategy A when there are slices) + one verification kernel;
-    // the memset of the result block is not a kernel of ours
-    // strategy A: prep, probe bitmaps (when there are slices), tiles, long pairs
-    if (e && e->strategy.kind == SSJ_STRATEGY_A) return nCO >= 2 ? 4 : 3;
+    // prep + one verification kernel (B, C); the memset of the result block is not ours.
+    // Strategy A: prep, probe bitmaps (when there are slices), then per chunk segment the
+    // run list, run_kernel and warp_tile_kernel (when there are slots), and long pairs.
+    if (e && e->strategy.kind == SSJ_STRATEGY_A) return (nCO >= 2 ? 2 : 1) + (nC ? 3 : 0) + 1;
     return 2;
 }
 

@@ -26,6 +26,10 @@ namespace ssjb {
 namespace {
 
 
+__host__ __device__ __forceinline__ uint32_t bitmap_alloc_words(uint32_t nw) {
+    return (nw + 4u) & ~3u;
+}
+
 __device__ __forceinline__ void acc_add(unsigned long long* acc, int word, unsigned v) {
     const unsigned w = __reduce_add_sync(0xffffffffu, v);
     if ((threadIdx.x & 31) == 0 && w) atomicAdd(acc + word, (unsigned long long)w);
@@ -120,10 +124,15 @@ __global__ void prep_kernel(const KParams p) {
                     (end - begin >= kSliceBitmapMinCands || rd.y > kLongPair)) {
                     const uint32_t* r = p.tokens + (size_t)rd.x * 8;
                     const uint32_t lo = r[0] & ~31u;
-                    const uint32_t nw = ((r[rd.y - 1] - lo) >> 5) + 1;
-                    if (nw <= kMaxBitmapWords) {
-                        const unsigned long long off = atomicAdd(p.acc + kAccBitmapWords, (unsigned long long)nw);
-                        if (off + nw <= p.bm_cap) {
+                    const uint32_t hi = r[rd.y - 1];
+                    const uint32_t nw = ((hi - lo) >> 5) + 1;
+                    // allocation: the words plus at least one zero word (clamped lookups of
+                    // tokens beyond the range land there), rounded to 16 bytes for cp.async;
+                    // no bitmap when the probe holds token 0xFFFFFFFF (the padding value)
+                    const uint32_t na = bitmap_alloc_words(nw);
+                    if (nw <= kMaxBitmapWords && hi != 0xFFFFFFFFu) {
+                        const unsigned long long off = atomicAdd(p.acc + kAccBitmapWords, (unsigned long long)na);
+                        if (off + na <= p.bm_cap) {
                             d0.w = (uint32_t)off;
                             d1.x = lo;
                             d1.y = nw;
@@ -156,7 +165,7 @@ __global__ void bitmap_kernel(const KParams p) {
         uint32_t* bits = p.bm_bits + d0.w;
         uint32_t* rank = p.bm_rank + d0.w;
         const uint32_t lo = d1.x, nw = d1.y;
-        for (uint32_t w = lane; w < nw; w += 32) bits[w] = 0;
+        for (uint32_t w = lane; w < bitmap_alloc_words(nw); w += 32) bits[w] = 0;
         __syncwarp();
         const uint32_t* r = p.tokens + (size_t)d0.y * 8;
         for (uint32_t u = lane; u < d0.z; u += 32) {
@@ -241,296 +250,6 @@ __device__ __forceinline__ bool verify_bitmap(const uint32_t* __restrict__ bits,
     return ov >= req;
 }
 
-// ---------------------------------------------------------------------------------------
-// Strategy A: load-balanced thread-per-pair over fixed slot tiles.
-//
-// A CTA owns kTile consecutive slots; thread t owns the kItems consecutive slots
-// slot0 + t*kItems + [0, kItems) ("blocked"): its C ids arrive in 16-byte loads, its flags
-// leave in one 8-byte store. The slot -> slice map of the tile is a block-wide inclusive
-// scan over "a slice ends here" marks. Per slice of the tile:
-//   * a probe bitmap built once per chunk (bitmap_kernel) is used when the slice is long;
-//     with >= kTileBitmapMinCands candidates in this tile it is copied to shared memory,
-//     otherwise read through L1 -- O(1) per candidate token, no merge with the probe;
-//   * short slices get the probe's tokens staged in shared memory for the sequential merge.
-// Each thread's candidate descriptors are loaded up front and the first 32-byte sector of
-// candidate q+1 is in flight while candidate q is verified.
-#if !SSJB_WARP_TILES
-struct TileSlice {
-    uint32_t end;     // cumulative end offset in C
-    uint32_t rpos8;   // probe set position (8-token units)
-    uint32_t rsize;   // |r|
-    uint32_t rofs;    // staged probe tokens in sh_r, or kNone
-    uint32_t gbofs;   // probe bitmap in global memory, or kNone
-    uint32_t lo;      // bitmap base token
-    uint32_t nwords;  // bitmap words
-    uint32_t sofs;    // bitmap copy in shared memory, or kNone
-};
-
-template <int kOut, bool kStats>
-__global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const KParams p, const uint32_t tile_begin) {
-    constexpr int kItems = kTile / kThreadsA;
-    constexpr int kSliceItems = kMaxTileSlices / kThreadsA;
-    static_assert(kSliceItems >= 1, "kMaxTileSlices >= kThreadsA");
-    static_assert(kTileBitmapWords * 2 >= kTile, "marks alias the bitmap region");
-    using Scan = cub::BlockScan<uint32_t, kThreadsA>;
-    __shared__ TileSlice sh_sl[kMaxTileSlices];
-    __shared__ __align__(16) uint32_t sh_bits[kTileBitmapWords];
-    __shared__ __align__(16) uint32_t sh_rank[kTileBitmapWords];
-    __shared__ __align__(16) uint32_t sh_r[kTileRCap];
-    __shared__ typename Scan::TempStorage scan_tmp;
-    uint32_t* sh_mark = sh_bits;  // [kTile] marks alias bits+rank (consumed before the copy)
-
-    const uint32_t tile = tile_begin + blockIdx.x;
-    const uint64_t slot0 = (uint64_t)tile * kTile;
-    if (slot0 >= p.nC) return;
-    const uint64_t slot1 = min(slot0 + (uint64_t)kTile, p.nC);
-    const uint32_t e0 = p.tile_first[tile];
-    const uint32_t tid = threadIdx.x;
-    const uint64_t my0 = slot0 + (uint64_t)tid * kItems;
-
-    // 1. this thread's candidate ids and their set descriptors (independent of the slices)
-    uint32_t cand[kItems];
-    if (kItems % 4 == 0 && my0 + kItems <= slot1 &&
-        ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0)) {
-        const uint4* c4 = reinterpret_cast<const uint4*>(p.C + my0);
-#pragma unroll
-        for (int q = 0; q < kItems / 4; ++q) {
-            const uint4 v = __ldg(c4 + q);
-            cand[4 * q] = v.x;
-            cand[4 * q + 1] = v.y;
-            cand[4 * q + 2] = v.z;
-            cand[4 * q + 3] = v.w;
-        }
-    } else if (kItems % 2 == 0 && my0 + kItems <= slot1 &&
-               ((reinterpret_cast<uintptr_t>(p.C) & 7) == 0)) {
-        const uint2* c2 = reinterpret_cast<const uint2*>(p.C + my0);
-#pragma unroll
-        for (int q = 0; q < kItems / 2; ++q) {
-            const uint2 v = __ldg(c2 + q);
-            cand[2 * q] = v.x;
-            cand[2 * q + 1] = v.y;
-        }
-    } else {
-#pragma unroll
-        for (int q = 0; q < kItems; ++q) cand[q] = my0 + q < slot1 ? __ldg(p.C + my0 + q) : 0u;
-    }
-    uint2 sd[kItems];
-#pragma unroll
-    for (int q = 0; q < kItems; ++q)
-        sd[q] = cand[q] < p.n_sets ? __ldg(p.sets + cand[q]) : make_uint2(0, 0);
-
-#if SSJB_EARLY_SECTOR
-    // 2. (issued before the slice setup) first 32-byte sector of the first candidate; the loop below prefetches item q+1's
-    //    sector before verifying item q
-    uint4 nw0, nw1;
-    {
-        const uint4* s4 = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[0].x * 8);
-        nw0 = __ldg(s4);
-        nw1 = __ldg(s4 + 1);
-    }
-
-#endif
-    uint32_t ns = 0;
-    bool fast = false;
-    if (e0 < p.n_slices) {
-        uint32_t e_hi = p.tile_first[tile + 1];
-        if (e_hi >= p.n_slices) e_hi = p.n_slices - 1;
-        ns = e_hi - e0 + 1;
-        fast = ns <= kMaxTileSlices;
-    }
-
-    uint32_t li[kItems];  // tile-local slice of each item; ns = not covered
-    if (fast) {
-#pragma unroll
-        for (int q = 0; q < kItems; ++q) sh_mark[tid * kItems + q] = 0;
-        __syncthreads();
-        uint32_t padded[kSliceItems], words[kSliceItems];
-#pragma unroll
-        for (int q = 0; q < kSliceItems; ++q) {
-            const uint32_t k = tid * kSliceItems + q;
-            padded[q] = 0;
-            words[q] = 0;
-            if (k < ns) {
-                const size_t e = (size_t)e0 + k;
-                const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(p.slices + e));
-                const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(p.slices + e) + 1);
-                const uint32_t begin = e ? __ldg(p.C_O + 2 * e - 1) : 0u;
-                TileSlice ts;
-                ts.end = d0.x;
-                ts.rpos8 = d0.y;
-                ts.rsize = d0.z;
-                ts.gbofs = d0.w;
-                ts.lo = d1.x;
-                ts.nwords = d1.y;
-                const uint64_t cb = max((uint64_t)begin, slot0), ce = min((uint64_t)d0.x, slot1);
-                const uint32_t cands = ce > cb ? (uint32_t)(ce - cb) : 0u;
-                if (d0.w != kNone) {
-                    if (cands >= kTileBitmapMinCands) words[q] = d1.y;
-                } else {
-                    padded[q] = (d0.z + 7u) & ~7u;
-                }
-                sh_sl[k] = ts;
-                if ((uint64_t)d0.x > slot0 && (uint64_t)d0.x < slot1) atomicAdd(&sh_mark[d0.x - slot0], 1u);
-            }
-        }
-        uint32_t rofs[kSliceItems], sofs[kSliceItems];
-        Scan(scan_tmp).ExclusiveSum(padded, rofs);
-        __syncthreads();
-        Scan(scan_tmp).ExclusiveSum(words, sofs);
-#pragma unroll
-        for (int q = 0; q < kSliceItems; ++q) {
-            const uint32_t k = tid * kSliceItems + q;
-            if (k < ns) {
-                sh_sl[k].rofs = (padded[q] && rofs[q] + padded[q] <= kTileRCap) ? rofs[q] : kNone;
-                sh_sl[k].sofs = (words[q] && sofs[q] + words[q] <= kTileBitmapWords) ? sofs[q] : kNone;
-            }
-        }
-        __syncthreads();
-        uint32_t marks[kItems];
-#pragma unroll
-        for (int q = 0; q < kItems; ++q) marks[q] = sh_mark[tid * kItems + q];
-        __syncthreads();  // scan_tmp reuse; marks consumed
-        Scan(scan_tmp).InclusiveSum(marks, li);
-        // Copy long slices' bitmaps and stage short slices' probes: one warp per slice.
-        const uint32_t warp = tid >> 5, lane = tid & 31;
-        for (uint32_t k = warp; k < ns; k += kThreadsA / 32) {
-            const TileSlice ts = sh_sl[k];
-            if (ts.sofs != kNone) {
-                for (uint32_t w = lane; w < ts.nwords; w += 32) {
-                    sh_bits[ts.sofs + w] = __ldg(p.bm_bits + ts.gbofs + w);
-                    sh_rank[ts.sofs + w] = __ldg(p.bm_rank + ts.gbofs + w);
-                }
-            } else if (ts.rofs != kNone) {
-                const uint4* src = reinterpret_cast<const uint4*>(p.tokens + (size_t)ts.rpos8 * 8);
-                uint4* dst = reinterpret_cast<uint4*>(sh_r + ts.rofs);
-                const uint32_t units = ((ts.rsize + 7u) & ~7u) >> 2;
-                for (uint32_t u = lane; u < units; u += 32) dst[u] = __ldg(src + u);
-            }
-        }
-        __syncthreads();
-    } else {
-#pragma unroll
-        for (int q = 0; q < kItems; ++q) li[q] = 0;
-    }
-
-#if !SSJB_EARLY_SECTOR
-    uint4 nw0, nw1;
-    {
-        const uint4* s4 = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[0].x * 8);
-        nw0 = __ldg(s4);
-        nw1 = __ldg(s4 + 1);
-    }
-#endif
-
-    // 3. verification
-    unsigned count = 0, prunes = 0, verified = 0;
-    uint32_t flag_bits[(kItems + 3) / 4] = {};
-#pragma unroll
-    for (int q = 0; q < kItems; ++q) {
-        const uint64_t slot = my0 + q;
-        const uint4 cw0 = nw0, cw1 = nw1;
-        if (q + 1 < kItems) {
-            const uint4* s4n = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[q + 1].x * 8);
-            nw0 = __ldg(s4n);
-            nw1 = __ldg(s4n + 1);
-        }
-        bool met = false;
-        uint32_t ov = 0;
-        if (slot < slot1 && e0 < p.n_slices) {
-            const uint32_t* r = nullptr;
-            const uint32_t* bits = nullptr;
-            const uint32_t* rank = nullptr;
-            uint32_t m = 0, lo = 0, nbits = 0;
-            bool covered;
-            if (fast) {
-                covered = li[q] < ns;
-                if (covered) {
-                    const TileSlice& ts = sh_sl[li[q]];
-                    m = ts.rsize;
-                    if (ts.sofs != kNone) {
-                        bits = sh_bits + ts.sofs;
-                        rank = sh_rank + ts.sofs;
-                    } else if (ts.gbofs != kNone) {
-                        bits = p.bm_bits + ts.gbofs;
-                        rank = p.bm_rank + ts.gbofs;
-                    }
-                    lo = ts.lo;
-                    nbits = ts.nwords * 32;
-                    r = ts.rofs != kNone ? sh_r + ts.rofs : p.tokens + (size_t)ts.rpos8 * 8;
-                }
-            } else {
-                const uint32_t e = upper_bound_ends(p.C_O, e0, p.n_slices, slot);
-                covered = e < p.n_slices;
-                if (covered) {
-                    const uint32_t probe = __ldg(p.C_O + 2 * (size_t)e);
-                    const uint2 rd = probe < p.n_sets ? __ldg(p.sets + probe) : make_uint2(0, 0);
-                    m = rd.y;
-                    r = p.tokens + (size_t)rd.x * 8;
-                }
-            }
-            if (covered) {
-                if (cand[q] >= p.n_sets) {
-                    flag_error(p.acc, kErrOutOfRange);
-                } else {
-                    const uint32_t n = sd[q].y;
-                    const uint4* s4 = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[q].x * 8);
-                    const uint64_t req = required_of(p, m, n);
-                    bool deferred = false;
-                    if (p.defer && n > kLongPair && req >= 1 && req <= (uint64_t)min(m, n)) {
-                        // long pair: hand it to long_kernel (one warp per pair)
-                        const unsigned long long idx = atomicAdd(p.defer_n, 1ull);
-                        if (idx < p.defer_cap) {
-                            p.defer[idx] = (uint32_t)slot;
-                            deferred = true;
-                        }
-                    }
-                    if (deferred) {
-                        // verdict, flag and stats come from long_kernel
-                    } else if (req == 0) {
-                        met = true;  // verify.hpp:57: no comparison, met = (0 >= 0)
-                        if (kOut == kOutResults)
-                            ov = full_overlap_seq(r, m, reinterpret_cast<const uint32_t*>(s4), n);
-                    } else if (req <= (uint64_t)min(m, n)) {
-                        if (bits) {
-                            met = verify_bitmap<kOut == kOutResults>(bits, rank, lo, nbits, m, s4, n,
-                                                                     (uint32_t)req, cw0, cw1, &ov);
-                        } else {
-                            met = merge_thread<kOut == kOutResults>(r, m, s4, n, (uint32_t)req,
-                                                                    cw0, cw1, &ov);
-                        }
-                    }
-                    if (kStats && !deferred) {
-                        ++verified;
-                        prunes += (!met && (m + n) > 0);
-                    }
-                }
-            }
-        }
-        count += met;
-        flag_bits[q >> 2] |= (met ? 1u : 0u) << (8 * (q & 3));
-        if (kOut == kOutResults) warp_append(p, met, slot, ov);
-    }
-    if (kOut == kOutFlags) {
-        if (kItems == 8 && my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 7) == 0) {
-            *reinterpret_cast<uint2*>(p.flags + my0) = make_uint2(flag_bits[0], flag_bits[1]);
-        } else if (kItems == 4 && my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 3) == 0) {
-            *reinterpret_cast<uint32_t*>(p.flags + my0) = flag_bits[0];
-        } else if (kItems == 2 && my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 1) == 0) {
-            *reinterpret_cast<uint16_t*>(p.flags + my0) = (uint16_t)flag_bits[0];
-        } else {
-#pragma unroll
-            for (int q = 0; q < kItems; ++q)
-                if (my0 + q < slot1) p.flags[my0 + q] = (flag_bits[q >> 2] >> (8 * (q & 3))) & 1u;
-        }
-    }
-    acc_add(p.acc, 0, count);
-    if (kStats) {
-        acc_add(p.acc, 2, verified);
-        acc_add(p.acc, 3, prunes);
-    }
-}
-
-#endif  // !SSJB_WARP_TILES
 
 // ---------------------------------------------------------------------------------------
 // Strategy A, warp-tile form: every warp owns kTile = 32 * kItems consecutive slots and works
@@ -541,12 +260,10 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) tile_kernel(const K
 // tokens are read through L1 (lanes of a tile share them). Long candidates are deferred to
 // long_kernel exactly as in tile_kernel.
 template <int kOut, bool kStats>
-__global__ void __launch_bounds__(kThreadsA, kTileMinBlocks)
-    warp_tile_kernel(const KParams p, const uint32_t tile_begin, const uint32_t tile_end) {
+__device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile, unsigned& count,
+                                          unsigned& prunes, unsigned& verified) {
     constexpr int kItems = SSJB_TILE_ITEMS;
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t tile = tile_begin + blockIdx.x * (kThreadsA / 32) + (threadIdx.x >> 5);
-    if (tile >= tile_end) return;  // warp-uniform
     const uint64_t slot0 = (uint64_t)tile * kTile;
     if (slot0 >= p.nC) return;
     const uint64_t slot1 = min(slot0 + (uint64_t)kTile, p.nC);
@@ -581,6 +298,7 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks)
     }
     const bool small = ns <= 32;  // warp-uniform
     const uint32_t my_end = lane < ns ? __ldg(p.C_O + 2 * ((size_t)e0 + lane) + 1) : 0xFFFFFFFFu;
+    const uint32_t beg0 = (e0 && e0 < p.n_slices) ? __ldg(p.C_O + 2 * (size_t)e0 - 1) : 0u;
 
     uint4 nw0, nw1;
     {
@@ -588,8 +306,8 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks)
         nw0 = __ldg(s4);
         nw1 = __ldg(s4 + 1);
     }
-    unsigned count = 0, prunes = 0, verified = 0;
     uint32_t flag_bits[(kItems + 3) / 4] = {};
+    bool all_written = true;
 #pragma unroll
     for (int q = 0; q < kItems; ++q) {
         const uint64_t slot = my0 + q;
@@ -601,6 +319,7 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks)
         }
         // slice of this slot: number of the tile's slice ends <= slot (all lanes shuffle)
         uint32_t li = 0;
+        uint32_t s_end = 0, s_beg = 0;
         if (small) {
             const uint32_t key = (uint32_t)min(slot, (uint64_t)0xFFFFFFFEu);
 #pragma unroll
@@ -610,12 +329,28 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks)
             }
             const uint32_t v = __shfl_sync(0xffffffffu, my_end, li & 31);
             if (li < 32 && v <= key) ++li;
+            s_end = __shfl_sync(0xffffffffu, my_end, li & 31);
+            const uint32_t pe = __shfl_sync(0xffffffffu, my_end, (li - 1) & 31);
+            s_beg = li ? pe : beg0;
         }
-        bool met = false;
+        bool met = false, written = false;
         uint32_t ov = 0;
         if (slot < slot1 && ns) {
-            const uint32_t e = small ? e0 + li : upper_bound_ends(p.C_O, e0, p.n_slices, slot);
-            if (e < p.n_slices && (!small || li < ns)) {
+            uint32_t e = e0 + li;
+            if (!small) {
+                e = upper_bound_ends(p.C_O, e0, p.n_slices, slot);
+                if (e < p.n_slices) {
+                    s_end = __ldg(p.C_O + 2 * (size_t)e + 1);
+                    s_beg = e ? __ldg(p.C_O + 2 * (size_t)e - 1) : 0u;
+                }
+            }
+            // slots of slices with >= kRunMinSlice candidates belong to run_kernel
+            const bool in_run = e < p.n_slices && (!small || li < ns) && s_end > s_beg &&
+                                min((uint64_t)s_end, p.nC) - s_beg >= kRunMinSlice;
+            if (in_run) {
+                // flag written by run_kernel
+            } else if (e < p.n_slices && (!small || li < ns)) {
+                written = true;
                 const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(p.slices + e));
                 const uint32_t m = d0.z;
                 const uint32_t* r = p.tokens + (size_t)d0.y * 8;
@@ -631,6 +366,7 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks)
                         if (idx < p.defer_cap) {
                             p.defer[idx] = (uint32_t)slot;
                             deferred = true;
+                            written = false;  // long_kernel writes it
                         }
                     }
                     if (deferred) {
@@ -655,22 +391,391 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks)
                         prunes += (!met && (m + n) > 0);
                     }
                 }
+            } else {
+                written = true;  // slot past the last slice: never verified, flag 0
             }
         }
+        all_written = all_written && (written || slot >= slot1);
         count += met;
         flag_bits[q >> 2] |= (met ? 1u : 0u) << (8 * (q & 3));
+        if (kOut == kOutFlags && !written && slot < slot1) flag_bits[q >> 2] |= 0x80u << (8 * (q & 3));
         if (kOut == kOutResults) warp_append(p, met, slot, ov);
     }
     if (kOut == kOutFlags) {
-        if (kItems == 8 && my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 7) == 0) {
+        if (all_written && kItems == 8 && my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 7) == 0) {
             *reinterpret_cast<uint2*>(p.flags + my0) = make_uint2(flag_bits[0], flag_bits[1 % ((kItems + 3) / 4)]);
-        } else if (kItems == 4 && my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 3) == 0) {
+        } else if (all_written && kItems == 4 && my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 3) == 0) {
             *reinterpret_cast<uint32_t*>(p.flags + my0) = flag_bits[0];
+        } else if (all_written && kItems == 2 && my0 + kItems <= slot1 && (((uintptr_t)(p.flags + my0)) & 1) == 0) {
+            *reinterpret_cast<uint16_t*>(p.flags + my0) = (uint16_t)flag_bits[0];
         } else {
 #pragma unroll
-            for (int q = 0; q < kItems; ++q)
-                if (my0 + q < slot1) p.flags[my0 + q] = (flag_bits[q >> 2] >> (8 * (q & 3))) & 1u;
+            for (int q = 0; q < kItems; ++q) {
+                const uint32_t f = (flag_bits[q >> 2] >> (8 * (q & 3))) & 0xFFu;
+                if (my0 + q < slot1 && !(f & 0x80u)) p.flags[my0 + q] = f & 1u;
+            }
         }
+    }
+}
+
+// Strategy A, warp-tile form: every warp owns kTile = 32 * kItems consecutive slots and works
+// alone -- no shared memory, no CTA barriers. Lane l owns slots slot0 + l*kItems + [0, kItems)
+// (C ids in one vector load, flags in one vector store). The slices of the warp tile (first
+// one from the prep kernel's index) are read one per lane; a slot's slice is found by a
+// 5-step shuffle binary search over those ends. Slice descriptors, probe bitmaps and probe
+// tokens are read through L1 (lanes of a tile share them). Long candidates are deferred to
+// long_kernel. Persistent over the segment's short-tile list; slots of slices with
+// >= kRunMinSlice candidates are left to run_kernel.
+template <int kOut, bool kStats>
+__global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) warp_tile_kernel(const KParams p) {
+    const uint64_t n = min((uint64_t)*p.short_n, p.short_cap);
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned count = 0, prunes = 0, verified = 0;
+    for (uint64_t w = gw; w < n; w += n_warps)
+        warp_tile<kOut, kStats>(p, __ldg(p.short_tiles + w), count, prunes, verified);
+    acc_add(p.acc, 0, count);
+    if (kStats) {
+        acc_add(p.acc, 2, verified);
+        acc_add(p.acc, 3, prunes);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Strategy A, long slices: runs.
+//
+// runs_gen_kernel (thread per tile of this segment): walks the tile's slices; for every
+// slice with >= kRunMinSlice candidates it emits the run (slice, kRun-aligned block) whose
+// first slot lies in this tile (at most two per tile: one long slice can begin in a 64-slot
+// tile, and the first tile of a block also starts the run of the slice entering the block);
+// a tile holding any short-slice slot or uncovered slot goes to the short-tile list.
+__global__ void runs_gen_kernel(const KParams p, const uint32_t tile_begin,
+                                const uint32_t tile_end) {
+    const uint32_t t = tile_begin + blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= tile_end) return;
+    const uint64_t slot0 = (uint64_t)t * kTile;
+    if (slot0 >= p.nC) return;
+    const uint64_t slot1 = min(slot0 + (uint64_t)kTile, p.nC);
+    const uint64_t blk0 = slot0 / kRun * kRun;
+    const uint64_t blk1 = min(blk0 + (uint64_t)kRun, p.nC);
+    uint32_t e = __ldg(p.tile_first + t);
+    uint64_t b = e ? min((uint64_t)__ldg(p.C_O + 2 * (size_t)e - 1), p.nC) : 0;  // decode: begin = previous end
+    uint64_t covered = slot0;
+    bool has_short = false;
+    for (; e < p.n_slices; ++e) {
+        if (b >= slot1) break;
+        const uint64_t end = min((uint64_t)__ldg(p.C_O + 2 * (size_t)e + 1), p.nC);
+        if (end > b && end > slot0) {
+            if (end - b >= kRunMinSlice) {
+                const uint64_t rb = max(b, blk0);
+                if (rb >= slot0 && rb < slot1) {
+                    const unsigned long long k = atomicAdd(p.runs_n, 1ull);
+                    if (k < p.runs_cap) {
+                        RunDesc d;
+                        d.slice = e;
+                        d.begin = (uint32_t)rb;
+                        d.end = (uint32_t)min(end, blk1);
+                        d.pad = 0;
+                        p.runs[k] = d;
+                    }
+                }
+            } else {
+                has_short = true;
+            }
+            covered = max(covered, end);
+        }
+        b = max(b, end);
+    }
+    if (covered < slot1) has_short = true;  // slots past the last slice (flag 0)
+    if (has_short) {
+        const unsigned long long k = atomicAdd(p.short_n, 1ull);
+        if (k < p.short_cap) p.short_tiles[k] = t;
+    }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// 8 consecutive tokens (32 bytes, 32-byte aligned) in one 256-bit load.
+__device__ __forceinline__ void ld_tokens8(const uint32_t* __restrict__ s, uint32_t t[8]) {
+    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]),
+                   "=r"(t[6]), "=r"(t[7])
+                 : "l"(s));
+}
+
+// Membership-bitmap verification with clamped lookups: word nwords of `bits` is zero and
+// every token outside [lo, lo + nbits) -- including the 0xFFFFFFFF padding after |s| -- is
+// clamped onto it, so a block of 8 tokens costs 8 unconditional lookups. After each block
+// the merge position is exact (j = tokens of s consumed, i = probe tokens <= the block's
+// last token, from rank), so the reference's bound (verify.hpp:58) is evaluated there;
+// verdicts are bit-exact (see ssj_device.cuh). kGlobal: bits/rank in global memory (read
+// through L1), else shared memory. t: s[0..8) already loaded.
+template <bool kFull, bool kGlobal>
+__device__ __forceinline__ bool bm_verify(const uint32_t* __restrict__ bits,
+                                          const uint32_t* __restrict__ rank, uint32_t lo,
+                                          uint32_t nbits, uint32_t m,
+                                          const uint32_t* __restrict__ s, uint32_t n,
+                                          uint32_t req, uint32_t t[8], uint32_t* ov_out) {
+    const uint32_t slack_r = m - req, slack_s = n - req;
+    uint32_t ov = 0, j = 0;
+    for (;;) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t d = min(t[q] - lo, nbits);
+            const uint32_t w = kGlobal ? __ldg(bits + (d >> 5)) : bits[d >> 5];
+            ov += (w >> (d & 31)) & 1u;
+        }
+        j += 8;
+        if (j >= n) break;  // s exhausted (padding never matches): the verdict is ov >= req
+        if (!kFull && ov >= req) break;
+        if (ov < req) {
+            const uint32_t d = t[7] - lo;
+            uint32_t i;
+            if (t[7] < lo) {
+                i = 0;
+            } else if (d >= nbits) {
+                i = m;
+            } else {
+                const uint32_t w = kGlobal ? __ldg(bits + (d >> 5)) : bits[d >> 5];
+                const uint32_t rk = kGlobal ? __ldg(rank + (d >> 5)) : rank[d >> 5];
+                i = rk + __popc(w & ((2u << (d & 31)) - 1u));
+            }
+            if (i - ov > slack_r || j - ov > slack_s) {
+                if (kFull) *ov_out = 0;
+                return false;
+            }
+        }
+        ld_tokens8(s + j, t);
+    }
+    if (kFull) *ov_out = ov >= req ? ov : 0;
+    return ov >= req;
+}
+
+// Per-run uniform state (every thread holds the same values).
+struct RunState {
+    uint32_t begin, end;      // slots
+    uint32_t slice;           // slice index (kNone: no run)
+    uint32_t rpos8, rsize;    // probe
+    uint32_t bofs, lo, nw;    // probe bitmap (bofs = kNone: none)
+};
+
+__device__ __forceinline__ void load_run(const KParams& p, uint64_t k, uint64_t nr, RunState& r) {
+    if (k < nr) {
+        const uint4 d = __ldg(reinterpret_cast<const uint4*>(p.runs) + k);
+        r.slice = d.x;
+        r.begin = d.y;
+        r.end = d.z;
+    } else {
+        r.slice = kNone;
+        r.begin = r.end = 0;
+    }
+}
+
+__device__ __forceinline__ void load_slice(const KParams& p, RunState& r) {
+    if (r.slice != kNone) {
+        const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(p.slices + r.slice));
+        const uint2 d1 = __ldg(reinterpret_cast<const uint2*>(p.slices + r.slice) + 2);
+        r.rpos8 = d0.y;
+        r.rsize = d0.z;
+        r.bofs = d0.w;
+        r.lo = d1.x;
+        r.nw = d1.y;
+    } else {
+        r.rpos8 = r.rsize = 0;
+        r.bofs = kNone;
+        r.lo = r.nw = 0;
+    }
+}
+
+// run_kernel: persistent; CTA c of G verifies blocks c, c + G, c + 2G, ... of kRunBlock
+// consecutive runs of the segment's list (the list is in slot order). All CTAs thus work on
+// one moving window of the chunk -- the candidates of nearby probes share L2 -- while
+// consecutive runs of a block usually share their slice, so its bitmap is staged once.
+// Thread t owns slots begin + q*kRunThreads + t (q < kRunItems) of every run. Per-thread
+// software pipeline over runs (no registers held for the in-flight token data):
+//   run k+3: C ids (registers)            run k+2: set descriptors {pos8, |s|} (registers)
+//   run k+1: first 32-byte sector of every candidate -> shared memory (cp.async, own slots),
+//            and, when run k+1 starts a new slice, its probe bitmap (cp.async by all threads)
+//   run k  : verification from shared memory; candidates whose verdict needs more than 8
+//            tokens continue with 256-bit loads from the CSR.
+// Bitmap buffers rotate over 3 slots and advance only when a new bitmap is loaded; the one
+// barrier per load (before its first use) also guarantees that no thread still reads the
+// buffer being refilled (that needs 3 loads in between, each behind a barrier).
+template <int kOut, bool kStats>
+__global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const KParams p) {
+    extern __shared__ __align__(16) uint32_t rsh[];
+    uint4* const sh_head = reinterpret_cast<uint4*>(rsh);  // [2][kRunItems][2][kRunThreads]
+    uint32_t* const sh_bits = rsh + 2 * kRunItems * 2 * kRunThreads * 4;  // [3][stride]
+    uint32_t* const sh_rank = sh_bits + kRunBmBuffers * kRunBmStride;
+    const uint32_t tid = threadIdx.x;
+    const uint64_t nr = min((uint64_t)*p.runs_n, p.runs_cap);
+    // i-th run of this CTA
+    auto run_of = [&](uint64_t i) -> uint64_t {
+        return ((uint64_t)blockIdx.x + (i / kRunBlock) * gridDim.x) * kRunBlock + i % kRunBlock;
+    };
+    unsigned count = 0, prunes = 0, verified = 0;
+    if (run_of(0) < nr) {
+        RunState R0, R1, R2, R3;
+        uint32_t c2[kRunItems], c3[kRunItems];
+        uint2 d0[kRunItems], d1[kRunItems], d2[kRunItems];
+        auto load_c = [&](const RunState& r, uint32_t* c) {
+#pragma unroll
+            for (uint32_t q = 0; q < kRunItems; ++q) {
+                const uint32_t slot = r.begin + q * kRunThreads + tid;
+                c[q] = slot < r.end ? __ldg(p.C + slot) : kNone;
+            }
+        };
+        auto load_d = [&](const RunState& r, const uint32_t* c, uint2* d) {
+#pragma unroll
+            for (uint32_t q = 0; q < kRunItems; ++q) {
+                const uint32_t slot = r.begin + q * kRunThreads + tid;
+                d[q] = make_uint2(kNone, 0);
+                if (slot < r.end) {
+                    if (c[q] < p.n_sets) d[q] = __ldg(p.sets + c[q]);
+                    else flag_error(p.acc, kErrOutOfRange);
+                }
+            }
+        };
+        // heads of run r into stage buffer `stage`; its bitmap into buffer `bb` when `load`
+        auto issue = [&](const RunState& r, const uint2* d, uint32_t stage, bool load,
+                         uint32_t bb) {
+#pragma unroll
+            for (uint32_t q = 0; q < kRunItems; ++q) {
+                if (d[q].x != kNone) {
+                    const uint4* src = reinterpret_cast<const uint4*>(p.tokens + (size_t)d[q].x * 8);
+                    uint4* dst = sh_head + ((stage * kRunItems + q) * 2) * kRunThreads + tid;
+                    cp_async16(dst, src);
+                    cp_async16(dst + kRunThreads, src + 1);
+                }
+            }
+            if (load) {
+                const uint32_t units = bitmap_alloc_words(r.nw) / 4;
+                const uint4* gb = reinterpret_cast<const uint4*>(p.bm_bits + r.bofs);
+                const uint4* gr = reinterpret_cast<const uint4*>(p.bm_rank + r.bofs);
+                uint4* sb = reinterpret_cast<uint4*>(sh_bits + bb * kRunBmStride);
+                uint4* sr = reinterpret_cast<uint4*>(sh_rank + bb * kRunBmStride);
+                for (uint32_t u = tid; u < units; u += kRunThreads) {
+                    cp_async16(sb + u, gb + u);
+                    cp_async16(sr + u, gr + u);
+                }
+            }
+            cp_async_commit();
+        };
+        auto smem_bm = [](const RunState& r) { return r.bofs != kNone && r.nw <= kRunBmWords; };
+
+        // prologue
+        load_run(p, run_of(0), nr, R0);
+        load_run(p, run_of(1), nr, R1);
+        load_run(p, run_of(2), nr, R2);
+        load_run(p, run_of(3), nr, R3);
+        load_slice(p, R0);
+        load_slice(p, R1);
+        uint32_t c0[kRunItems], c1[kRunItems];
+        load_c(R0, c0);
+        load_c(R1, c1);
+        load_c(R2, c2);
+        load_d(R0, c0, d0);
+        load_d(R1, c1, d1);
+        uint32_t b0 = 0;                    // bitmap buffer of run k
+        bool ld0 = smem_bm(R0);             // run k's bitmap was loaded (barrier before use)
+        issue(R0, d0, 0, ld0, b0);
+
+        for (uint64_t k = 0; run_of(k) < nr; ++k) {
+            const uint32_t stage = (uint32_t)k & 1u;
+            // run k+1: heads (+ bitmap when it starts a new slice)
+            const bool ld1 = smem_bm(R1) && R1.slice != R0.slice;
+            const uint32_t b1 = ld1 ? (b0 + 1) % kRunBmBuffers : b0;
+            issue(R1, d1, stage ^ 1u, ld1, b1);
+            // run k+2: descriptors and slice; run k+3: C ids
+            load_d(R2, c2, d2);
+            load_slice(p, R2);
+            load_c(R3, c3);
+            RunState R4;
+            load_run(p, run_of(k + 4), nr, R4);
+            cp_async_wait<1>();
+            if (ld0) __syncthreads();  // CTA-uniform
+
+            // ---- verify run k ----
+            const uint32_t m = R0.rsize;
+            const uint32_t* r = p.tokens + (size_t)R0.rpos8 * 8;
+            const bool sbm = smem_bm(R0);
+            const bool gbm = !sbm && R0.bofs != kNone;
+            const uint32_t nbits = R0.nw * 32u;
+#pragma unroll
+            for (uint32_t q = 0; q < kRunItems; ++q) {
+                const uint32_t slot = R0.begin + q * kRunThreads + tid;
+                bool met = false;
+                uint32_t ov = 0;
+                if (d0[q].x != kNone) {
+                    const uint32_t n = d0[q].y;
+                    const uint32_t* s = p.tokens + (size_t)d0[q].x * 8;
+                    const uint64_t req = required_of(p, m, n);
+                    bool deferred = false;
+                    if (p.defer && n > kLongPair && req >= 1 && req <= (uint64_t)min(m, n)) {
+                        const unsigned long long idx = atomicAdd(p.defer_n, 1ull);
+                        if (idx < p.defer_cap) {
+                            p.defer[idx] = slot;
+                            deferred = true;
+                        }
+                    }
+                    if (deferred) {
+                        // verdict, flag and stats come from long_kernel
+                    } else if (req == 0) {
+                        met = true;  // verify.hpp:57: no comparison, met = (0 >= 0)
+                        if (kOut == kOutResults) ov = full_overlap_seq(r, m, s, n);
+                    } else if (req <= (uint64_t)min(m, n)) {
+                        const uint4* h = sh_head + ((stage * kRunItems + q) * 2) * kRunThreads + tid;
+                        const uint4 w0 = h[0], w1 = h[kRunThreads];
+                        uint32_t t8[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+                        if (sbm) {
+                            met = bm_verify<kOut == kOutResults, false>(
+                                sh_bits + b0 * kRunBmStride, sh_rank + b0 * kRunBmStride, R0.lo,
+                                nbits, m, s, n, (uint32_t)req, t8, &ov);
+                        } else if (gbm) {
+                            met = bm_verify<kOut == kOutResults, true>(
+                                p.bm_bits + R0.bofs, p.bm_rank + R0.bofs, R0.lo, nbits, m, s, n,
+                                (uint32_t)req, t8, &ov);
+                        } else {
+                            met = merge_thread<kOut == kOutResults>(
+                                r, m, reinterpret_cast<const uint4*>(s), n, (uint32_t)req, w0, w1,
+                                &ov);
+                        }
+                    }
+                    if (!deferred) {
+                        if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
+                        if (kStats) {
+                            ++verified;
+                            prunes += (!met && (m + n) > 0);
+                        }
+                    }
+                }
+                count += met;
+                if (kOut == kOutResults) warp_append(p, met, slot, ov);
+            }
+
+            // rotate the pipeline
+            b0 = b1;
+            ld0 = ld1;
+            R0 = R1;
+            R1 = R2;
+            R2 = R3;
+            R3 = R4;
+#pragma unroll
+            for (uint32_t q = 0; q < kRunItems; ++q) {
+                d0[q] = d1[q];
+                d1[q] = d2[q];
+                c2[q] = c3[q];
+            }
+        }
+        cp_async_wait<0>();
     }
     acc_add(p.acc, 0, count);
     if (kStats) {
@@ -1040,35 +1145,47 @@ cudaError_t launch_prep(const KParams& p, cudaStream_t st, int* launches) {
     return cudaGetLastError();
 }
 
+int sm_count() {
+    static int cached[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cached[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = n > 0 ? n : 148;
+    }
+    return cached[dev];
+}
+
+template <int kOut, bool kStats>
+cudaError_t launch_tiles_t(const KParams& p, uint32_t tile_begin, uint32_t tile_end,
+                           cudaStream_t st) {
+    const int sms = sm_count();
+    const uint32_t nt = tile_end - tile_begin;
+    runs_gen_kernel<<<(nt + 255) / 256, 256, 0, st>>>(p, tile_begin, tile_end);
+    auto rk = run_kernel<kOut, kStats>;
+    static bool attr = false;  // per instantiation; the attribute is per device function
+    if (!attr) {
+        cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRunSmemBytes);
+        attr = true;
+    }
+    rk<<<sms * kRunMinBlocks, kRunThreads, kRunSmemBytes, st>>>(p);
+    warp_tile_kernel<kOut, kStats><<<sms * kTileMinBlocks, kThreadsA, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_begin,
                          uint32_t tile_end, cudaStream_t st) {
     if (tile_end <= tile_begin) return cudaSuccess;
-#if SSJB_WARP_TILES
-    {
-        constexpr uint32_t wpb = kThreadsA / 32;
-        const uint32_t g = (tile_end - tile_begin + wpb - 1) / wpb;
-        switch (out * 2 + (stats ? 1 : 0)) {
-            case 0: warp_tile_kernel<kOutCount, false><<<g, kThreadsA, 0, st>>>(p, tile_begin, tile_end); break;
-            case 1: warp_tile_kernel<kOutCount, true><<<g, kThreadsA, 0, st>>>(p, tile_begin, tile_end); break;
-            case 2: warp_tile_kernel<kOutFlags, false><<<g, kThreadsA, 0, st>>>(p, tile_begin, tile_end); break;
-            case 3: warp_tile_kernel<kOutFlags, true><<<g, kThreadsA, 0, st>>>(p, tile_begin, tile_end); break;
-            case 4: warp_tile_kernel<kOutResults, false><<<g, kThreadsA, 0, st>>>(p, tile_begin, tile_end); break;
-            default: warp_tile_kernel<kOutResults, true><<<g, kThreadsA, 0, st>>>(p, tile_begin, tile_end); break;
-        }
-        return cudaGetLastError();
-    }
-#else
-    const uint32_t grid = tile_end - tile_begin;
     switch (out * 2 + (stats ? 1 : 0)) {
-        case 0: tile_kernel<kOutCount, false><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
-        case 1: tile_kernel<kOutCount, true><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
-        case 2: tile_kernel<kOutFlags, false><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
-        case 3: tile_kernel<kOutFlags, true><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
-        case 4: tile_kernel<kOutResults, false><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
-        default: tile_kernel<kOutResults, true><<<grid, kThreadsA, 0, st>>>(p, tile_begin); break;
+        case 0: return launch_tiles_t<kOutCount, false>(p, tile_begin, tile_end, st);
+        case 1: return launch_tiles_t<kOutCount, true>(p, tile_begin, tile_end, st);
+        case 2: return launch_tiles_t<kOutFlags, false>(p, tile_begin, tile_end, st);
+        case 3: return launch_tiles_t<kOutFlags, true>(p, tile_begin, tile_end, st);
+        case 4: return launch_tiles_t<kOutResults, false>(p, tile_begin, tile_end, st);
+        default: return launch_tiles_t<kOutResults, true>(p, tile_begin, tile_end, st);
     }
-    return cudaGetLastError();
-#endif
 }
 
 cudaError_t launch_long(const KParams& p, int out, bool stats, cudaStream_t st) {

@@ -8,7 +8,8 @@
 
 namespace ssjb {
 
-// Tile geometry of the load-balanced thread-per-pair kernel (strategy A).
+// Geometry of the warp-tile kernel (strategy A, short slices): every warp owns
+// kTile = 32 * SSJB_TILE_ITEMS consecutive slots.
 #ifndef SSJB_TILE_THREADS
 #define SSJB_TILE_THREADS 128
 #endif
@@ -18,31 +19,46 @@ namespace ssjb {
 #ifndef SSJB_TILE_MIN_BLOCKS
 #define SSJB_TILE_MIN_BLOCKS 8
 #endif
-#ifndef SSJB_WARP_TILES
-#define SSJB_WARP_TILES 1
-#endif
 constexpr uint32_t kThreadsA = SSJB_TILE_THREADS;            // threads per CTA
-#if SSJB_WARP_TILES
-// warp tiles: every warp owns 32 * kItems consecutive slots (no CTA-level cooperation)
-constexpr uint32_t kTile = 32 * SSJB_TILE_ITEMS;
-#else
-constexpr uint32_t kTile = SSJB_TILE_THREADS * SSJB_TILE_ITEMS;  // candidate slots per CTA
-#endif
+constexpr uint32_t kTile = 32 * SSJB_TILE_ITEMS;             // slots per warp tile
 constexpr int kTileMinBlocks = SSJB_TILE_MIN_BLOCKS;         // CTAs per SM (register cap)
-constexpr uint32_t kMaxTileSlices = kTile / 2 < 512 ? kTile / 2 : 512;  // slices described in smem per tile
-constexpr uint32_t kTileRCap = 2048;       // probe tokens staged in shared memory per tile
-constexpr uint32_t kTileBitmapWords = 2048;  // bitmap words (bits + rank) copied to smem per tile
 constexpr uint32_t kSliceBitmapMinCands = 64;  // slices this long get a probe bitmap per chunk
-#ifndef SSJB_EARLY_SECTOR
-#define SSJB_EARLY_SECTOR 0
-#endif
-#ifndef SSJB_TILE_BM_COPY_MIN
-#define SSJB_TILE_BM_COPY_MIN 64
-#endif
-constexpr uint32_t kTileBitmapMinCands = SSJB_TILE_BM_COPY_MIN;  // ... copied to smem when a tile has this many
 constexpr uint32_t kMaxBitmapWords = 8192;     // probe token range cap (256K tokens)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kLongPair = 256;            // candidates longer than this go to long_kernel
+
+// Strategy A, long slices ("runs"): a run is the part of one slice with >= kRunMinSlice
+// candidates that falls into one kRun-aligned block of slots. run_kernel verifies runs with
+// the probe bitmap staged in shared memory and a per-thread cp.async pipeline; every other
+// slot (short slices, uncovered slots) is verified by warp_tile_kernel over a list of tiles.
+#ifndef SSJB_RUN_MIN_SLICE
+#define SSJB_RUN_MIN_SLICE 128
+#endif
+#ifndef SSJB_RUN_MIN_BLOCKS
+#define SSJB_RUN_MIN_BLOCKS 3
+#endif
+constexpr uint32_t kRunThreads = 256;
+constexpr uint32_t kRunItems = 2;                       // slots per thread per run
+constexpr uint32_t kRun = kRunThreads * kRunItems;      // 512 slots per run (multiple of kTile)
+constexpr uint32_t kRunMinSlice = SSJB_RUN_MIN_SLICE;
+constexpr uint32_t kRunBmWords = 1024;                  // bitmap words staged in shared memory
+constexpr uint32_t kRunBmStride = kRunBmWords + 4;      // + the zero word (16-byte rounded)
+constexpr uint32_t kRunBmBuffers = 3;                   // see run_kernel (one barrier per load)
+constexpr int kRunMinBlocks = SSJB_RUN_MIN_BLOCKS;
+#ifndef SSJB_RUN_BLOCK
+#define SSJB_RUN_BLOCK 16
+#endif
+constexpr uint32_t kRunBlock = SSJB_RUN_BLOCK;          // consecutive runs per CTA turn
+constexpr size_t kRunSmemBytes =
+    (size_t)2 * kRunItems * 2 * kRunThreads * 16 + (size_t)2 * kRunBmBuffers * kRunBmStride * 4;
+static_assert(kRun % kTile == 0, "runs are made of whole tiles");
+
+struct RunDesc {
+    uint32_t slice;  // slice index
+    uint32_t begin;  // first slot
+    uint32_t end;    // one past the last slot
+    uint32_t pad;
+};
 
 // Per-slice descriptor built once per chunk by prep_kernel (32 bytes, one sector).
 struct SliceDesc {
@@ -80,6 +96,12 @@ struct KParams {
     uint32_t* defer;                // strategy A: slots of long pairs for long_kernel
     unsigned long long* defer_n;    // their count (this launch's segment)
     uint64_t defer_cap;
+    RunDesc* runs;                  // strategy A: runs of long slices (this segment)
+    unsigned long long* runs_n;
+    uint64_t runs_cap;
+    uint32_t* short_tiles;          // strategy A: tiles holding short-slice / uncovered slots
+    unsigned long long* short_n;
+    uint64_t short_cap;
     uint8_t* flags;                 // Pairs mode (nullable)
     uint32_t* res_slots;            // results mode (nullable)
     uint32_t* res_ov;

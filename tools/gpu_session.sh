@@ -19,7 +19,7 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
      --log-file $OUT/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --e2e-steps 1 \
      --no-cpu-baseline > $OUT/ncu_launch_bench_$TAG.log 2>&1
   echo "ncu launches rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tile_kernel -s 1 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-run_kernel} -s ${KSKIP:-1} -c 1 \
      -o $OUT/prof_$TAG -f python bench.py --steps 1 --warmup 1 --e2e-steps 1 --no-cpu-baseline \
      > $OUT/ncu_full_$TAG.log 2>&1
   echo "ncu full rc=$?"
