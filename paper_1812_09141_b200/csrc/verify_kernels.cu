@@ -444,11 +444,10 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) warp_tile_kernel(co
 // ---------------------------------------------------------------------------------------
 // Strategy A, long slices: runs.
 //
-// runs_gen_kernel (thread per tile of this segment): walks the tile's slices; for every
-// slice with >= kRunMinSlice candidates it emits the run (slice, kRun-aligned block) whose
-// first slot lies in this tile (at most two per tile: one long slice can begin in a 64-slot
-// tile, and the first tile of a block also starts the run of the slice entering the block);
-// a tile holding any short-slice slot or uncovered slot goes to the short-tile list.
+// runs_gen_kernel (thread per tile of this segment): walks the tile's slices. A slice with
+// >= kRunMinSlice candidates is cut into runs of kRun slots from its first slot inside the
+// segment (all emitted by the tile holding that slot); a tile holding any slot of a short
+// slice, or a slot past the last slice, goes to the short-tile list.
 __global__ void runs_gen_kernel(const KParams p, const uint32_t tile_begin,
                                 const uint32_t tile_end) {
     const uint32_t t = tile_begin + blockIdx.x * blockDim.x + threadIdx.x;
@@ -456,8 +455,8 @@ __global__ void runs_gen_kernel(const KParams p, const uint32_t tile_begin,
     const uint64_t slot0 = (uint64_t)t * kTile;
     if (slot0 >= p.nC) return;
     const uint64_t slot1 = min(slot0 + (uint64_t)kTile, p.nC);
-    const uint64_t blk0 = slot0 / kRun * kRun;
-    const uint64_t blk1 = min(blk0 + (uint64_t)kRun, p.nC);
+    const uint64_t seg0 = (uint64_t)tile_begin * kTile;
+    const uint64_t seg1 = min((uint64_t)tile_end * kTile, p.nC);
     uint32_t e = __ldg(p.tile_first + t);
     uint64_t b = e ? min((uint64_t)__ldg(p.C_O + 2 * (size_t)e - 1), p.nC) : 0;  // decode: begin = previous end
     uint64_t covered = slot0;
@@ -467,16 +466,18 @@ __global__ void runs_gen_kernel(const KParams p, const uint32_t tile_begin,
         const uint64_t end = min((uint64_t)__ldg(p.C_O + 2 * (size_t)e + 1), p.nC);
         if (end > b && end > slot0) {
             if (end - b >= kRunMinSlice) {
-                const uint64_t rb = max(b, blk0);
-                if (rb >= slot0 && rb < slot1) {
-                    const unsigned long long k = atomicAdd(p.runs_n, 1ull);
-                    if (k < p.runs_cap) {
+                const uint64_t start = max(b, seg0);
+                if (start >= slot0 && start < slot1) {
+                    const uint64_t stop = min(end, seg1);
+                    const uint64_t nrun = (stop - start + kRun - 1) / kRun;
+                    const unsigned long long k = atomicAdd(p.runs_n, (unsigned long long)nrun);
+                    for (uint64_t i = 0; i < nrun && k + i < p.runs_cap; ++i) {
                         RunDesc d;
                         d.slice = e;
-                        d.begin = (uint32_t)rb;
-                        d.end = (uint32_t)min(end, blk1);
+                        d.begin = (uint32_t)(start + i * kRun);
+                        d.end = (uint32_t)min(start + (i + 1) * kRun, stop);
                         d.pad = 0;
-                        p.runs[k] = d;
+                        p.runs[k + i] = d;
                     }
                 }
             } else {
@@ -509,54 +510,6 @@ __device__ __forceinline__ void ld_tokens8(const uint32_t* __restrict__ s, uint3
                  : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]),
                    "=r"(t[6]), "=r"(t[7])
                  : "l"(s));
-}
-
-// Membership-bitmap verification with clamped lookups: word nwords of `bits` is zero and
-// every token outside [lo, lo + nbits) -- including the 0xFFFFFFFF padding after |s| -- is
-// clamped onto it, so a block of 8 tokens costs 8 unconditional lookups. After each block
-// the merge position is exact (j = tokens of s consumed, i = probe tokens <= the block's
-// last token, from rank), so the reference's bound (verify.hpp:58) is evaluated there;
-// verdicts are bit-exact (see ssj_device.cuh). kGlobal: bits/rank in global memory (read
-// through L1), else shared memory. t: s[0..8) already loaded.
-template <bool kFull, bool kGlobal>
-__device__ __forceinline__ bool bm_verify(const uint32_t* __restrict__ bits,
-                                          const uint32_t* __restrict__ rank, uint32_t lo,
-                                          uint32_t nbits, uint32_t m,
-                                          const uint32_t* __restrict__ s, uint32_t n,
-                                          uint32_t req, uint32_t t[8], uint32_t* ov_out) {
-    const uint32_t slack_r = m - req, slack_s = n - req;
-    uint32_t ov = 0, j = 0;
-    for (;;) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const uint32_t d = min(t[q] - lo, nbits);
-            const uint32_t w = kGlobal ? __ldg(bits + (d >> 5)) : bits[d >> 5];
-            ov += (w >> (d & 31)) & 1u;
-        }
-        j += 8;
-        if (j >= n) break;  // s exhausted (padding never matches): the verdict is ov >= req
-        if (!kFull && ov >= req) break;
-        if (ov < req) {
-            const uint32_t d = t[7] - lo;
-            uint32_t i;
-            if (t[7] < lo) {
-                i = 0;
-            } else if (d >= nbits) {
-                i = m;
-            } else {
-                const uint32_t w = kGlobal ? __ldg(bits + (d >> 5)) : bits[d >> 5];
-                const uint32_t rk = kGlobal ? __ldg(rank + (d >> 5)) : rank[d >> 5];
-                i = rk + __popc(w & ((2u << (d & 31)) - 1u));
-            }
-            if (i - ov > slack_r || j - ov > slack_s) {
-                if (kFull) *ov_out = 0;
-                return false;
-            }
-        }
-        ld_tokens8(s + j, t);
-    }
-    if (kFull) *ov_out = ov >= req ? ov : 0;
-    return ov >= req;
 }
 
 // Per-run uniform state (every thread holds the same values).
@@ -595,187 +548,384 @@ __device__ __forceinline__ void load_slice(const KParams& p, RunState& r) {
     }
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on `bar` (bytes multiple of 16).
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(smem)),
+        "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Membership of 8 tokens in a probe bitmap with clamped lookups: word nbits/32 of `bits`
+// is zero and every token outside [lo, lo + nbits) -- including the 0xFFFFFFFF padding after
+// |s| -- is clamped onto it, so a block costs 8 unconditional lookups. kGlobal: bits in
+// global memory (read through L1), else shared memory.
+template <bool kGlobal>
+__device__ __forceinline__ uint32_t count8(const uint32_t* __restrict__ bits, uint32_t lo,
+                                           uint32_t nbits, const uint32_t t[8]) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t d = min(t[q] - lo, nbits);
+        const uint32_t w = kGlobal ? __ldg(bits + (d >> 5)) : bits[d >> 5];
+        c += (w >> (d & 31)) & 1u;
+    }
+    return c;
+}
+
+// Continue a pair after its first 8 tokens (j = 8, ov = matches so far), 8 tokens per step
+// from the CSR (256-bit loads). After each step the merge position is exact (j = tokens of s
+// consumed, i = probe tokens <= the step's last token, from rank), so the reference's bound
+// (verify.hpp:58) is evaluated there; verdicts are bit-exact (see ssj_device.cuh).
+template <bool kFull, bool kGlobal>
+__device__ __forceinline__ bool bm_continue(const uint32_t* __restrict__ bits,
+                                            const uint32_t* __restrict__ rank, uint32_t lo,
+                                            uint32_t nbits, uint32_t m,
+                                            const uint32_t* __restrict__ s, uint32_t n,
+                                            uint32_t req, uint32_t ov, uint32_t* ov_out) {
+    const uint32_t slack_r = m - req, slack_s = n - req;
+    uint32_t j = 8;
+    for (;;) {
+        uint32_t t[8];
+        ld_tokens8(s + j, t);
+        ov += count8<kGlobal>(bits, lo, nbits, t);
+        j += 8;
+        if (j >= n) break;  // s exhausted (padding never matches): the verdict is ov >= req
+        if (!kFull && ov >= req) break;
+        if (ov < req) {
+            const uint32_t d = t[7] - lo;
+            uint32_t i;
+            if (t[7] < lo) {
+                i = 0;
+            } else if (d >= nbits) {
+                i = m;
+            } else {
+                const uint32_t w = kGlobal ? __ldg(bits + (d >> 5)) : bits[d >> 5];
+                const uint32_t rk = kGlobal ? __ldg(rank + (d >> 5)) : rank[d >> 5];
+                i = rk + __popc(w & ((2u << (d & 31)) - 1u));
+            }
+            if (i - ov > slack_r || j - ov > slack_s) {
+                if (kFull) *ov_out = 0;
+                return false;
+            }
+        }
+    }
+    if (kFull) *ov_out = ov >= req ? ov : 0;
+    return ov >= req;
+}
+
+// Warp-aggregated append of deferred long pairs (all 32 lanes call it).
+__device__ __forceinline__ bool warp_defer(const KParams& p, bool want, uint32_t slot) {
+    const unsigned mask = __ballot_sync(0xffffffffu, want);
+    if (!mask) return false;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(p.defer_n, (unsigned long long)__popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (!want) return false;
+    const unsigned long long idx = base + __popc(mask & ((1u << lane) - 1u));
+    if (idx >= p.defer_cap) return false;  // cannot happen: one entry per slot of the segment
+    p.defer[idx] = slot;
+    return true;
+}
+
+__device__ __forceinline__ uint32_t req_u32(const KParams& p, uint32_t m, uint32_t n) {
+    const uint32_t sum = m + n;
+    if (p.req_tab && sum >= m && sum < p.req_tab_n) return __ldg(p.req_tab + sum);
+    return (uint32_t)min(dev_required(p.pred, m, n), (uint64_t)0xFFFFFFFFu);
+}
+
+// Verify one run whose probe has a bitmap, in two phases per warp:
+//  1. every lane tests the first 8 tokens of each of its kRunItems candidates (staged in
+//     shared memory) against the bitmap; the pair is decided when |s| <= 8, when the overlap
+//     already reaches `required` (not in results mode), or when the s-side bound
+//     (verify.hpp:58) rejects it; otherwise (slot, s, |s|, required, overlap) goes to the
+//     warp's queue (in the heads area, behind the items still to be read);
+//  2. the queue is drained 32 entries per round with bm_continue (no divergence between
+//     lanes whose pairs need one block and lanes whose pairs need several).
+template <int kOut, bool kStats, bool kGlobal>
+__device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R, const uint2* d,
+                                           const uint32_t* __restrict__ bits,
+                                           const uint32_t* __restrict__ rank, uint4* wq,
+                                           unsigned& count, unsigned& prunes,
+                                           unsigned& verified) {
+    constexpr bool kFull = kOut == kOutResults;
+    constexpr uint32_t T = kRunThreads, I = kRunItems;
+    const uint32_t lane = threadIdx.x & 31, tid = threadIdx.x;
+    const uint32_t m = R.rsize, lo = R.lo, nbits = R.nw * 32u;
+    uint32_t req[I];
+#pragma unroll
+    for (uint32_t q = 0; q < I; ++q) req[q] = d[q].x != kNone ? req_u32(p, m, d[q].y) : 0u;
+    uint32_t nq = 0;
+#pragma unroll
+    for (uint32_t q = 0; q < I; ++q) {
+        const uint32_t slot = R.begin + q * T + tid;
+        const bool valid = d[q].x != kNone;
+        const uint32_t n = d[q].y, rq = req[q];
+        const bool inrange = valid && rq >= 1 && rq <= min(m, n);
+        const bool deferred = warp_defer(p, inrange && n > kLongPair, slot);
+        bool met = valid && rq == 0, decided = true;
+        uint32_t ov = 0;
+        if (inrange && !deferred) {
+            const uint4 w0 = wq[(q * 2) * 32 + lane], w1 = wq[(q * 2 + 1) * 32 + lane];
+            const uint32_t t8[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            ov = count8<kGlobal>(bits, lo, nbits, t8);
+            if (n <= 8) met = ov >= rq;
+            else if (!kFull && ov >= rq) met = true;
+            else if (ov < rq && 8u - ov > n - rq) met = false;
+            else decided = false;
+        } else if (kFull && met) {
+            ov = full_overlap_seq(p.tokens + (size_t)R.rpos8 * 8, m,
+                                  p.tokens + (size_t)d[q].x * 8, n);
+        }
+        __syncwarp();  // heads of item q read by every lane before the queue may cover them
+        const unsigned qmask = __ballot_sync(0xffffffffu, !decided);
+        if (!decided)
+            wq[nq + __popc(qmask & ((1u << lane) - 1u))] =
+                make_uint4(slot, d[q].x, n, rq | (ov << 16));
+        nq += __popc(qmask);
+        if (valid && decided && !deferred) {
+            if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
+            if (kStats) {
+                ++verified;
+                prunes += (!met && (m + n) > 0);
+            }
+            count += met;
+        }
+        if (kFull) warp_append(p, valid && decided && !deferred && met, slot, ov);
+    }
+    __syncwarp();
+    for (uint32_t base = 0; base < nq; base += 32) {
+        const uint32_t e = base + lane;
+        bool met = false;
+        uint32_t ov = 0, slot = 0;
+        if (e < nq) {
+            const uint4 qe = wq[e];
+            slot = qe.x;
+            const uint32_t n = qe.z, rq = qe.w & 0xFFFFu;
+            met = bm_continue<kFull, kGlobal>(bits, rank, lo, nbits, m,
+                                              p.tokens + (size_t)qe.y * 8, n, rq, qe.w >> 16, &ov);
+            if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
+            if (kStats) {
+                ++verified;
+                prunes += (!met && (m + n) > 0);
+            }
+            count += met;
+        }
+        if (kFull) warp_append(p, met, slot, ov);
+    }
+    __syncwarp();  // queue read before the next run's heads land here
+}
+
+// A run whose probe has no bitmap: thread-sequential early-exit merge per candidate.
+template <int kOut, bool kStats>
+__device__ __forceinline__ void run_merge(const KParams& p, const RunState& R, const uint2* d,
+                                          const uint4* wq, unsigned& count, unsigned& prunes,
+                                          unsigned& verified) {
+    constexpr bool kFull = kOut == kOutResults;
+    constexpr uint32_t T = kRunThreads, I = kRunItems;
+    const uint32_t lane = threadIdx.x & 31, tid = threadIdx.x;
+    const uint32_t m = R.rsize;
+    const uint32_t* r = p.tokens + (size_t)R.rpos8 * 8;
+#pragma unroll
+    for (uint32_t q = 0; q < I; ++q) {
+        const uint32_t slot = R.begin + q * T + tid;
+        const bool valid = d[q].x != kNone;
+        const uint32_t n = d[q].y;
+        const uint32_t rq = valid ? req_u32(p, m, n) : 0u;
+        const bool inrange = valid && rq >= 1 && rq <= min(m, n);
+        const bool deferred = warp_defer(p, inrange && n > kLongPair, slot);
+        bool met = valid && rq == 0;
+        uint32_t ov = 0;
+        const uint32_t* s = p.tokens + (size_t)d[q].x * 8;
+        if (inrange && !deferred) {
+            met = merge_thread<kFull>(r, m, reinterpret_cast<const uint4*>(s), n, rq,
+                                      wq[(q * 2) * 32 + lane], wq[(q * 2 + 1) * 32 + lane], &ov);
+        } else if (kFull && met) {
+            ov = full_overlap_seq(r, m, s, n);
+        }
+        if (valid && !deferred) {
+            if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
+            if (kStats) {
+                ++verified;
+                prunes += (!met && (m + n) > 0);
+            }
+            count += met;
+        }
+        if (kFull) warp_append(p, valid && !deferred && met, slot, ov);
+    }
+    __syncwarp();
+}
+
 // run_kernel: persistent; CTA c of G verifies blocks c, c + G, c + 2G, ... of kRunBlock
-// consecutive runs of the segment's list (the list is in slot order). All CTAs thus work on
-// one moving window of the chunk -- the candidates of nearby probes share L2 -- while
-// consecutive runs of a block usually share their slice, so its bitmap is staged once.
-// Thread t owns slots begin + q*kRunThreads + t (q < kRunItems) of every run. Per-thread
-// software pipeline over runs (no registers held for the in-flight token data):
-//   run k+3: C ids (registers)            run k+2: set descriptors {pos8, |s|} (registers)
-//   run k+1: first 32-byte sector of every candidate -> shared memory (cp.async, own slots),
-//            and, when run k+1 starts a new slice, its probe bitmap (cp.async by all threads)
-//   run k  : verification from shared memory; candidates whose verdict needs more than 8
-//            tokens continue with 256-bit loads from the CSR.
-// Bitmap buffers rotate over 3 slots and advance only when a new bitmap is loaded; the one
-// barrier per load (before its first use) also guarantees that no thread still reads the
-// buffer being refilled (that needs 3 loads in between, each behind a barrier).
+// consecutive runs of the segment's list (the list follows slot order, and the runs of one
+// slice are consecutive). All CTAs thus work on one moving window of the chunk -- the
+// candidates of nearby probes share L2 -- and consecutive runs of a block usually share
+// their slice, so its bitmap is staged once.
+//
+// Thread t owns slots begin + q*kRunThreads + t (q < kRunItems) of every run. Per run k:
+//   C ids of run k+2 and set descriptors {pos8, |s|} of run k+1 are prefetched into
+//   registers one run ahead; the first 32-byte sector of each of the thread's candidates of
+//   run k is fetched into shared memory by cp.async (the warp's own area, no CTA barrier);
+//   the probe bitmap of a run that starts a new slice is fetched one run ahead by one
+//   thread with a TMA bulk copy on a `full` mbarrier into one of two buffers, which warps
+//   release on an `empty` mbarrier when they move on.
 template <int kOut, bool kStats>
 __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const KParams p) {
     extern __shared__ __align__(16) uint32_t rsh[];
-    uint4* const sh_head = reinterpret_cast<uint4*>(rsh);  // [2][kRunItems][2][kRunThreads]
-    uint32_t* const sh_bits = rsh + 2 * kRunItems * 2 * kRunThreads * 4;  // [3][stride]
-    uint32_t* const sh_rank = sh_bits + kRunBmBuffers * kRunBmStride;
-    const uint32_t tid = threadIdx.x;
+    constexpr uint32_t T = kRunThreads, I = kRunItems;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint4* const wq = reinterpret_cast<uint4*>(rsh) + warp * (I * 2 * 32);  // [item][half][lane]
+    uint32_t* const s_bits = rsh + T * I * 8;                               // [2][stride]
+    uint32_t* const s_rank = s_bits + kRunBmBufs * kRunBmStride;            // [2][stride]
+    uint64_t* const full = reinterpret_cast<uint64_t*>(s_rank + kRunBmBufs * kRunBmStride);
+    uint64_t* const empty = full + kRunBmBufs;
     const uint64_t nr = min((uint64_t)*p.runs_n, p.runs_cap);
-    // i-th run of this CTA
     auto run_of = [&](uint64_t i) -> uint64_t {
         return ((uint64_t)blockIdx.x + (i / kRunBlock) * gridDim.x) * kRunBlock + i % kRunBlock;
     };
     unsigned count = 0, prunes = 0, verified = 0;
     if (run_of(0) < nr) {
-        RunState R0, R1, R2, R3;
-        uint32_t c2[kRunItems], c3[kRunItems];
-        uint2 d0[kRunItems], d1[kRunItems], d2[kRunItems];
+        if (tid == 0) {
+            for (uint32_t b = 0; b < kRunBmBufs; ++b) {
+                mbar_init(full + b, 1);
+                mbar_init(empty + b, T / 32);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+
+        auto smem_bm = [](const RunState& r) { return r.bofs != kNone && r.nw <= kRunBmWords; };
         auto load_c = [&](const RunState& r, uint32_t* c) {
 #pragma unroll
-            for (uint32_t q = 0; q < kRunItems; ++q) {
-                const uint32_t slot = r.begin + q * kRunThreads + tid;
+            for (uint32_t q = 0; q < I; ++q) {
+                const uint32_t slot = r.begin + q * T + tid;
                 c[q] = slot < r.end ? __ldg(p.C + slot) : kNone;
             }
         };
-        auto load_d = [&](const RunState& r, const uint32_t* c, uint2* d) {
+        auto load_d = [&](const uint32_t* c, uint2* d) {
 #pragma unroll
-            for (uint32_t q = 0; q < kRunItems; ++q) {
-                const uint32_t slot = r.begin + q * kRunThreads + tid;
+            for (uint32_t q = 0; q < I; ++q) {
                 d[q] = make_uint2(kNone, 0);
-                if (slot < r.end) {
+                if (c[q] != kNone) {
                     if (c[q] < p.n_sets) d[q] = __ldg(p.sets + c[q]);
                     else flag_error(p.acc, kErrOutOfRange);
                 }
             }
         };
-        // heads of run r into stage buffer `stage`; its bitmap into buffer `bb` when `load`
-        auto issue = [&](const RunState& r, const uint2* d, uint32_t stage, bool load,
-                         uint32_t bb) {
-#pragma unroll
-            for (uint32_t q = 0; q < kRunItems; ++q) {
-                if (d[q].x != kNone) {
-                    const uint4* src = reinterpret_cast<const uint4*>(p.tokens + (size_t)d[q].x * 8);
-                    uint4* dst = sh_head + ((stage * kRunItems + q) * 2) * kRunThreads + tid;
-                    cp_async16(dst, src);
-                    cp_async16(dst + kRunThreads, src + 1);
-                }
+        uint32_t nload = 0;  // bitmap loads issued so far (every thread tracks it)
+        auto issue_bm = [&](const RunState& r) {
+            const uint32_t b = nload % kRunBmBufs;
+            if (tid == 0) {
+                if (nload >= kRunBmBufs) mbar_wait(empty + b, ((nload / kRunBmBufs) - 1) & 1);
+                const uint32_t bytes = bitmap_alloc_words(r.nw) * 4;
+                mbar_expect_tx(full + b, 2 * bytes);
+                bulk_g2s(s_bits + b * kRunBmStride, p.bm_bits + r.bofs, bytes, full + b);
+                bulk_g2s(s_rank + b * kRunBmStride, p.bm_rank + r.bofs, bytes, full + b);
             }
-            if (load) {
-                const uint32_t units = bitmap_alloc_words(r.nw) / 4;
-                const uint4* gb = reinterpret_cast<const uint4*>(p.bm_bits + r.bofs);
-                const uint4* gr = reinterpret_cast<const uint4*>(p.bm_rank + r.bofs);
-                uint4* sb = reinterpret_cast<uint4*>(sh_bits + bb * kRunBmStride);
-                uint4* sr = reinterpret_cast<uint4*>(sh_rank + bb * kRunBmStride);
-                for (uint32_t u = tid; u < units; u += kRunThreads) {
-                    cp_async16(sb + u, gb + u);
-                    cp_async16(sr + u, gr + u);
-                }
-            }
-            cp_async_commit();
+            ++nload;
         };
-        auto smem_bm = [](const RunState& r) { return r.bofs != kNone && r.nw <= kRunBmWords; };
 
-        // prologue
+        RunState R0, R1, R2;
         load_run(p, run_of(0), nr, R0);
         load_run(p, run_of(1), nr, R1);
         load_run(p, run_of(2), nr, R2);
-        load_run(p, run_of(3), nr, R3);
         load_slice(p, R0);
         load_slice(p, R1);
-        uint32_t c0[kRunItems], c1[kRunItems];
-        load_c(R0, c0);
-        load_c(R1, c1);
-        load_c(R2, c2);
-        load_d(R0, c0, d0);
-        load_d(R1, c1, d1);
-        uint32_t b0 = 0;                    // bitmap buffer of run k
-        bool ld0 = smem_bm(R0);             // run k's bitmap was loaded (barrier before use)
-        issue(R0, d0, 0, ld0, b0);
+        uint32_t c[I];
+        uint2 d0[I], d1[I];
+        load_c(R0, c);
+        load_d(c, d0);
+        load_c(R1, c);
+        bool ld0 = smem_bm(R0);  // run k's bitmap is a fresh load (wait on `full`)
+        if (ld0) issue_bm(R0);
+        uint32_t L0 = nload - 1;  // load index holding run k's bitmap (if any)
 
         for (uint64_t k = 0; run_of(k) < nr; ++k) {
-            const uint32_t stage = (uint32_t)k & 1u;
-            // run k+1: heads (+ bitmap when it starts a new slice)
-            const bool ld1 = smem_bm(R1) && R1.slice != R0.slice;
-            const uint32_t b1 = ld1 ? (b0 + 1) % kRunBmBuffers : b0;
-            issue(R1, d1, stage ^ 1u, ld1, b1);
-            // run k+2: descriptors and slice; run k+3: C ids
-            load_d(R2, c2, d2);
-            load_slice(p, R2);
-            load_c(R3, c3);
-            RunState R4;
-            load_run(p, run_of(k + 4), nr, R4);
-            cp_async_wait<1>();
-            if (ld0) __syncthreads();  // CTA-uniform
-
-            // ---- verify run k ----
-            const uint32_t m = R0.rsize;
-            const uint32_t* r = p.tokens + (size_t)R0.rpos8 * 8;
-            const bool sbm = smem_bm(R0);
-            const bool gbm = !sbm && R0.bofs != kNone;
-            const uint32_t nbits = R0.nw * 32u;
+            // heads of run k -> this warp's area
 #pragma unroll
-            for (uint32_t q = 0; q < kRunItems; ++q) {
-                const uint32_t slot = R0.begin + q * kRunThreads + tid;
-                bool met = false;
-                uint32_t ov = 0;
+            for (uint32_t q = 0; q < I; ++q) {
                 if (d0[q].x != kNone) {
-                    const uint32_t n = d0[q].y;
-                    const uint32_t* s = p.tokens + (size_t)d0[q].x * 8;
-                    const uint64_t req = required_of(p, m, n);
-                    bool deferred = false;
-                    if (p.defer && n > kLongPair && req >= 1 && req <= (uint64_t)min(m, n)) {
-                        const unsigned long long idx = atomicAdd(p.defer_n, 1ull);
-                        if (idx < p.defer_cap) {
-                            p.defer[idx] = slot;
-                            deferred = true;
-                        }
-                    }
-                    if (deferred) {
-                        // verdict, flag and stats come from long_kernel
-                    } else if (req == 0) {
-                        met = true;  // verify.hpp:57: no comparison, met = (0 >= 0)
-                        if (kOut == kOutResults) ov = full_overlap_seq(r, m, s, n);
-                    } else if (req <= (uint64_t)min(m, n)) {
-                        const uint4* h = sh_head + ((stage * kRunItems + q) * 2) * kRunThreads + tid;
-                        const uint4 w0 = h[0], w1 = h[kRunThreads];
-                        uint32_t t8[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-                        if (sbm) {
-                            met = bm_verify<kOut == kOutResults, false>(
-                                sh_bits + b0 * kRunBmStride, sh_rank + b0 * kRunBmStride, R0.lo,
-                                nbits, m, s, n, (uint32_t)req, t8, &ov);
-                        } else if (gbm) {
-                            met = bm_verify<kOut == kOutResults, true>(
-                                p.bm_bits + R0.bofs, p.bm_rank + R0.bofs, R0.lo, nbits, m, s, n,
-                                (uint32_t)req, t8, &ov);
-                        } else {
-                            met = merge_thread<kOut == kOutResults>(
-                                r, m, reinterpret_cast<const uint4*>(s), n, (uint32_t)req, w0, w1,
-                                &ov);
-                        }
-                    }
-                    if (!deferred) {
-                        if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
-                        if (kStats) {
-                            ++verified;
-                            prunes += (!met && (m + n) > 0);
-                        }
-                    }
+                    const uint4* src = reinterpret_cast<const uint4*>(p.tokens + (size_t)d0[q].x * 8);
+                    cp_async16(wq + (q * 2) * 32 + lane, src);
+                    cp_async16(wq + (q * 2 + 1) * 32 + lane, src + 1);
                 }
-                count += met;
-                if (kOut == kOutResults) warp_append(p, met, slot, ov);
             }
+            cp_async_commit();
+            // prefetch: descriptors of run k+1, C ids of run k+2, run k+3, slice of run k+2
+            load_d(c, d1);
+            load_c(R2, c);
+            RunState R3;
+            load_run(p, run_of(k + 3), nr, R3);
+            load_slice(p, R2);
+            // bitmap of run k+1 when it starts a new slice
+            const bool ld1 = smem_bm(R1) && R1.slice != R0.slice;
+            if (ld1) issue_bm(R1);
+            const uint32_t L1 = ld1 ? nload - 1 : L0;
 
-            // rotate the pipeline
-            b0 = b1;
+            cp_async_wait<0>();
+            __syncwarp();
+            if (R0.bofs != kNone) {
+                if (smem_bm(R0)) {
+                    const uint32_t bb = L0 % kRunBmBufs;
+                    if (ld0) mbar_wait(full + bb, (L0 / kRunBmBufs) & 1);
+                    run_bitmap<kOut, kStats, false>(p, R0, d0, s_bits + bb * kRunBmStride,
+                                                    s_rank + bb * kRunBmStride, wq, count,
+                                                    prunes, verified);
+                } else {
+                    run_bitmap<kOut, kStats, true>(p, R0, d0, p.bm_bits + R0.bofs,
+                                                   p.bm_rank + R0.bofs, wq, count, prunes,
+                                                   verified);
+                }
+            } else {
+                run_merge<kOut, kStats>(p, R0, d0, wq, count, prunes, verified);
+            }
+            // moving to a new bitmap: release the previous one (one arrival per warp)
+            if (ld1 && L1 > 0 && lane == 0) mbar_arrive(empty + (L1 - 1) % kRunBmBufs);
+
             ld0 = ld1;
+            L0 = L1;
             R0 = R1;
             R1 = R2;
             R2 = R3;
-            R3 = R4;
 #pragma unroll
-            for (uint32_t q = 0; q < kRunItems; ++q) {
-                d0[q] = d1[q];
-                d1[q] = d2[q];
-                c2[q] = c3[q];
-            }
+            for (uint32_t q = 0; q < I; ++q) d0[q] = d1[q];
         }
-        cp_async_wait<0>();
     }
     acc_add(p.acc, 0, count);
     if (kStats) {

@@ -27,31 +27,39 @@ constexpr uint32_t kMaxBitmapWords = 8192;     // probe token range cap (256K to
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kLongPair = 256;            // candidates longer than this go to long_kernel
 
-// Strategy A, long slices ("runs"): a run is the part of one slice with >= kRunMinSlice
-// candidates that falls into one kRun-aligned block of slots. run_kernel verifies runs with
-// the probe bitmap staged in shared memory and a per-thread cp.async pipeline; every other
-// slot (short slices, uncovered slots) is verified by warp_tile_kernel over a list of tiles.
+// Strategy A, long slices ("runs"): a run is a piece of <= kRun consecutive slots of one
+// slice with >= kRunMinSlice candidates (slices are cut at the chunk-segment boundaries
+// first). run_kernel verifies runs with the probe bitmap staged in shared memory; every
+// other slot (short slices, uncovered slots) is verified by warp_tile_kernel over a list of
+// tiles.
 #ifndef SSJB_RUN_MIN_SLICE
 #define SSJB_RUN_MIN_SLICE 128
 #endif
 #ifndef SSJB_RUN_MIN_BLOCKS
-#define SSJB_RUN_MIN_BLOCKS 3
+#define SSJB_RUN_MIN_BLOCKS 4
 #endif
-constexpr uint32_t kRunThreads = 256;
-constexpr uint32_t kRunItems = 2;                       // slots per thread per run
-constexpr uint32_t kRun = kRunThreads * kRunItems;      // 512 slots per run (multiple of kTile)
+#ifndef SSJB_RUN_BLOCK
+#define SSJB_RUN_BLOCK 8
+#endif
+#ifndef SSJB_RUN_THREADS
+#define SSJB_RUN_THREADS 256
+#endif
+#ifndef SSJB_RUN_ITEMS
+#define SSJB_RUN_ITEMS 2
+#endif
+constexpr uint32_t kRunThreads = SSJB_RUN_THREADS;
+constexpr uint32_t kRunItems = SSJB_RUN_ITEMS;          // slots per thread per run
+constexpr uint32_t kRun = kRunThreads * kRunItems;      // slots per run
 constexpr uint32_t kRunMinSlice = SSJB_RUN_MIN_SLICE;
 constexpr uint32_t kRunBmWords = 1024;                  // bitmap words staged in shared memory
 constexpr uint32_t kRunBmStride = kRunBmWords + 4;      // + the zero word (16-byte rounded)
-constexpr uint32_t kRunBmBuffers = 3;                   // see run_kernel (one barrier per load)
+constexpr uint32_t kRunBmBufs = 2;
 constexpr int kRunMinBlocks = SSJB_RUN_MIN_BLOCKS;
-#ifndef SSJB_RUN_BLOCK
-#define SSJB_RUN_BLOCK 16
-#endif
 constexpr uint32_t kRunBlock = SSJB_RUN_BLOCK;          // consecutive runs per CTA turn
-constexpr size_t kRunSmemBytes =
-    (size_t)2 * kRunItems * 2 * kRunThreads * 16 + (size_t)2 * kRunBmBuffers * kRunBmStride * 4;
-static_assert(kRun % kTile == 0, "runs are made of whole tiles");
+// shared memory: candidate heads [warp][item][half][lane] uint4 (reused as the warp's
+// continuation queue), 2 bitmap buffers (bits + rank), 4 mbarriers
+constexpr size_t kRunSmemBytes = (size_t)kRunThreads * kRunItems * 32 +
+                                 (size_t)2 * kRunBmBufs * kRunBmStride * 4 + 4 * 8;
 
 struct RunDesc {
     uint32_t slice;  // slice index
