@@ -154,6 +154,7 @@ struct ssj_engine {
     uint2* d_sets = nullptr;
     bool owns_collection = true;
     uint32_t* d_req_tab = nullptr;  // Jaccard/Dice required overlap by |r|+|s|
+    uint4* d_heads = nullptr;       // packed set heads (null: tokens too large to pack)
     uint32_t req_tab_n = 0;
     cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
     ChunkSlot slot[2];
@@ -228,6 +229,11 @@ int make_pred_dev(const ssj_predicate& p, PredDev* out) {
     if ((p.function == SSJ_JACCARD || p.function == SSJ_DICE) && d.B == 0)
         return fail(SSJ_ERR_INVALID_ARGUMENT, "threshold denominator overflows");
     d.wide = (d.A >= (1ull << 30) || d.B >= (1ull << 32)) ? 1 : 0;
+    if ((p.function == SSJ_JACCARD || p.function == SSJ_DICE) && !d.wide) {
+        d.A32 = (uint32_t)d.A;
+        d.B32 = (uint32_t)d.B;
+        d.Binv = 0xFFFFFFFFu / d.B32;
+    }
     *out = d;
     return SSJ_OK;
 }
@@ -240,7 +246,27 @@ KParams base_params(const ssj_engine& e) {
     p.pred = e.pred;
     p.req_tab = e.d_req_tab;
     p.req_tab_n = e.req_tab_n;
+    p.heads = e.d_heads;
     return p;
+}
+
+// Packed set heads (verify_kernels.cuh) for the run kernel; left null when some token is
+// too large for the packing (the kernels then read descriptors and the CSR instead).
+int build_heads(ssj_engine& e) {
+    if (!e.n_sets) return SSJ_OK;
+    unsigned* d_max = nullptr;
+    SSJ_CK(cudaMalloc(&e.d_heads, (size_t)e.n_sets * 2 * sizeof(uint4)));
+    SSJ_CK(cudaMalloc(&d_max, sizeof(unsigned)));
+    SSJ_CK(cudaMemset(d_max, 0, sizeof(unsigned)));
+    SSJ_CK(ssjb::launch_build_heads(e.d_tokens, e.d_sets, e.n_sets, e.d_heads, d_max, 0));
+    unsigned mx = 0;
+    SSJ_CK(cudaMemcpy(&mx, d_max, sizeof(unsigned), cudaMemcpyDeviceToHost));
+    cudaFree(d_max);
+    if (mx >= ssjb::kHeadTokenLimit) {
+        cudaFree(e.d_heads);
+        e.d_heads = nullptr;
+    }
+    return SSJ_OK;
 }
 
 // Jaccard and Dice: equivalent_overlap depends on |r| + |s| only (similarity.hpp:113-118),
@@ -697,6 +723,7 @@ int ssj_engine_create(ssj_engine** out, int device, const uint32_t* tokens, cons
     uint32_t max_size = 0;
     for (uint32_t i = 0; i < n_sets; ++i) max_size = std::max(max_size, offsets[i + 1] - offsets[i]);
     if ((rc = build_req_table(*e, max_size))) return cleanup(rc);
+    if ((rc = build_heads(*e))) return cleanup(rc);
     *out = e;
     return SSJ_OK;
 }
@@ -745,6 +772,10 @@ int ssj_engine_create_from_device(ssj_engine** out, int device, const uint32_t* 
             return rc;
         }
     }
+    if ((rc = build_heads(*e))) {
+        ssj_engine_destroy(e);
+        return rc;
+    }
     *out = e;
     return SSJ_OK;
 }
@@ -782,6 +813,7 @@ void ssj_engine_destroy(ssj_engine* e) {
     cudaFree(e->dev_runs);
     cudaFree(e->dev_short);
     cudaFree(e->d_req_tab);
+    cudaFree(e->d_heads);
     cudaFree(e->d_res_slots);
     cudaFree(e->d_res_ov);
     cudaFree(e->d_res_n);

@@ -27,7 +27,14 @@ struct PredDev {
     int32_t wide;  // 1 -> u128 path needed (A >= 2^30 or B >= 2^32)
     uint64_t A, B;
     uint64_t num, den, ovt;
+    uint32_t A32, B32, Binv;  // Jaccard/Dice, !wide: A, B and floor((2^32 - 1) / B)
+    uint32_t pad;
 };
+
+// Jaccard / Dice required overlap ceil(A * sum / B) in 32-bit arithmetic when A * sum < 2^32
+// (exact: q0 = umulhi(x, floor((2^32-1)/B)) is within 2 below floor(x / B)); else the
+// reference formula. Returns min(required, 2^32 - 1).
+__device__ __forceinline__ uint32_t dev_required_fast(const PredDev& p, uint32_t r, uint32_t s);
 
 typedef unsigned __int128 u128;
 
@@ -61,6 +68,23 @@ __device__ __forceinline__ uint64_t dev_required(const PredDev& p, uint32_t r, u
         case kFnCosine: return dev_ceil_scaled_sqrt(p.num, p.den, r, s);
         default: return p.ovt;
     }
+}
+
+__device__ __forceinline__ uint32_t dev_required_fast(const PredDev& p, uint32_t r, uint32_t s) {
+    if ((p.fn == kFnJaccard || p.fn == kFnDice) && !p.wide) {
+        const uint64_t sum = (uint64_t)r + s;
+        const uint64_t x64 = (uint64_t)p.A32 * sum;
+        if (x64 <= 0xFFFFFFFFull) {
+            const uint32_t x = (uint32_t)x64;
+            uint32_t q = __umulhi(x, p.Binv);
+            uint32_t rem = x - q * p.B32;
+            if (rem >= p.B32) { ++q; rem -= p.B32; }
+            if (rem >= p.B32) { ++q; rem -= p.B32; }
+            return q + (rem != 0);
+        }
+    }
+    const uint64_t v = dev_required(p, r, s);
+    return v > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)v;
 }
 
 // Exactness argument used by every kernel below (verify.hpp:50-72):

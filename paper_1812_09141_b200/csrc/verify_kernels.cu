@@ -590,29 +590,33 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t 
         : "memory");
 }
 
-// Membership of 8 tokens in a probe bitmap with clamped lookups: word nbits/32 of `bits`
-// is zero and every token outside [lo, lo + nbits) -- including the 0xFFFFFFFF padding after
-// |s| -- is clamped onto it, so a block costs 8 unconditional lookups. kGlobal: bits in
-// global memory (read through L1), else shared memory.
-template <bool kGlobal>
-__device__ __forceinline__ uint32_t count8(const uint32_t* __restrict__ bits, uint32_t lo,
-                                           uint32_t nbits, const uint32_t t[8]) {
+// Membership of 8 tokens in the probe: tokens outside [lo, lo + R) -- including the padding
+// past |s| -- are clamped onto entry R, which is always empty, so a block costs 8
+// unconditional lookups.
+//   kMap   : byte map in shared memory (map[d] = 1 iff lo + d is a probe token), R = range
+//   !kMap  : membership bitmap in global memory (word R/32 is zero), read through L1
+template <bool kMap>
+__device__ __forceinline__ uint32_t count8(const uint8_t* __restrict__ map,
+                                           const uint32_t* __restrict__ bits, uint32_t lo,
+                                           uint32_t R, const uint32_t t[8]) {
     uint32_t c = 0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-        const uint32_t d = min(t[q] - lo, nbits);
-        const uint32_t w = kGlobal ? __ldg(bits + (d >> 5)) : bits[d >> 5];
-        c += (w >> (d & 31)) & 1u;
+        const uint32_t d = min(t[q] - lo, R);
+        if (kMap) c += map[d];
+        else c += (__ldg(bits + (d >> 5)) >> (d & 31)) & 1u;
     }
     return c;
 }
 
 // Continue a pair after its first 8 tokens (j = 8, ov = matches so far), 8 tokens per step
 // from the CSR (256-bit loads). After each step the merge position is exact (j = tokens of s
-// consumed, i = probe tokens <= the step's last token, from rank), so the reference's bound
-// (verify.hpp:58) is evaluated there; verdicts are bit-exact (see ssj_device.cuh).
-template <bool kFull, bool kGlobal>
-__device__ __forceinline__ bool bm_continue(const uint32_t* __restrict__ bits,
+// consumed, i = probe tokens <= the step's last token, from the global bitmap's rank), so
+// the reference's bound (verify.hpp:58) is evaluated there; verdicts are bit-exact (see
+// ssj_device.cuh).
+template <bool kFull, bool kMap>
+__device__ __forceinline__ bool bm_continue(const uint8_t* __restrict__ map,
+                                            const uint32_t* __restrict__ bits,
                                             const uint32_t* __restrict__ rank, uint32_t lo,
                                             uint32_t nbits, uint32_t m,
                                             const uint32_t* __restrict__ s, uint32_t n,
@@ -622,7 +626,7 @@ __device__ __forceinline__ bool bm_continue(const uint32_t* __restrict__ bits,
     for (;;) {
         uint32_t t[8];
         ld_tokens8(s + j, t);
-        ov += count8<kGlobal>(bits, lo, nbits, t);
+        ov += count8<kMap>(map, bits, lo, nbits, t);
         j += 8;
         if (j >= n) break;  // s exhausted (padding never matches): the verdict is ov >= req
         if (!kFull && ov >= req) break;
@@ -634,9 +638,8 @@ __device__ __forceinline__ bool bm_continue(const uint32_t* __restrict__ bits,
             } else if (d >= nbits) {
                 i = m;
             } else {
-                const uint32_t w = kGlobal ? __ldg(bits + (d >> 5)) : bits[d >> 5];
-                const uint32_t rk = kGlobal ? __ldg(rank + (d >> 5)) : rank[d >> 5];
-                i = rk + __popc(w & ((2u << (d & 31)) - 1u));
+                const uint32_t w = __ldg(bits + (d >> 5));
+                i = __ldg(rank + (d >> 5)) + __popc(w & ((2u << (d & 31)) - 1u));
             }
             if (i - ov > slack_r || j - ov > slack_s) {
                 if (kFull) *ov_out = 0;
@@ -672,52 +675,58 @@ __device__ __forceinline__ uint32_t req_u32(const KParams& p, uint32_t m, uint32
 
 // Verify one run whose probe has a bitmap, in two phases per warp:
 //  1. every lane tests the first 8 tokens of each of its kRunItems candidates (staged in
-//     shared memory) against the bitmap; the pair is decided when |s| <= 8, when the overlap
-//     already reaches `required` (not in results mode), or when the s-side bound
+//     shared memory at hd) against the probe; the pair is decided when |s| <= 8, when the
+//     overlap already reaches `required` (not in results mode), or when the s-side bound
 //     (verify.hpp:58) rejects it; otherwise (slot, s, |s|, required, overlap) goes to the
 //     warp's queue (in the heads area, behind the items still to be read);
 //  2. the queue is drained 32 entries per round with bm_continue (no divergence between
 //     lanes whose pairs need one block and lanes whose pairs need several).
-template <int kOut, bool kStats, bool kGlobal>
-__device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R, const uint2* d,
-                                           const uint32_t* __restrict__ bits,
-                                           const uint32_t* __restrict__ rank, uint4* wq,
+// pos8[q] / n[q]: the candidate's CSR position and size (pos8 = kNone: no candidate);
+// kPacked: the staged heads are packed records (tokens in the low 24 bits).
+template <int kOut, bool kStats, bool kMap, bool kPacked>
+__device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
+                                           const uint32_t* pos8, const uint32_t* nn,
+                                           const uint8_t* __restrict__ map, uint4* hd,
                                            unsigned& count, unsigned& prunes,
                                            unsigned& verified) {
     constexpr bool kFull = kOut == kOutResults;
     constexpr uint32_t T = kRunThreads, I = kRunItems;
     const uint32_t lane = threadIdx.x & 31, tid = threadIdx.x;
     const uint32_t m = R.rsize, lo = R.lo, nbits = R.nw * 32u;
-    uint32_t req[I];
-#pragma unroll
-    for (uint32_t q = 0; q < I; ++q) req[q] = d[q].x != kNone ? req_u32(p, m, d[q].y) : 0u;
+    const uint32_t* bits = p.bm_bits + R.bofs;
+    const uint32_t* rank = p.bm_rank + R.bofs;
     uint32_t nq = 0;
 #pragma unroll
     for (uint32_t q = 0; q < I; ++q) {
         const uint32_t slot = R.begin + q * T + tid;
-        const bool valid = d[q].x != kNone;
-        const uint32_t n = d[q].y, rq = req[q];
+        const bool valid = pos8[q] != kNone;
+        const uint32_t n = nn[q];
+        const uint32_t rq = valid ? dev_required_fast(p.pred, m, n) : 0u;
         const bool inrange = valid && rq >= 1 && rq <= min(m, n);
         const bool deferred = warp_defer(p, inrange && n > kLongPair, slot);
         bool met = valid && rq == 0, decided = true;
         uint32_t ov = 0;
         if (inrange && !deferred) {
-            const uint4 w0 = wq[(q * 2) * 32 + lane], w1 = wq[(q * 2 + 1) * 32 + lane];
-            const uint32_t t8[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-            ov = count8<kGlobal>(bits, lo, nbits, t8);
+            const uint4 w0 = hd[(q * 32 + lane) * 2], w1 = hd[(q * 32 + lane) * 2 + 1];
+            uint32_t t8[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            if (kPacked) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) t8[u] &= kHeadTokenMask;
+            }
+            ov = count8<kMap>(map, bits, lo, nbits, t8);
             if (n <= 8) met = ov >= rq;
             else if (!kFull && ov >= rq) met = true;
             else if (ov < rq && 8u - ov > n - rq) met = false;
             else decided = false;
         } else if (kFull && met) {
             ov = full_overlap_seq(p.tokens + (size_t)R.rpos8 * 8, m,
-                                  p.tokens + (size_t)d[q].x * 8, n);
+                                  p.tokens + (size_t)pos8[q] * 8, n);
         }
         __syncwarp();  // heads of item q read by every lane before the queue may cover them
         const unsigned qmask = __ballot_sync(0xffffffffu, !decided);
         if (!decided)
-            wq[nq + __popc(qmask & ((1u << lane) - 1u))] =
-                make_uint4(slot, d[q].x, n, rq | (ov << 16));
+            hd[nq + __popc(qmask & ((1u << lane) - 1u))] =
+                make_uint4(slot, pos8[q], n, rq | (ov << 16));
         nq += __popc(qmask);
         if (valid && decided && !deferred) {
             if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
@@ -735,11 +744,11 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R, 
         bool met = false;
         uint32_t ov = 0, slot = 0;
         if (e < nq) {
-            const uint4 qe = wq[e];
+            const uint4 qe = hd[e];
             slot = qe.x;
             const uint32_t n = qe.z, rq = qe.w & 0xFFFFu;
-            met = bm_continue<kFull, kGlobal>(bits, rank, lo, nbits, m,
-                                              p.tokens + (size_t)qe.y * 8, n, rq, qe.w >> 16, &ov);
+            met = bm_continue<kFull, kMap>(map, bits, rank, lo, nbits, m,
+                                           p.tokens + (size_t)qe.y * 8, n, rq, qe.w >> 16, &ov);
             if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
             if (kStats) {
                 ++verified;
@@ -749,13 +758,14 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R, 
         }
         if (kFull) warp_append(p, met, slot, ov);
     }
-    __syncwarp();  // queue read before the next run's heads land here
+    __syncwarp();  // queue read before the next heads land here
 }
 
 // A run whose probe has no bitmap: thread-sequential early-exit merge per candidate.
-template <int kOut, bool kStats>
-__device__ __forceinline__ void run_merge(const KParams& p, const RunState& R, const uint2* d,
-                                          const uint4* wq, unsigned& count, unsigned& prunes,
+template <int kOut, bool kStats, bool kPacked>
+__device__ __forceinline__ void run_merge(const KParams& p, const RunState& R,
+                                          const uint32_t* pos8, const uint32_t* nn,
+                                          const uint4* hd, unsigned& count, unsigned& prunes,
                                           unsigned& verified) {
     constexpr bool kFull = kOut == kOutResults;
     constexpr uint32_t T = kRunThreads, I = kRunItems;
@@ -765,17 +775,20 @@ __device__ __forceinline__ void run_merge(const KParams& p, const RunState& R, c
 #pragma unroll
     for (uint32_t q = 0; q < I; ++q) {
         const uint32_t slot = R.begin + q * T + tid;
-        const bool valid = d[q].x != kNone;
-        const uint32_t n = d[q].y;
-        const uint32_t rq = valid ? req_u32(p, m, n) : 0u;
+        const bool valid = pos8[q] != kNone;
+        const uint32_t n = nn[q];
+        const uint32_t rq = valid ? dev_required_fast(p.pred, m, n) : 0u;
         const bool inrange = valid && rq >= 1 && rq <= min(m, n);
         const bool deferred = warp_defer(p, inrange && n > kLongPair, slot);
         bool met = valid && rq == 0;
         uint32_t ov = 0;
-        const uint32_t* s = p.tokens + (size_t)d[q].x * 8;
+        const uint32_t* s = p.tokens + (size_t)pos8[q] * 8;
         if (inrange && !deferred) {
-            met = merge_thread<kFull>(r, m, reinterpret_cast<const uint4*>(s), n, rq,
-                                      wq[(q * 2) * 32 + lane], wq[(q * 2 + 1) * 32 + lane], &ov);
+            // the CSR (not the packed record) holds the exact tokens
+            const uint4* s4 = reinterpret_cast<const uint4*>(s);
+            const uint4 w0 = kPacked ? __ldg(s4) : hd[(q * 32 + lane) * 2];
+            const uint4 w1 = kPacked ? __ldg(s4 + 1) : hd[(q * 32 + lane) * 2 + 1];
+            met = merge_thread<kFull>(r, m, s4, n, rq, w0, w1, &ov);
         } else if (kFull && met) {
             ov = full_overlap_seq(r, m, s, n);
         }
@@ -796,135 +809,156 @@ __device__ __forceinline__ void run_merge(const KParams& p, const RunState& R, c
 // consecutive runs of the segment's list (the list follows slot order, and the runs of one
 // slice are consecutive). All CTAs thus work on one moving window of the chunk -- the
 // candidates of nearby probes share L2 -- and consecutive runs of a block usually share
-// their slice, so its bitmap is staged once.
+// their slice.
 //
-// Thread t owns slots begin + q*kRunThreads + t (q < kRunItems) of every run. Per run k:
-//   C ids of run k+2 and set descriptors {pos8, |s|} of run k+1 are prefetched into
-//   registers one run ahead; the first 32-byte sector of each of the thread's candidates of
-//   run k is fetched into shared memory by cp.async (the warp's own area, no CTA barrier);
-//   the probe bitmap of a run that starts a new slice is fetched one run ahead by one
-//   thread with a TMA bulk copy on a `full` mbarrier into one of two buffers, which warps
-//   release on an `empty` mbarrier when they move on.
-template <int kOut, bool kStats>
+// Thread t owns slots begin + q*kRunThreads + t (q < kRunItems) of every run. The first
+// 32-byte sector of each of its candidates is fetched by cp.async into the warp's head
+// buffer (the thread's own slots: no barrier): kPacked (the collection has packed head
+// records) one run ahead into the other of two buffers, with the C ids prefetched one run
+// further -- one 32-byte fetch gives the first 8 tokens, |s| and the CSR position; else set
+// descriptors are prefetched one run ahead and the CSR sector is fetched at the run's start.
+// When a run starts a new slice whose probe spans <= kRunMapRange tokens, the CTA builds the
+// probe's byte map in one of two shared buffers (zero-fill, barrier, scatter of the probe's
+// tokens, barrier); a buffer is rebuilt only after the barriers of the next slice change, so
+// nobody still reads it.
+template <int kOut, bool kStats, bool kPacked>
 __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const KParams p) {
     extern __shared__ __align__(16) uint32_t rsh[];
     constexpr uint32_t T = kRunThreads, I = kRunItems;
+    constexpr uint32_t HB = I * 2 * 32;  // uint4 per warp head buffer
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint4* const wq = reinterpret_cast<uint4*>(rsh) + warp * (I * 2 * 32);  // [item][half][lane]
-    uint32_t* const s_bits = rsh + T * I * 8;                               // [2][stride]
-    uint32_t* const s_rank = s_bits + kRunBmBufs * kRunBmStride;            // [2][stride]
-    uint64_t* const full = reinterpret_cast<uint64_t*>(s_rank + kRunBmBufs * kRunBmStride);
-    uint64_t* const empty = full + kRunBmBufs;
+    uint4* const hbase = reinterpret_cast<uint4*>(rsh) + warp * (2 * HB);  // [2 bufs][item][lane][half]
+    uint8_t* const s_map = reinterpret_cast<uint8_t*>(rsh + T * I * 8 * 2);  // [2][kRunMapBytes]
     const uint64_t nr = min((uint64_t)*p.runs_n, p.runs_cap);
     auto run_of = [&](uint64_t i) -> uint64_t {
         return ((uint64_t)blockIdx.x + (i / kRunBlock) * gridDim.x) * kRunBlock + i % kRunBlock;
     };
     unsigned count = 0, prunes = 0, verified = 0;
     if (run_of(0) < nr) {
-        if (tid == 0) {
-            for (uint32_t b = 0; b < kRunBmBufs; ++b) {
-                mbar_init(full + b, 1);
-                mbar_init(empty + b, T / 32);
-            }
-            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        }
-        __syncthreads();
-
-        auto smem_bm = [](const RunState& r) { return r.bofs != kNone && r.nw <= kRunBmWords; };
+        auto map_ok = [](const RunState& r) {
+            return r.bofs != kNone && r.nw * 32u <= kRunMapRange;
+        };
         auto load_c = [&](const RunState& r, uint32_t* c) {
 #pragma unroll
             for (uint32_t q = 0; q < I; ++q) {
                 const uint32_t slot = r.begin + q * T + tid;
                 c[q] = slot < r.end ? __ldg(p.C + slot) : kNone;
-            }
-        };
-        auto load_d = [&](const uint32_t* c, uint2* d) {
-#pragma unroll
-            for (uint32_t q = 0; q < I; ++q) {
-                d[q] = make_uint2(kNone, 0);
-                if (c[q] != kNone) {
-                    if (c[q] < p.n_sets) d[q] = __ldg(p.sets + c[q]);
-                    else flag_error(p.acc, kErrOutOfRange);
+                if (c[q] != kNone && c[q] >= p.n_sets) {
+                    flag_error(p.acc, kErrOutOfRange);
+                    c[q] = kNone;
                 }
             }
         };
-        uint32_t nload = 0;  // bitmap loads issued so far (every thread tracks it)
-        auto issue_bm = [&](const RunState& r) {
-            const uint32_t b = nload % kRunBmBufs;
-            if (tid == 0) {
-                if (nload >= kRunBmBufs) mbar_wait(empty + b, ((nload / kRunBmBufs) - 1) & 1);
-                const uint32_t bytes = bitmap_alloc_words(r.nw) * 4;
-                mbar_expect_tx(full + b, 2 * bytes);
-                bulk_g2s(s_bits + b * kRunBmStride, p.bm_bits + r.bofs, bytes, full + b);
-                bulk_g2s(s_rank + b * kRunBmStride, p.bm_rank + r.bofs, bytes, full + b);
-            }
-            ++nload;
-        };
-
-        RunState R0, R1, R2;
-        load_run(p, run_of(0), nr, R0);
-        load_run(p, run_of(1), nr, R1);
-        load_run(p, run_of(2), nr, R2);
-        load_slice(p, R0);
-        load_slice(p, R1);
-        uint32_t c[I];
-        uint2 d0[I], d1[I];
-        load_c(R0, c);
-        load_d(c, d0);
-        load_c(R1, c);
-        bool ld0 = smem_bm(R0);  // run k's bitmap is a fresh load (wait on `full`)
-        if (ld0) issue_bm(R0);
-        uint32_t L0 = nload - 1;  // load index holding run k's bitmap (if any)
-
-        for (uint64_t k = 0; run_of(k) < nr; ++k) {
-            // heads of run k -> this warp's area
+        // packed heads of the candidates c[] -> head buffer b (cp.async group per run)
+        auto issue_heads = [&](const uint32_t* c, uint32_t b) {
+            uint4* hd = hbase + b * HB;
 #pragma unroll
             for (uint32_t q = 0; q < I; ++q) {
-                if (d0[q].x != kNone) {
-                    const uint4* src = reinterpret_cast<const uint4*>(p.tokens + (size_t)d0[q].x * 8);
-                    cp_async16(wq + (q * 2) * 32 + lane, src);
-                    cp_async16(wq + (q * 2 + 1) * 32 + lane, src + 1);
+                if (c[q] != kNone) {
+                    cp_async16(hd + (q * 32 + lane) * 2, p.heads + 2 * (size_t)c[q]);
+                    cp_async16(hd + (q * 32 + lane) * 2 + 1, p.heads + 2 * (size_t)c[q] + 1);
                 }
             }
             cp_async_commit();
-            // prefetch: descriptors of run k+1, C ids of run k+2, run k+3, slice of run k+2
-            load_d(c, d1);
-            load_c(R2, c);
-            RunState R3;
-            load_run(p, run_of(k + 3), nr, R3);
-            load_slice(p, R2);
-            // bitmap of run k+1 when it starts a new slice
-            const bool ld1 = smem_bm(R1) && R1.slice != R0.slice;
-            if (ld1) issue_bm(R1);
-            const uint32_t L1 = ld1 ? nload - 1 : L0;
+        };
 
-            cp_async_wait<0>();
-            __syncwarp();
-            if (R0.bofs != kNone) {
-                if (smem_bm(R0)) {
-                    const uint32_t bb = L0 % kRunBmBufs;
-                    if (ld0) mbar_wait(full + bb, (L0 / kRunBmBufs) & 1);
-                    run_bitmap<kOut, kStats, false>(p, R0, d0, s_bits + bb * kRunBmStride,
-                                                    s_rank + bb * kRunBmStride, wq, count,
-                                                    prunes, verified);
-                } else {
-                    run_bitmap<kOut, kStats, true>(p, R0, d0, p.bm_bits + R0.bofs,
-                                                   p.bm_rank + R0.bofs, wq, count, prunes,
-                                                   verified);
+        RunState R0, R1;
+        load_run(p, run_of(0), nr, R0);
+        load_run(p, run_of(1), nr, R1);
+        load_slice(p, R0);
+        uint32_t c[I];
+        uint2 d0[I];  // !kPacked: set descriptors of run k (then k+1)
+        load_c(R0, c);
+        if (kPacked) {
+            issue_heads(c, 0);
+        } else {
+#pragma unroll
+            for (uint32_t q = 0; q < I; ++q) d0[q] = c[q] != kNone ? __ldg(p.sets + c[q]) : make_uint2(kNone, 0);
+        }
+        load_c(R1, c);
+        uint32_t map_slice = kNone, mb = 1;  // slice whose map is in buffer mb
+
+        for (uint64_t k = 0; run_of(k) < nr; ++k) {
+            const uint32_t hb = (uint32_t)k & 1u;
+            uint4* const hd = hbase + hb * HB;
+            uint2 d1[I];
+            if (kPacked) {
+                issue_heads(c, hb ^ 1u);  // run k+1
+            } else {
+                // heads of run k (cp.async) and descriptors of run k+1
+#pragma unroll
+                for (uint32_t q = 0; q < I; ++q) {
+                    if (d0[q].x != kNone) {
+                        const uint4* src = reinterpret_cast<const uint4*>(p.tokens + (size_t)d0[q].x * 8);
+                        cp_async16(hd + (q * 32 + lane) * 2, src);
+                        cp_async16(hd + (q * 32 + lane) * 2 + 1, src + 1);
+                    }
+                }
+                cp_async_commit();
+#pragma unroll
+                for (uint32_t q = 0; q < I; ++q) d1[q] = c[q] != kNone ? __ldg(p.sets + c[q]) : make_uint2(kNone, 0);
+            }
+            // prefetch: slice of run k+1, C ids of run k+2, run k+2
+            load_slice(p, R1);
+            RunState R2;
+            load_run(p, run_of(k + 2), nr, R2);
+            load_c(R2, c);
+
+            // the probe's byte map (CTA-uniform condition)
+            const bool use_map = map_ok(R0);
+            if (use_map && R0.slice != map_slice) {
+                mb ^= 1u;
+                map_slice = R0.slice;
+                uint8_t* mp = s_map + mb * kRunMapBytes;
+                const uint32_t range = R0.nw * 32u;
+                const uint32_t* r = p.tokens + (size_t)R0.rpos8 * 8;
+                for (uint32_t u = tid; u * 16 <= range; u += T)
+                    reinterpret_cast<uint4*>(mp)[u] = make_uint4(0, 0, 0, 0);
+                __syncthreads();
+                for (uint32_t i = tid; i < R0.rsize; i += T) mp[__ldg(r + i) - R0.lo] = 1;
+                __syncthreads();
+            }
+
+            uint32_t pos8[I], nn[I];
+            if (kPacked) {
+                cp_async_wait<1>();  // run k's group (run k+1's may stay in flight)
+                __syncwarp();
+#pragma unroll
+                for (uint32_t q = 0; q < I; ++q) {
+                    const uint32_t slot = R0.begin + q * T + tid;
+                    pos8[q] = kNone;
+                    nn[q] = 0;
+                    if (slot < R0.end) {
+                        const uint4 w0 = hd[(q * 32 + lane) * 2], w1 = hd[(q * 32 + lane) * 2 + 1];
+                        pos8[q] = __byte_perm(__byte_perm(w0.x, w0.y, 0x0073), __byte_perm(w0.z, w0.w, 0x0073), 0x5410);
+                        nn[q] = __byte_perm(__byte_perm(w1.x, w1.y, 0x0073), __byte_perm(w1.z, w1.w, 0x0073), 0x5410);
+                    }
                 }
             } else {
-                run_merge<kOut, kStats>(p, R0, d0, wq, count, prunes, verified);
+                cp_async_wait<0>();
+                __syncwarp();
+#pragma unroll
+                for (uint32_t q = 0; q < I; ++q) {
+                    pos8[q] = d0[q].x;
+                    nn[q] = d0[q].y;
+                }
             }
-            // moving to a new bitmap: release the previous one (one arrival per warp)
-            if (ld1 && L1 > 0 && lane == 0) mbar_arrive(empty + (L1 - 1) % kRunBmBufs);
+            if (use_map) {
+                run_bitmap<kOut, kStats, true, kPacked>(p, R0, pos8, nn, s_map + mb * kRunMapBytes,
+                                                        hd, count, prunes, verified);
+            } else if (R0.bofs != kNone) {
+                run_bitmap<kOut, kStats, false, kPacked>(p, R0, pos8, nn, nullptr, hd, count,
+                                                         prunes, verified);
+            } else {
+                run_merge<kOut, kStats, kPacked>(p, R0, pos8, nn, hd, count, prunes, verified);
+            }
 
-            ld0 = ld1;
-            L0 = L1;
             R0 = R1;
             R1 = R2;
-            R2 = R3;
+            if (!kPacked) {
 #pragma unroll
-            for (uint32_t q = 0; q < I; ++q) d0[q] = d1[q];
+                for (uint32_t q = 0; q < I; ++q) d0[q] = d1[q];
+            }
         }
     }
     acc_add(p.acc, 0, count);
@@ -1295,6 +1329,25 @@ cudaError_t launch_prep(const KParams& p, cudaStream_t st, int* launches) {
     return cudaGetLastError();
 }
 
+__global__ void build_heads_kernel(const uint32_t* __restrict__ tokens, const uint2* __restrict__ sets,
+                                   uint32_t n_sets, uint4* __restrict__ heads,
+                                   unsigned* __restrict__ max_token) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_sets) return;
+    const uint2 sd = sets[i];
+    const uint32_t* t = tokens + (size_t)sd.x * 8;
+    uint32_t v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t info = q < 4 ? (sd.x >> (8 * q)) & 0xFFu : (sd.y >> (8 * (q - 4))) & 0xFFu;
+        const uint32_t tok = (uint32_t)q < sd.y ? (t[q] & kHeadTokenMask) : kHeadTokenMask;
+        v[q] = tok | (info << 24);
+    }
+    heads[2 * (size_t)i] = make_uint4(v[0], v[1], v[2], v[3]);
+    heads[2 * (size_t)i + 1] = make_uint4(v[4], v[5], v[6], v[7]);
+    if (sd.y) atomicMax(max_token, t[sd.y - 1]);  // sets are sorted: the last token is the largest
+}
+
 int sm_count() {
     static int cached[64] = {};
     int dev = 0;
@@ -1314,11 +1367,11 @@ cudaError_t launch_tiles_t(const KParams& p, uint32_t tile_begin, uint32_t tile_
     const int sms = sm_count();
     const uint32_t nt = tile_end - tile_begin;
     runs_gen_kernel<<<(nt + 255) / 256, 256, 0, st>>>(p, tile_begin, tile_end);
-    auto rk = run_kernel<kOut, kStats>;
-    static bool attr = false;  // per instantiation; the attribute is per device function
-    if (!attr) {
+    auto rk = p.heads ? run_kernel<kOut, kStats, true> : run_kernel<kOut, kStats, false>;
+    static bool attr[2] = {false, false};  // per instantiation; the attribute is per function
+    if (!attr[p.heads ? 1 : 0]) {
         cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRunSmemBytes);
-        attr = true;
+        attr[p.heads ? 1 : 0] = true;
     }
     rk<<<sms * kRunMinBlocks, kRunThreads, kRunSmemBytes, st>>>(p);
     warp_tile_kernel<kOut, kStats><<<sms * kTileMinBlocks, kThreadsA, 0, st>>>(p);
@@ -1391,6 +1444,13 @@ cudaError_t launch_path(const KParams& p, int out, uint32_t group, cudaStream_t 
 cudaError_t launch_read_bw(const void* buf, uint64_t bytes, uint32_t reps, unsigned* sink,
                            cudaStream_t st) {
     read_bw_kernel<<<148 * 8, 512, 0, st>>>(static_cast<const uint4*>(buf), bytes / 16, reps, sink);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_build_heads(const uint32_t* tokens, const uint2* sets, uint32_t n_sets,
+                               uint4* heads, unsigned* max_token, cudaStream_t st) {
+    if (!n_sets) return cudaSuccess;
+    build_heads_kernel<<<(n_sets + 255) / 256, 256, 0, st>>>(tokens, sets, n_sets, heads, max_token);
     return cudaGetLastError();
 }
 

@@ -39,7 +39,7 @@ constexpr uint32_t kLongPair = 256;            // candidates longer than this go
 #define SSJB_RUN_MIN_BLOCKS 4
 #endif
 #ifndef SSJB_RUN_BLOCK
-#define SSJB_RUN_BLOCK 8
+#define SSJB_RUN_BLOCK 16
 #endif
 #ifndef SSJB_RUN_THREADS
 #define SSJB_RUN_THREADS 256
@@ -51,15 +51,13 @@ constexpr uint32_t kRunThreads = SSJB_RUN_THREADS;
 constexpr uint32_t kRunItems = SSJB_RUN_ITEMS;          // slots per thread per run
 constexpr uint32_t kRun = kRunThreads * kRunItems;      // slots per run
 constexpr uint32_t kRunMinSlice = SSJB_RUN_MIN_SLICE;
-constexpr uint32_t kRunBmWords = 1024;                  // bitmap words staged in shared memory
-constexpr uint32_t kRunBmStride = kRunBmWords + 4;      // + the zero word (16-byte rounded)
-constexpr uint32_t kRunBmBufs = 2;
+constexpr uint32_t kRunMapRange = 8160;                 // probe token range held as a byte map
+constexpr uint32_t kRunMapBytes = 8192;                 // per map buffer (range + empty entry)
 constexpr int kRunMinBlocks = SSJB_RUN_MIN_BLOCKS;
 constexpr uint32_t kRunBlock = SSJB_RUN_BLOCK;          // consecutive runs per CTA turn
-// shared memory: candidate heads [warp][item][half][lane] uint4 (reused as the warp's
-// continuation queue), 2 bitmap buffers (bits + rank), 4 mbarriers
-constexpr size_t kRunSmemBytes = (size_t)kRunThreads * kRunItems * 32 +
-                                 (size_t)2 * kRunBmBufs * kRunBmStride * 4 + 4 * 8;
+// shared memory: two candidate-head buffers per warp [buf][item][lane] 32 bytes (the
+// current one doubles as the warp's continuation queue), two probe byte maps
+constexpr size_t kRunSmemBytes = (size_t)kRunThreads * kRunItems * 32 * 2 + 2 * kRunMapBytes;
 
 struct RunDesc {
     uint32_t slice;  // slice index
@@ -95,6 +93,7 @@ struct KParams {
     uint32_t* tile_first;        // [n_tiles + 1], first slice with end > t * kTile
     uint32_t n_tiles;
     PredDev pred;
+    const uint4* heads;             // packed set heads, 2 x uint4 per set (nullable)
     const uint32_t* req_tab;        // Jaccard/Dice: required overlap by |r|+|s| (nullable)
     uint32_t req_tab_n;
     SliceDesc* slices;              // strategy A: per-slice descriptors (nullable otherwise)
@@ -120,7 +119,17 @@ struct KParams {
 
 enum OutKind : int { kOutCount = 0, kOutFlags = 1, kOutResults = 2 };
 
+// Packed set heads: one 32-byte record per set -- the set's first 8 tokens (0x00FFFFFF past
+// |s|) in the low 24 bits, and in the top bytes of tokens 0..3 / 4..7 the set's CSR
+// position pos8 / size |s| (little-endian). Usable when every token is < kHeadTokenLimit
+// (then the padding value lies outside every probe bitmap's range).
+constexpr uint32_t kHeadTokenMask = 0x00FFFFFFu;
+constexpr uint32_t kHeadTokenLimit = 0x00FFFFE0u;
+
 // Launchers (stream-ordered, no synchronisation). Return cudaGetLastError().
+// Build the packed heads of a collection; *max_token receives the largest token (atomicMax).
+cudaError_t launch_build_heads(const uint32_t* tokens, const uint2* sets, uint32_t n_sets,
+                               uint4* heads, unsigned* max_token, cudaStream_t st);
 // prep_kernel (+ bitmap_kernel when p.slices && p.bm_cap): validation, tile index, slice
 // descriptors and probe bitmaps. Returns the number of kernels launched through *launches.
 cudaError_t launch_prep(const KParams& p, cudaStream_t st, int* launches = nullptr);
