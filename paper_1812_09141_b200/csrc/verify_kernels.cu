@@ -548,48 +548,6 @@ __device__ __forceinline__ void load_slice(const KParams& p, RunState& r) {
     }
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(gmem)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// TMA bulk copy global -> shared, completion counted on `bar` (bytes multiple of 16).
-__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes,
-                                         uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-            smem_u32(smem)),
-        "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
 // Membership of 8 tokens in the probe: tokens outside [lo, lo + R) -- including the padding
 // past |s| -- are clamped onto entry R, which is always empty, so a block costs 8
 // unconditional lookups.
@@ -665,12 +623,6 @@ __device__ __forceinline__ bool warp_defer(const KParams& p, bool want, uint32_t
     if (idx >= p.defer_cap) return false;  // cannot happen: one entry per slot of the segment
     p.defer[idx] = slot;
     return true;
-}
-
-__device__ __forceinline__ uint32_t req_u32(const KParams& p, uint32_t m, uint32_t n) {
-    const uint32_t sum = m + n;
-    if (p.req_tab && sum >= m && sum < p.req_tab_n) return __ldg(p.req_tab + sum);
-    return (uint32_t)min(dev_required(p.pred, m, n), (uint64_t)0xFFFFFFFFu);
 }
 
 // Verify one run whose probe has a bitmap, in two phases per warp:
@@ -826,15 +778,19 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
     extern __shared__ __align__(16) uint32_t rsh[];
     constexpr uint32_t T = kRunThreads, I = kRunItems;
     constexpr uint32_t HB = I * 2 * 32;  // uint4 per warp head buffer
+    constexpr uint32_t NB = kRunHeadBufs;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint4* const hbase = reinterpret_cast<uint4*>(rsh) + warp * (2 * HB);  // [2 bufs][item][lane][half]
-    uint8_t* const s_map = reinterpret_cast<uint8_t*>(rsh + T * I * 8 * 2);  // [2][kRunMapBytes]
-    const uint64_t nr = min((uint64_t)*p.runs_n, p.runs_cap);
-    auto run_of = [&](uint64_t i) -> uint64_t {
-        return ((uint64_t)blockIdx.x + (i / kRunBlock) * gridDim.x) * kRunBlock + i % kRunBlock;
+    uint4* const hbase = reinterpret_cast<uint4*>(rsh) + warp * (NB * HB);  // [bufs][item][lane][half]
+    uint8_t* const s_map = reinterpret_cast<uint8_t*>(rsh + T * I * 8 * NB);  // [2][kRunMapBytes]
+    const uint32_t nr = (uint32_t)min((uint64_t)*p.runs_n, p.runs_cap);
+    // this CTA's runs: blocks blockIdx.x, blockIdx.x + G, ... of kRunBlock consecutive runs
+    const uint32_t stride = (gridDim.x - 1) * kRunBlock;
+    auto next_run = [&](uint32_t r) -> uint32_t {
+        return ((r + 1) % kRunBlock) ? r + 1 : r + 1 + stride;
     };
     unsigned count = 0, prunes = 0, verified = 0;
-    if (run_of(0) < nr) {
+    const uint32_t first = blockIdx.x * kRunBlock;
+    if (first < nr) {
         auto map_ok = [](const RunState& r) {
             return r.bofs != kNone && r.nw * 32u <= kRunMapRange;
         };
@@ -842,48 +798,61 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
 #pragma unroll
             for (uint32_t q = 0; q < I; ++q) {
                 const uint32_t slot = r.begin + q * T + tid;
-                c[q] = slot < r.end ? __ldg(p.C + slot) : kNone;
-                if (c[q] != kNone && c[q] >= p.n_sets) {
-                    flag_error(p.acc, kErrOutOfRange);
-                    c[q] = kNone;
-                }
+                c[q] = slot < r.end ? __ldg(p.C + slot) : kNone;  // checked when used
             }
         };
-        // packed heads of the candidates c[] -> head buffer b (cp.async group per run)
-        auto issue_heads = [&](const uint32_t* c, uint32_t b) {
+        // packed heads of the candidates c[] -> head buffer b (cp.async group per run);
+        // returns the mask of items with a candidate
+        auto issue_heads = [&](const uint32_t* c, uint32_t b) -> uint32_t {
             uint4* hd = hbase + b * HB;
+            uint32_t vm = 0;
 #pragma unroll
             for (uint32_t q = 0; q < I; ++q) {
-                if (c[q] != kNone) {
+                if (c[q] < p.n_sets) {
                     cp_async16(hd + (q * 32 + lane) * 2, p.heads + 2 * (size_t)c[q]);
                     cp_async16(hd + (q * 32 + lane) * 2 + 1, p.heads + 2 * (size_t)c[q] + 1);
+                    vm |= 1u << q;
+                } else if (c[q] != kNone) {
+                    flag_error(p.acc, kErrOutOfRange);
                 }
             }
             cp_async_commit();
+            return vm;
+        };
+        auto load_d = [&](const uint32_t* c, uint2* d) {
+#pragma unroll
+            for (uint32_t q = 0; q < I; ++q) {
+                d[q] = make_uint2(kNone, 0);
+                if (c[q] < p.n_sets) d[q] = __ldg(p.sets + c[q]);
+                else if (c[q] != kNone) flag_error(p.acc, kErrOutOfRange);
+            }
         };
 
+        uint32_t run0 = first, run1 = next_run(first), run2 = next_run(run1);
         RunState R0, R1;
-        load_run(p, run_of(0), nr, R0);
-        load_run(p, run_of(1), nr, R1);
+        load_run(p, run0, nr, R0);
+        load_run(p, run1, nr, R1);
         load_slice(p, R0);
         uint32_t c[I];
         uint2 d0[I];  // !kPacked: set descriptors of run k (then k+1)
         load_c(R0, c);
+        uint32_t vm0 = 0;  // kPacked: items of run k with a candidate
         if (kPacked) {
-            issue_heads(c, 0);
+            if (NB == 2) vm0 = issue_heads(c, 0);
         } else {
-#pragma unroll
-            for (uint32_t q = 0; q < I; ++q) d0[q] = c[q] != kNone ? __ldg(p.sets + c[q]) : make_uint2(kNone, 0);
+            load_d(c, d0);
         }
-        load_c(R1, c);
+        if (!kPacked || NB == 2) load_c(R1, c);
         uint32_t map_slice = kNone, mb = 1;  // slice whose map is in buffer mb
 
-        for (uint64_t k = 0; run_of(k) < nr; ++k) {
-            const uint32_t hb = (uint32_t)k & 1u;
+        for (uint32_t k = 0; run0 < nr; ++k) {
+            const uint32_t hb = NB == 2 ? (k & 1u) : 0u;
             uint4* const hd = hbase + hb * HB;
             uint2 d1[I];
+            uint32_t vm1 = 0;
             if (kPacked) {
-                issue_heads(c, hb ^ 1u);  // run k+1
+                vm1 = issue_heads(c, NB == 2 ? hb ^ 1u : 0u);  // run k+1 (double buffer) or run k
+                if (NB == 1) vm0 = vm1;
             } else {
                 // heads of run k (cp.async) and descriptors of run k+1
 #pragma unroll
@@ -895,14 +864,13 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
                     }
                 }
                 cp_async_commit();
-#pragma unroll
-                for (uint32_t q = 0; q < I; ++q) d1[q] = c[q] != kNone ? __ldg(p.sets + c[q]) : make_uint2(kNone, 0);
+                load_d(c, d1);
             }
-            // prefetch: slice of run k+1, C ids of run k+2, run k+2
+            // prefetch: slice of run k+1, C ids of run k+2 (k+1 when single-buffered), run k+2
             load_slice(p, R1);
             RunState R2;
-            load_run(p, run_of(k + 2), nr, R2);
-            load_c(R2, c);
+            load_run(p, run2, nr, R2);
+            load_c((!kPacked || NB == 2) ? R2 : R1, c);
 
             // the probe's byte map (CTA-uniform condition)
             const bool use_map = map_ok(R0);
@@ -921,14 +889,14 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
 
             uint32_t pos8[I], nn[I];
             if (kPacked) {
-                cp_async_wait<1>();  // run k's group (run k+1's may stay in flight)
+                if (NB == 2) cp_async_wait<1>();  // run k's group (run k+1's may stay in flight)
+                else cp_async_wait<0>();
                 __syncwarp();
 #pragma unroll
                 for (uint32_t q = 0; q < I; ++q) {
-                    const uint32_t slot = R0.begin + q * T + tid;
                     pos8[q] = kNone;
                     nn[q] = 0;
-                    if (slot < R0.end) {
+                    if (vm0 >> q & 1u) {
                         const uint4 w0 = hd[(q * 32 + lane) * 2], w1 = hd[(q * 32 + lane) * 2 + 1];
                         pos8[q] = __byte_perm(__byte_perm(w0.x, w0.y, 0x0073), __byte_perm(w0.z, w0.w, 0x0073), 0x5410);
                         nn[q] = __byte_perm(__byte_perm(w1.x, w1.y, 0x0073), __byte_perm(w1.z, w1.w, 0x0073), 0x5410);
@@ -955,6 +923,10 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
 
             R0 = R1;
             R1 = R2;
+            run0 = run1;
+            run1 = run2;
+            run2 = next_run(run2);
+            vm0 = vm1;
             if (!kPacked) {
 #pragma unroll
                 for (uint32_t q = 0; q < I; ++q) d0[q] = d1[q];

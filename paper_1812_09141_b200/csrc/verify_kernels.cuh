@@ -57,7 +57,12 @@ constexpr int kRunMinBlocks = SSJB_RUN_MIN_BLOCKS;
 constexpr uint32_t kRunBlock = SSJB_RUN_BLOCK;          // consecutive runs per CTA turn
 // shared memory: two candidate-head buffers per warp [buf][item][lane] 32 bytes (the
 // current one doubles as the warp's continuation queue), two probe byte maps
-constexpr size_t kRunSmemBytes = (size_t)kRunThreads * kRunItems * 32 * 2 + 2 * kRunMapBytes;
+#ifndef SSJB_RUN_HEAD_BUFS
+#define SSJB_RUN_HEAD_BUFS 2
+#endif
+constexpr uint32_t kRunHeadBufs = SSJB_RUN_HEAD_BUFS;  // 2: heads of run k+1 fetched during run k
+constexpr size_t kRunSmemBytes =
+    (size_t)kRunThreads * kRunItems * 32 * kRunHeadBufs + 2 * kRunMapBytes;
 
 struct RunDesc {
     uint32_t slice;  // slice index
