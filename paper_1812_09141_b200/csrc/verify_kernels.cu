@@ -635,10 +635,11 @@ __device__ __forceinline__ bool warp_defer(const KParams& p, bool want, uint32_t
 //     lanes whose pairs need one block and lanes whose pairs need several).
 // pos8[q] / n[q]: the candidate's CSR position and size (pos8 = kNone: no candidate);
 // kPacked: the staged heads are packed records (tokens in the low 24 bits).
-template <int kOut, bool kStats, bool kMap, bool kPacked>
+template <int kOut, bool kStats, bool kMap, bool kPacked, bool kReg>
 __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
                                            const uint32_t* pos8, const uint32_t* nn,
                                            const uint8_t* __restrict__ map, uint4* hd,
+                                           const uint32_t (&hr)[kRunItems][8],
                                            unsigned& count, unsigned& prunes,
                                            unsigned& verified) {
     constexpr bool kFull = kOut == kOutResults;
@@ -659,8 +660,15 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
         bool met = valid && rq == 0, decided = true;
         uint32_t ov = 0;
         if (inrange && !deferred) {
-            const uint4 w0 = hd[(q * 32 + lane) * 2], w1 = hd[(q * 32 + lane) * 2 + 1];
-            uint32_t t8[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            uint32_t t8[8];
+            if (kReg) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) t8[u] = hr[q][u];
+            } else {
+                const uint4 w0 = hd[(q * 32 + lane) * 2], w1 = hd[(q * 32 + lane) * 2 + 1];
+                t8[0] = w0.x; t8[1] = w0.y; t8[2] = w0.z; t8[3] = w0.w;
+                t8[4] = w1.x; t8[5] = w1.y; t8[6] = w1.z; t8[7] = w1.w;
+            }
             if (kPacked) {
 #pragma unroll
                 for (int u = 0; u < 8; ++u) t8[u] &= kHeadTokenMask;
@@ -674,7 +682,7 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
             ov = full_overlap_seq(p.tokens + (size_t)R.rpos8 * 8, m,
                                   p.tokens + (size_t)pos8[q] * 8, n);
         }
-        __syncwarp();  // heads of item q read by every lane before the queue may cover them
+        if (!kReg) __syncwarp();  // heads of item q read by every lane before the queue covers them
         const unsigned qmask = __ballot_sync(0xffffffffu, !decided);
         if (!decided)
             hd[nq + __popc(qmask & ((1u << lane) - 1u))] =
@@ -714,7 +722,7 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
 }
 
 // A run whose probe has no bitmap: thread-sequential early-exit merge per candidate.
-template <int kOut, bool kStats, bool kPacked>
+template <int kOut, bool kStats, bool kPacked, bool kReg>
 __device__ __forceinline__ void run_merge(const KParams& p, const RunState& R,
                                           const uint32_t* pos8, const uint32_t* nn,
                                           const uint4* hd, unsigned& count, unsigned& prunes,
@@ -738,8 +746,8 @@ __device__ __forceinline__ void run_merge(const KParams& p, const RunState& R,
         if (inrange && !deferred) {
             // the CSR (not the packed record) holds the exact tokens
             const uint4* s4 = reinterpret_cast<const uint4*>(s);
-            const uint4 w0 = kPacked ? __ldg(s4) : hd[(q * 32 + lane) * 2];
-            const uint4 w1 = kPacked ? __ldg(s4 + 1) : hd[(q * 32 + lane) * 2 + 1];
+            const uint4 w0 = (kPacked || kReg) ? __ldg(s4) : hd[(q * 32 + lane) * 2];
+            const uint4 w1 = (kPacked || kReg) ? __ldg(s4 + 1) : hd[(q * 32 + lane) * 2 + 1];
             met = merge_thread<kFull>(r, m, s4, n, rq, w0, w1, &ov);
         } else if (kFull && met) {
             ov = full_overlap_seq(r, m, s, n);
@@ -778,10 +786,12 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
     extern __shared__ __align__(16) uint32_t rsh[];
     constexpr uint32_t T = kRunThreads, I = kRunItems;
     constexpr uint32_t HB = I * 2 * 32;  // uint4 per warp head buffer
-    constexpr uint32_t NB = kRunHeadBufs;
+    constexpr uint32_t NB = kRunHeadBufs;  // 0: heads in registers (LDG.256), queue-only buffer
+    constexpr bool kReg = NB == 0;
+    constexpr uint32_t NBS = kReg ? 1 : NB;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint4* const hbase = reinterpret_cast<uint4*>(rsh) + warp * (NB * HB);  // [bufs][item][lane][half]
-    uint8_t* const s_map = reinterpret_cast<uint8_t*>(rsh + T * I * 8 * NB);  // [2][kRunMapBytes]
+    uint4* const hbase = reinterpret_cast<uint4*>(rsh) + warp * (NBS * HB);  // [bufs][item][lane][half]
+    uint8_t* const s_map = reinterpret_cast<uint8_t*>(rsh + T * I * 8 * NBS);  // [2][kRunMapBytes]
     const uint32_t nr = (uint32_t)min((uint64_t)*p.runs_n, p.runs_cap);
     // this CTA's runs: blocks blockIdx.x, blockIdx.x + G, ... of kRunBlock consecutive runs
     const uint32_t stride = (gridDim.x - 1) * kRunBlock;
@@ -843,6 +853,7 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
             load_d(c, d0);
         }
         if (!kPacked || NB == 2) load_c(R1, c);
+        uint32_t hr[I][8];  // kReg: first 8 tokens (packed records) of run k's candidates
         uint32_t map_slice = kNone, mb = 1;  // slice whose map is in buffer mb
 
         for (uint32_t k = 0; run0 < nr; ++k) {
@@ -850,11 +861,27 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
             uint4* const hd = hbase + hb * HB;
             uint2 d1[I];
             uint32_t vm1 = 0;
-            if (kPacked) {
+            if (kReg) {
+                // run k's heads straight into registers (one 256-bit load per candidate)
+#pragma unroll
+                for (uint32_t q = 0; q < I; ++q) {
+                    const uint32_t* src = nullptr;
+                    if (kPacked) {
+                        if (c[q] < p.n_sets) src = reinterpret_cast<const uint32_t*>(p.heads + 2 * (size_t)c[q]);
+                        else if (c[q] != kNone) flag_error(p.acc, kErrOutOfRange);
+                    } else if (d0[q].x != kNone) {
+                        src = p.tokens + (size_t)d0[q].x * 8;
+                    }
+                    if (src) ld_tokens8(src, hr[q]);
+                    if (kPacked) vm1 |= (src != nullptr) << q;
+                }
+                if (kPacked) vm0 = vm1;
+                else load_d(c, d1);
+            } else if (kPacked) {
                 vm1 = issue_heads(c, NB == 2 ? hb ^ 1u : 0u);  // run k+1 (double buffer) or run k
                 if (NB == 1) vm0 = vm1;
             } else {
-                // heads of run k (cp.async) and descriptors of run k+1
+                // heads of run k (cp.async) and descriptors of run k+1 (NB >= 1 here)
 #pragma unroll
                 for (uint32_t q = 0; q < I; ++q) {
                     if (d0[q].x != kNone) {
@@ -889,21 +916,30 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
 
             uint32_t pos8[I], nn[I];
             if (kPacked) {
-                if (NB == 2) cp_async_wait<1>();  // run k's group (run k+1's may stay in flight)
-                else cp_async_wait<0>();
-                __syncwarp();
+                if (!kReg) {
+                    if (NB == 2) cp_async_wait<1>();  // run k's group (run k+1's may stay in flight)
+                    else cp_async_wait<0>();
+                    __syncwarp();
+                }
 #pragma unroll
                 for (uint32_t q = 0; q < I; ++q) {
                     pos8[q] = kNone;
                     nn[q] = 0;
                     if (vm0 >> q & 1u) {
-                        const uint4 w0 = hd[(q * 32 + lane) * 2], w1 = hd[(q * 32 + lane) * 2 + 1];
+                        uint4 w0, w1;
+                        if (kReg) {
+                            w0 = make_uint4(hr[q][0], hr[q][1], hr[q][2], hr[q][3]);
+                            w1 = make_uint4(hr[q][4], hr[q][5], hr[q][6], hr[q][7]);
+                        } else {
+                            w0 = hd[(q * 32 + lane) * 2];
+                            w1 = hd[(q * 32 + lane) * 2 + 1];
+                        }
                         pos8[q] = __byte_perm(__byte_perm(w0.x, w0.y, 0x0073), __byte_perm(w0.z, w0.w, 0x0073), 0x5410);
                         nn[q] = __byte_perm(__byte_perm(w1.x, w1.y, 0x0073), __byte_perm(w1.z, w1.w, 0x0073), 0x5410);
                     }
                 }
             } else {
-                cp_async_wait<0>();
+                if (!kReg) cp_async_wait<0>();
                 __syncwarp();
 #pragma unroll
                 for (uint32_t q = 0; q < I; ++q) {
@@ -912,13 +948,13 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
                 }
             }
             if (use_map) {
-                run_bitmap<kOut, kStats, true, kPacked>(p, R0, pos8, nn, s_map + mb * kRunMapBytes,
-                                                        hd, count, prunes, verified);
+                run_bitmap<kOut, kStats, true, kPacked, kReg>(p, R0, pos8, nn, s_map + mb * kRunMapBytes,
+                                                              hd, hr, count, prunes, verified);
             } else if (R0.bofs != kNone) {
-                run_bitmap<kOut, kStats, false, kPacked>(p, R0, pos8, nn, nullptr, hd, count,
-                                                         prunes, verified);
+                run_bitmap<kOut, kStats, false, kPacked, kReg>(p, R0, pos8, nn, nullptr, hd, hr,
+                                                               count, prunes, verified);
             } else {
-                run_merge<kOut, kStats, kPacked>(p, R0, pos8, nn, hd, count, prunes, verified);
+                run_merge<kOut, kStats, kPacked, kReg>(p, R0, pos8, nn, hd, count, prunes, verified);
             }
 
             R0 = R1;

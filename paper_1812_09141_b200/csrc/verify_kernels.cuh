@@ -58,11 +58,11 @@ constexpr uint32_t kRunBlock = SSJB_RUN_BLOCK;          // consecutive runs per 
 // shared memory: two candidate-head buffers per warp [buf][item][lane] 32 bytes (the
 // current one doubles as the warp's continuation queue), two probe byte maps
 #ifndef SSJB_RUN_HEAD_BUFS
-#define SSJB_RUN_HEAD_BUFS 2
+#define SSJB_RUN_HEAD_BUFS 0
 #endif
 constexpr uint32_t kRunHeadBufs = SSJB_RUN_HEAD_BUFS;  // 2: heads of run k+1 fetched during run k
 constexpr size_t kRunSmemBytes =
-    (size_t)kRunThreads * kRunItems * 32 * kRunHeadBufs + 2 * kRunMapBytes;
+    (size_t)kRunThreads * kRunItems * 32 * (kRunHeadBufs ? kRunHeadBufs : 1) + 2 * kRunMapBytes;
 
 struct RunDesc {
     uint32_t slice;  // slice index

@@ -180,6 +180,42 @@ def test_random_chunks_vs_oracle(ssj, gpu, oracle, case):
                 assert np.array_equal(out.flags, ref["flags"]), (fn, kind, group)
 
 
+TOKEN_RANGES = [
+    # (scale, offset): tokens t -> t * scale + offset (monotone, so sets stay sorted)
+    (1, 0x00FFFFE0 - 3000),        # largest tokens just below the packed-head limit
+    (1, 0x00FFFFE0 - 1000),        # some tokens at/above the limit: descriptor + CSR path
+    (1, 1 << 28),                  # all tokens large
+    (131, 0),                      # probes spanning > 8160 tokens: bitmap read through L1
+    (4099, 0),                     # probes spanning > 256K tokens: no bitmap, merge path
+    (1, 0xFFFFFFFF - 2999),        # token 0xFFFFFFFF (the CSR padding value) is a real token
+]
+
+
+@pytest.mark.parametrize("scale,offset", TOKEN_RANGES)
+def test_token_value_ranges(ssj, gpu, oracle, scale, offset):
+    """Every token-value regime of the strategy-A path: packed head records (tokens below
+    0x00FFFFE0), set descriptors + CSR sectors otherwise, the byte map / global bitmap / merge
+    paths by probe span, and the padding value as a real token."""
+    rng = np.random.default_rng(scale * 7 + (offset & 0xFFFF))
+    base = random_collection(ssj, rng, 2500, 90, 3000, zipf=True)
+    toks = (base.tokens.astype(np.uint64) * scale + offset).astype(np.uint32)
+    coll = ssj.Collection(toks, base.offsets, base.original_id)
+    chunk = random_chunk(ssj, rng, coll, 150_000, 600, zero_width=0.05)
+    for fn, num, den, ovt in ((J, 4, 5, 1), (J, 1, 2, 1), (OV, 1, 1, 2)):
+        ref = oracle.verify_chunk(coll.tokens, coll.offsets, chunk.C, chunk.C_O,
+                                  oracle.pred(fn, num, den, ovt))
+        with engine(ssj, coll, make_pred(ssj, fn, num, den, ovt), "A", 1) as eng:
+            out = eng.verify_chunk(chunk)
+            assert out.count == ref["count"], (fn, num, den)
+            assert np.array_equal(out.flags, ref["flags"]), (fn, num, den)
+        with engine(ssj, coll, make_pred(ssj, fn, num, den, ovt), "A", 1) as eng:
+            ref2 = oracle.verify_chunk(coll.tokens, coll.offsets, chunk.C, chunk.C_O,
+                                       oracle.pred(fn, num, den, ovt), want_overlaps=True)
+            slots, ovs = eng.verify_chunk_results(chunk)
+            want = np.nonzero(ref2["flags"])[0]
+            assert np.array_equal(slots, want) and np.array_equal(ovs, ref2["overlaps"][want])
+
+
 def test_wide_threshold_u128_path(ssj, gpu, oracle):
     """num >= 2^30 takes the device u128 path of equivalent_overlap."""
     rng = np.random.default_rng(5)
