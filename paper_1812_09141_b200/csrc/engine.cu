@@ -336,7 +336,7 @@ cudaError_t launch_strategy(const ssj_engine& e, const KParams& p, int out, uint
         default: {
             cudaError_t err = ssjb::launch_tiles(p, out, stats, tile_begin, tile_end, st);
             if (err != cudaSuccess) return err;
-            return ssjb::launch_long(p, out, stats, st);
+            return ssjb::launch_long(p, out, stats, tile_begin, tile_end, st);
         }
     }
 }
@@ -452,6 +452,7 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
             const int pc = (int)(lo / piece);
             p.defer = s.ddefer + lo;
             p.defer_n = s.ddefer_n + kCounters * pc;
+            p.seg_tag = (uint32_t)pc + 1;
             p.defer_cap = hi - lo;
             p.runs = s.druns + 2 * (size_t)t0;
             p.runs_n = s.ddefer_n + kCounters * pc + 1;
@@ -1035,6 +1036,7 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
         p.bm_cap = bitmap_words_for(nC);
         p.defer = e->dev_defer;
         p.defer_n = e->dev_defer_n;
+        p.seg_tag = 1;
         p.defer_cap = nC;
         p.runs = e->dev_runs;
         p.runs_n = e->dev_defer_n + 1;

@@ -87,6 +87,17 @@ __device__ __forceinline__ bool verify_pair(const KParams& p, const uint32_t* r,
     return merge_thread<kOut == kOutResults>(r, m, s4, n, (uint32_t)req, w0, w1, ov);
 }
 
+// A pair longer than kLongPair tokens is left to long_slice_kernel: the first pass marks its
+// slice once per chunk segment (tag = segment index + 1 in the slice descriptor's spare word)
+// and lists it; long_slice_kernel re-derives the slice's long pairs from C.
+__device__ __forceinline__ void mark_long_slice(const KParams& p, uint32_t e) {
+    unsigned* mk = reinterpret_cast<unsigned*>(p.slices + e) + 6;  // SliceDesc::pad0
+    if (atomicMax(mk, p.seg_tag) < p.seg_tag) {
+        const unsigned long long idx = atomicAdd(p.defer_n, 1ull);
+        if (idx < p.defer_cap) p.defer[idx] = e;  // cap = segment slots >= marked slices
+    }
+}
+
 // First slice e in [lo, hi) whose end offset (C_O[2e+1]) is > key.
 __device__ __forceinline__ uint32_t upper_bound_ends(const uint32_t* __restrict__ C_O,
                                                      uint32_t lo, uint32_t hi, uint64_t key) {
@@ -362,12 +373,9 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
                     const uint64_t req = required_of(p, m, n);
                     bool deferred = false;
                     if (p.defer && n > kLongPair && req >= 1 && req <= (uint64_t)min(m, n)) {
-                        const unsigned long long idx = atomicAdd(p.defer_n, 1ull);
-                        if (idx < p.defer_cap) {
-                            p.defer[idx] = (uint32_t)slot;
-                            deferred = true;
-                            written = false;  // long_kernel writes it
-                        }
+                        mark_long_slice(p, e);
+                        deferred = true;
+                        written = false;  // long_slice_kernel writes it
                     }
                     if (deferred) {
                         // verdict, flag and stats come from long_kernel
@@ -609,20 +617,12 @@ __device__ __forceinline__ bool bm_continue(const uint8_t* __restrict__ map,
     return ov >= req;
 }
 
-// Warp-aggregated append of deferred long pairs (all 32 lanes call it).
-__device__ __forceinline__ bool warp_defer(const KParams& p, bool want, uint32_t slot) {
+// Long pairs of a run are left to long_slice_kernel: one lane marks the run's slice (all 32
+// lanes call it).
+__device__ __forceinline__ bool warp_defer(const KParams& p, bool want, uint32_t slice) {
     const unsigned mask = __ballot_sync(0xffffffffu, want);
-    if (!mask) return false;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(mask) - 1;
-    unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(p.defer_n, (unsigned long long)__popc(mask));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (!want) return false;
-    const unsigned long long idx = base + __popc(mask & ((1u << lane) - 1u));
-    if (idx >= p.defer_cap) return false;  // cannot happen: one entry per slot of the segment
-    p.defer[idx] = slot;
-    return true;
+    if (mask && (threadIdx.x & 31) == (uint32_t)(__ffs(mask) - 1)) mark_long_slice(p, slice);
+    return want;
 }
 
 // Verify one run whose probe has a bitmap, in two phases per warp:
@@ -656,7 +656,7 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
         const uint32_t n = nn[q];
         const uint32_t rq = valid ? dev_required_fast(p.pred, m, n) : 0u;
         const bool inrange = valid && rq >= 1 && rq <= min(m, n);
-        const bool deferred = warp_defer(p, inrange && n > kLongPair, slot);
+        const bool deferred = warp_defer(p, inrange && n > kLongPair, R.slice);
         bool met = valid && rq == 0, decided = true;
         uint32_t ov = 0;
         if (inrange && !deferred) {
@@ -739,7 +739,7 @@ __device__ __forceinline__ void run_merge(const KParams& p, const RunState& R,
         const uint32_t n = nn[q];
         const uint32_t rq = valid ? dev_required_fast(p.pred, m, n) : 0u;
         const bool inrange = valid && rq >= 1 && rq <= min(m, n);
-        const bool deferred = warp_defer(p, inrange && n > kLongPair, slot);
+        const bool deferred = warp_defer(p, inrange && n > kLongPair, R.slice);
         bool met = valid && rq == 0;
         uint32_t ov = 0;
         const uint32_t* s = p.tokens + (size_t)pos8[q] * 8;
@@ -1135,81 +1135,137 @@ __global__ void path_kernel(const KParams p, const uint32_t rcap) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Long pairs deferred by tile_kernel (candidate longer than kLongPair tokens): one warp per
-// pair. With a probe bitmap the warp reads 32 consecutive candidate tokens per step
-// (one coalesced 128-byte load), tests membership in parallel, adds popc(ballot) to the
-// overlap and evaluates the reference's bound at the exact merge position after the step's
-// last token (rank lookup). Without a bitmap it walks the merge path (path_pair, G = 32).
+// Long pairs (candidate longer than kLongPair tokens), slice-parallel: CTA per slice marked
+// by the first pass in this chunk segment. The CTA builds the probe's membership bitmap and
+// per-word rank in shared memory (zero-fill, atomicOr scatter of the probe's tokens, block
+// scan), then its warps sweep the slice's slots of the segment 32 at a time; every long
+// candidate is verified by the whole warp: 32 candidate tokens per step (one coalesced 128 B
+// load), membership lookups, popc(ballot), and the reference's bound (verify.hpp:58) at the
+// exact merge position after the step's last token (rank lookup). Probes spanning more than
+// kMaxBitmapWords words walk the merge path (path_pair) instead.
+constexpr uint32_t kLongThreads = 512;
+constexpr size_t kLongSmemBytes = (size_t)(2 * kMaxBitmapWords + 4) * 4;
+
 template <int kOut, bool kStats>
-__global__ void long_kernel(const KParams p) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+__global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams p,
+                                                                  const uint64_t seg_lo,
+                                                                  const uint64_t seg_hi) {
+    extern __shared__ __align__(16) uint32_t lsh[];
+    uint32_t* const bits = lsh;                          // [kMaxBitmapWords + 1]
+    uint32_t* const rank = lsh + kMaxBitmapWords + 4;    // [kMaxBitmapWords]
+    using Scan = cub::BlockScan<uint32_t, kLongThreads>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    constexpr uint32_t kPer = kMaxBitmapWords / kLongThreads;  // words per thread in the scan
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr uint32_t W = kLongThreads / 32;
     const uint64_t n_items = min((uint64_t)*p.defer_n, p.defer_cap);
     unsigned count = 0, prunes = 0, verified = 0;
-    for (uint64_t w = gw; w < n_items; w += n_warps) {
-        const uint64_t slot = __ldg(p.defer + w);
-        const uint32_t e = upper_bound_ends(p.C_O, 0, p.n_slices, slot);
+    for (uint64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const uint32_t e = __ldg(p.defer + it);
         const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(p.slices + e));
-        const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(p.slices + e) + 1);
         const uint32_t m = d0.z;
         const uint32_t* r = p.tokens + (size_t)d0.y * 8;
-        const uint32_t cand = __ldg(p.C + slot);  // < n_sets: checked by tile_kernel
-        const uint2 sd = __ldg(p.sets + cand);
-        const uint32_t n = sd.y;
-        const uint32_t* s = p.tokens + (size_t)sd.x * 8;
-        const uint64_t req = required_of(p, m, n);
-        bool met;
-        uint32_t ov = 0;
-        if (d0.w != kNone && req >= 1 && req <= (uint64_t)min(m, n)) {
-            const uint32_t* bits = p.bm_bits + d0.w;
-            const uint32_t* rank = p.bm_rank + d0.w;
-            const uint32_t lo = d1.x, nbits = d1.y * 32;
-            const uint32_t slack_r = m - (uint32_t)req, slack_s = n - (uint32_t)req;
-            uint32_t j = 0;
-            bool decided = false;
-            met = false;
-            while (j < n) {
-                const uint32_t cnt = min(32u, n - j);
-                const uint32_t tok = lane < cnt ? __ldg(s + j + lane) : 0u;
-                const uint32_t d = tok - lo;
-                const bool in = lane < cnt && d < nbits;
-                const uint32_t bit = in ? (__ldg(bits + (d >> 5)) >> (d & 31)) & 1u : 0u;
-                ov += __popc(__ballot_sync(0xffffffffu, bit));
-                j += cnt;
-                if (j >= n) break;
-                if (kOut != kOutResults && ov >= req) {
-                    met = true;
-                    decided = true;
-                    break;
+        const uint64_t b0 = e ? __ldg(p.C_O + 2 * (size_t)e - 1) : 0;
+        const uint64_t begin = max(b0, seg_lo), end = min((uint64_t)d0.x, seg_hi);
+        const uint32_t lo = m ? (__ldg(r) & ~31u) : 0u;
+        const uint32_t hi = m ? __ldg(r + m - 1) : 0u;
+        const uint32_t nw = m ? ((hi - lo) >> 5) + 1 : 0u;
+        const bool use_bm = m && nw <= kMaxBitmapWords && hi != 0xFFFFFFFFu;  // CTA-uniform
+        const uint32_t nbits = nw * 32u;
+        __syncthreads();  // previous slice's readers are done with the bitmap
+        if (use_bm) {
+            for (uint32_t w = tid; w <= nw; w += kLongThreads) bits[w] = 0;
+            __syncthreads();
+            for (uint32_t i = tid; i < m; i += kLongThreads) {
+                const uint32_t d = __ldg(r + i) - lo;
+                atomicOr(bits + (d >> 5), 1u << (d & 31));
+            }
+            __syncthreads();
+            uint32_t c[kPer], x[kPer];
+#pragma unroll
+            for (uint32_t q = 0; q < kPer; ++q) {
+                const uint32_t w = tid * kPer + q;
+                c[q] = w < nw ? __popc(bits[w]) : 0u;
+            }
+            Scan(scan_tmp).ExclusiveSum(c, x);
+#pragma unroll
+            for (uint32_t q = 0; q < kPer; ++q) {
+                const uint32_t w = tid * kPer + q;
+                if (w < nw) rank[w] = x[q];
+            }
+            __syncthreads();
+        }
+        for (uint64_t base = begin + (uint64_t)warp * 32; base < end; base += (uint64_t)W * 32) {
+            const uint64_t myslot = base + lane;
+            uint32_t cand = 0, n = 0, req = 0, pos = 0;
+            bool want = false;
+            if (myslot < end) {
+                cand = __ldg(p.C + myslot);
+                if (cand < p.n_sets) {  // out-of-range ids were flagged by the first pass
+                    const uint2 sd = __ldg(p.sets + cand);
+                    n = sd.y;
+                    pos = sd.x;
+                    req = dev_required_fast(p.pred, m, n);
+                    want = n > kLongPair && req >= 1 && req <= min(m, n);
                 }
-                if (ov < req) {
-                    const uint32_t tl = __shfl_sync(0xffffffffu, tok, 31);
-                    const uint32_t dl = tl - lo;
-                    uint32_t i;
-                    if (tl < lo) i = 0;
-                    else if (dl >= nbits) i = m;
-                    else i = __ldg(rank + (dl >> 5)) + __popc(__ldg(bits + (dl >> 5)) & ((2u << (dl & 31)) - 1u));
-                    if (i - ov > slack_r || j - ov > slack_s) {
-                        decided = true;
-                        break;
+            }
+            unsigned mask = __ballot_sync(0xffffffffu, want);
+            while (mask) {
+                const int l = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const uint32_t sn = __shfl_sync(0xffffffffu, n, l);
+                const uint32_t sreq = __shfl_sync(0xffffffffu, req, l);
+                const uint32_t* s = p.tokens + (size_t)__shfl_sync(0xffffffffu, pos, l) * 8;
+                const uint64_t slot = base + l;
+                bool met;
+                uint32_t ov = 0;
+                if (use_bm) {
+                    const uint32_t slack_r = m - sreq, slack_s = sn - sreq;
+                    uint32_t j = 0;
+                    bool decided = false;
+                    met = false;
+                    while (j < sn) {
+                        const uint32_t cnt = min(32u, sn - j);
+                        const uint32_t tok = lane < cnt ? __ldg(s + j + lane) : 0u;
+                        const uint32_t d = min(tok - lo, nbits);  // word nw is zero
+                        const uint32_t bit = lane < cnt ? (bits[d >> 5] >> (d & 31)) & 1u : 0u;
+                        ov += __popc(__ballot_sync(0xffffffffu, bit));
+                        j += cnt;
+                        if (j >= sn) break;
+                        if (kOut != kOutResults && ov >= sreq) {
+                            met = true;
+                            decided = true;
+                            break;
+                        }
+                        if (ov < sreq) {
+                            const uint32_t tl = __shfl_sync(0xffffffffu, tok, 31);
+                            const uint32_t dl = tl - lo;
+                            uint32_t i;
+                            if (tl < lo) i = 0;
+                            else if (dl >= nbits) i = m;
+                            else i = rank[dl >> 5] + __popc(bits[dl >> 5] & ((2u << (dl & 31)) - 1u));
+                            if (i - ov > slack_r || j - ov > slack_s) {
+                                decided = true;
+                                break;
+                            }
+                        }
+                    }
+                    if (!decided) met = ov >= sreq;
+                    if (!met) ov = 0;
+                } else {
+                    met = path_pair<32, kOut == kOutResults>(r, m, s, sn, sreq, lane, 0xffffffffu, &ov);
+                }
+                if (lane == 0) {
+                    if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
+                    count += met;
+                    if (kStats) {
+                        ++verified;
+                        prunes += (!met && (m + sn) > 0);
                     }
                 }
-            }
-            if (!decided) met = ov >= req;
-            if (!met) ov = 0;
-        } else {
-            met = path_pair<32, kOut == kOutResults>(r, m, s, n, req, lane, 0xffffffffu, &ov);
-        }
-        if (lane == 0) {
-            if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
-            count += met;
-            if (kStats) {
-                ++verified;
-                prunes += (!met && (m + n) > 0);
+                if (kOut == kOutResults) warp_append(p, met && lane == 0, slot, ov);
             }
         }
-        if (kOut == kOutResults) warp_append(p, met && lane == 0, slot, ov);
     }
     acc_add(p.acc, 0, count);
     if (kStats) {
@@ -1399,18 +1455,31 @@ cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_be
     }
 }
 
-cudaError_t launch_long(const KParams& p, int out, bool stats, cudaStream_t st) {
-    if (!p.defer) return cudaSuccess;
-    const uint32_t grid = 148 * 8, threads = 256;
-    switch (out * 2 + (stats ? 1 : 0)) {
-        case 0: long_kernel<kOutCount, false><<<grid, threads, 0, st>>>(p); break;
-        case 1: long_kernel<kOutCount, true><<<grid, threads, 0, st>>>(p); break;
-        case 2: long_kernel<kOutFlags, false><<<grid, threads, 0, st>>>(p); break;
-        case 3: long_kernel<kOutFlags, true><<<grid, threads, 0, st>>>(p); break;
-        case 4: long_kernel<kOutResults, false><<<grid, threads, 0, st>>>(p); break;
-        default: long_kernel<kOutResults, true><<<grid, threads, 0, st>>>(p); break;
+template <int kOut, bool kStats>
+cudaError_t launch_long_t(const KParams& p, uint64_t seg_lo, uint64_t seg_hi, cudaStream_t st) {
+    auto k = long_slice_kernel<kOut, kStats>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLongSmemBytes);
+        attr = true;
     }
+    k<<<sm_count() * 2, kLongThreads, kLongSmemBytes, st>>>(p, seg_lo, seg_hi);
     return cudaGetLastError();
+}
+
+cudaError_t launch_long(const KParams& p, int out, bool stats, uint32_t tile_begin,
+                        uint32_t tile_end, cudaStream_t st) {
+    if (!p.defer) return cudaSuccess;
+    const uint64_t lo = (uint64_t)tile_begin * kTile;
+    const uint64_t hi = min((uint64_t)tile_end * kTile, p.nC);
+    switch (out * 2 + (stats ? 1 : 0)) {
+        case 0: return launch_long_t<kOutCount, false>(p, lo, hi, st);
+        case 1: return launch_long_t<kOutCount, true>(p, lo, hi, st);
+        case 2: return launch_long_t<kOutFlags, false>(p, lo, hi, st);
+        case 3: return launch_long_t<kOutFlags, true>(p, lo, hi, st);
+        case 4: return launch_long_t<kOutResults, false>(p, lo, hi, st);
+        default: return launch_long_t<kOutResults, true>(p, lo, hi, st);
+    }
 }
 
 cudaError_t launch_block(const KParams& p, int out, bool stats, uint32_t threads,

@@ -105,9 +105,10 @@ struct KParams {
     uint32_t* bm_bits;              // probe membership bitmaps (word = 32 tokens)
     uint32_t* bm_rank;              // probe tokens below each bitmap word
     uint64_t bm_cap;                // bitmap words available (0 = no bitmaps)
-    uint32_t* defer;                // strategy A: slots of long pairs for long_kernel
+    uint32_t* defer;                // strategy A: slices with long pairs (this segment)
     unsigned long long* defer_n;    // their count (this launch's segment)
     uint64_t defer_cap;
+    uint32_t seg_tag;               // chunk segment index + 1 (marks in SliceDesc::pad0)
     RunDesc* runs;                  // strategy A: runs of long slices (this segment)
     unsigned long long* runs_n;
     uint64_t runs_cap;
@@ -141,8 +142,10 @@ cudaError_t launch_prep(const KParams& p, cudaStream_t st, int* launches = nullp
 // Strategy A: tiles [tile_begin, tile_end)
 cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_begin,
                          uint32_t tile_end, cudaStream_t st);
-// Strategy A, second pass: the long pairs tile_kernel deferred (one warp per pair)
-cudaError_t launch_long(const KParams& p, int out, bool stats, cudaStream_t st);
+// Strategy A, second pass: slices the first pass marked for long pairs, slots of tiles
+// [tile_begin, tile_end) (CTA per slice, bitmap in shared memory, one warp per pair)
+cudaError_t launch_long(const KParams& p, int out, bool stats, uint32_t tile_begin,
+                        uint32_t tile_end, cudaStream_t st);
 // Strategy B: block of `threads` per probe slice
 cudaError_t launch_block(const KParams& p, int out, bool stats, uint32_t threads,
                          cudaStream_t st);
