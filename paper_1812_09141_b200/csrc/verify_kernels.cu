@@ -1144,7 +1144,7 @@ __global__ void path_kernel(const KParams p, const uint32_t rcap) {
 // exact merge position after the step's last token (rank lookup). Probes spanning more than
 // kMaxBitmapWords words walk the merge path (path_pair) instead.
 constexpr uint32_t kLongThreads = 512;
-constexpr size_t kLongSmemBytes = (size_t)(2 * kMaxBitmapWords + 4) * 4;
+constexpr size_t kLongSmemBytes = (size_t)(2 * kMaxBitmapWords + 4) * 4 + kLongThreads * 16 + 16;
 
 template <int kOut, bool kStats>
 __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams p,
@@ -1153,6 +1153,8 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
     extern __shared__ __align__(16) uint32_t lsh[];
     uint32_t* const bits = lsh;                          // [kMaxBitmapWords + 1]
     uint32_t* const rank = lsh + kMaxBitmapWords + 4;    // [kMaxBitmapWords]
+    uint4* const llist = reinterpret_cast<uint4*>(rank + kMaxBitmapWords);  // [kLongThreads]
+    uint32_t* const lcount = reinterpret_cast<uint32_t*>(llist + kLongThreads);
     using Scan = cub::BlockScan<uint32_t, kLongThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
     constexpr uint32_t kPer = kMaxBitmapWords / kLongThreads;  // words per thread in the scan
@@ -1195,12 +1197,14 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
             }
             __syncthreads();
         }
-        for (uint64_t base = begin + (uint64_t)warp * 32; base < end; base += (uint64_t)W * 32) {
-            const uint64_t myslot = base + lane;
-            uint32_t cand = 0, n = 0, req = 0, pos = 0;
+        // the slice's long pairs, kLongThreads slots at a time: compacted into a shared list,
+        // then one warp per listed pair
+        for (uint64_t cb = begin; cb < end; cb += kLongThreads) {
+            const uint64_t myslot = cb + tid;
+            uint32_t n = 0, req = 0, pos = 0;
             bool want = false;
             if (myslot < end) {
-                cand = __ldg(p.C + myslot);
+                const uint32_t cand = __ldg(p.C + myslot);
                 if (cand < p.n_sets) {  // out-of-range ids were flagged by the first pass
                     const uint2 sd = __ldg(p.sets + cand);
                     n = sd.y;
@@ -1209,14 +1213,22 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                     want = n > kLongPair && req >= 1 && req <= min(m, n);
                 }
             }
-            unsigned mask = __ballot_sync(0xffffffffu, want);
-            while (mask) {
-                const int l = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const uint32_t sn = __shfl_sync(0xffffffffu, n, l);
-                const uint32_t sreq = __shfl_sync(0xffffffffu, req, l);
-                const uint32_t* s = p.tokens + (size_t)__shfl_sync(0xffffffffu, pos, l) * 8;
-                const uint64_t slot = base + l;
+            if (tid == 0) *lcount = 0;
+            __syncthreads();
+            const unsigned wm = __ballot_sync(0xffffffffu, want);
+            uint32_t wbase = 0;
+            if (lane == 0 && wm) wbase = atomicAdd(lcount, (uint32_t)__popc(wm));
+            wbase = __shfl_sync(0xffffffffu, wbase, 0);
+            if (want)
+                llist[wbase + __popc(wm & ((1u << lane) - 1u))] =
+                    make_uint4((uint32_t)(myslot - cb), pos, n, req);
+            __syncthreads();
+            const uint32_t nl = *lcount;
+            for (uint32_t li = warp; li < nl; li += W) {
+                const uint4 ent = llist[li];
+                const uint64_t slot = cb + ent.x;
+                const uint32_t sn = ent.z, sreq = ent.w;
+                const uint32_t* s = p.tokens + (size_t)ent.y * 8;
                 bool met;
                 uint32_t ov = 0;
                 if (use_bm) {
@@ -1224,9 +1236,11 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                     uint32_t j = 0;
                     bool decided = false;
                     met = false;
+                    // next step's tokens are in flight while this step is tested
+                    uint32_t tok = lane < sn ? __ldg(s + lane) : 0xFFFFFFFFu;
                     while (j < sn) {
                         const uint32_t cnt = min(32u, sn - j);
-                        const uint32_t tok = lane < cnt ? __ldg(s + j + lane) : 0u;
+                        const uint32_t nxt = j + 32 + lane < sn ? __ldg(s + j + 32 + lane) : 0xFFFFFFFFu;
                         const uint32_t d = min(tok - lo, nbits);  // word nw is zero
                         const uint32_t bit = lane < cnt ? (bits[d >> 5] >> (d & 31)) & 1u : 0u;
                         ov += __popc(__ballot_sync(0xffffffffu, bit));
@@ -1249,6 +1263,7 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                                 break;
                             }
                         }
+                        tok = nxt;
                     }
                     if (!decided) met = ov >= sreq;
                     if (!met) ov = 0;
@@ -1265,6 +1280,7 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                 }
                 if (kOut == kOutResults) warp_append(p, met && lane == 0, slot, ov);
             }
+            __syncthreads();  // list consumed
         }
     }
     acc_add(p.acc, 0, count);
