@@ -1144,6 +1144,12 @@ __global__ void path_kernel(const KParams p, const uint32_t rcap) {
 // exact merge position after the step's last token (rank lookup). Probes spanning more than
 // kMaxBitmapWords words walk the merge path (path_pair) instead.
 constexpr uint32_t kLongThreads = 512;
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
 constexpr size_t kLongSmemBytes = (size_t)(2 * kMaxBitmapWords + 4) * 4 + kLongThreads * 16 + 16;
 
 template <int kOut, bool kStats>
@@ -1155,6 +1161,8 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
     uint32_t* const rank = lsh + kMaxBitmapWords + 4;    // [kMaxBitmapWords]
     uint4* const llist = reinterpret_cast<uint4*>(rank + kMaxBitmapWords);  // [kLongThreads]
     uint32_t* const lcount = reinterpret_cast<uint32_t*>(llist + kLongThreads);
+    const uint32_t bits_s = (uint32_t)__cvta_generic_to_shared(bits);
+    const uint32_t rank_s = (uint32_t)__cvta_generic_to_shared(rank);
     using Scan = cub::BlockScan<uint32_t, kLongThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
     constexpr uint32_t kPer = kMaxBitmapWords / kLongThreads;  // words per thread in the scan
@@ -1232,19 +1240,24 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                 bool met;
                 uint32_t ov = 0;
                 if (use_bm) {
+                    // 64 candidate tokens per step (2 per lane, coalesced), the next step's
+                    // in flight; tokens past |s| read as 0xFFFFFFFF and clamp onto the
+                    // bitmap's zero word
                     const uint32_t slack_r = m - sreq, slack_s = sn - sreq;
                     uint32_t j = 0;
                     bool decided = false;
                     met = false;
-                    // next step's tokens are in flight while this step is tested
-                    uint32_t tok = lane < sn ? __ldg(s + lane) : 0xFFFFFFFFu;
-                    while (j < sn) {
-                        const uint32_t cnt = min(32u, sn - j);
-                        const uint32_t nxt = j + 32 + lane < sn ? __ldg(s + j + 32 + lane) : 0xFFFFFFFFu;
-                        const uint32_t d = min(tok - lo, nbits);  // word nw is zero
-                        const uint32_t bit = lane < cnt ? (bits[d >> 5] >> (d & 31)) & 1u : 0u;
-                        ov += __popc(__ballot_sync(0xffffffffu, bit));
-                        j += cnt;
+                    uint32_t a0 = lane < sn ? __ldg(s + lane) : 0xFFFFFFFFu;
+                    uint32_t a1 = 32 + lane < sn ? __ldg(s + 32 + lane) : 0xFFFFFFFFu;
+                    for (;;) {
+                        const uint32_t n0 = j + 64 + lane < sn ? __ldg(s + j + 64 + lane) : 0xFFFFFFFFu;
+                        const uint32_t n1 = j + 96 + lane < sn ? __ldg(s + j + 96 + lane) : 0xFFFFFFFFu;
+                        const uint32_t e0 = min(a0 - lo, nbits), e1 = min(a1 - lo, nbits);
+                        const uint32_t w0 = lds_u32(bits_s + ((e0 >> 5) << 2));
+                        const uint32_t w1 = lds_u32(bits_s + ((e1 >> 5) << 2));
+                        ov += __popc(__ballot_sync(0xffffffffu, (w0 >> (e0 & 31)) & 1u)) +
+                              __popc(__ballot_sync(0xffffffffu, (w1 >> (e1 & 31)) & 1u));
+                        j += 64;
                         if (j >= sn) break;
                         if (kOut != kOutResults && ov >= sreq) {
                             met = true;
@@ -1252,18 +1265,20 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                             break;
                         }
                         if (ov < sreq) {
-                            const uint32_t tl = __shfl_sync(0xffffffffu, tok, 31);
+                            const uint32_t tl = __shfl_sync(0xffffffffu, a1, 31);
                             const uint32_t dl = tl - lo;
                             uint32_t i;
                             if (tl < lo) i = 0;
                             else if (dl >= nbits) i = m;
-                            else i = rank[dl >> 5] + __popc(bits[dl >> 5] & ((2u << (dl & 31)) - 1u));
+                            else i = lds_u32(rank_s + ((dl >> 5) << 2)) +
+                                     __popc(lds_u32(bits_s + ((dl >> 5) << 2)) & ((2u << (dl & 31)) - 1u));
                             if (i - ov > slack_r || j - ov > slack_s) {
                                 decided = true;
                                 break;
                             }
                         }
-                        tok = nxt;
+                        a0 = n0;
+                        a1 = n1;
                     }
                     if (!decided) met = ov >= sreq;
                     if (!met) ov = 0;
