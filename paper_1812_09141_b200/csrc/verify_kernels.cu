@@ -129,10 +129,9 @@ __global__ void prep_kernel(const KParams p) {
                 const uint2 rd = p.sets[probe];
                 d0.y = rd.x;
                 d0.z = rd.y;
-                // a probe bitmap pays off for long slices, and for long probes (their long
-                // candidates are verified 32 tokens per step by long_kernel)
-                if (p.bm_cap && rd.y && end > begin &&
-                    (end - begin >= kSliceBitmapMinCands || rd.y > kLongPair)) {
+                // a probe bitmap pays off for long slices (long pairs build their own in
+                // shared memory, long_slice_kernel)
+                if (p.bm_cap && rd.y && end > begin && end - begin >= kSliceBitmapMinCands) {
                     const uint32_t* r = p.tokens + (size_t)rd.x * 8;
                     const uint32_t lo = r[0] & ~31u;
                     const uint32_t hi = r[rd.y - 1];
@@ -1144,6 +1143,10 @@ __global__ void path_kernel(const KParams p, const uint32_t rcap) {
 // exact merge position after the step's last token (rank lookup). Probes spanning more than
 // kMaxBitmapWords words walk the merge path (path_pair) instead.
 constexpr uint32_t kLongThreads = 512;
+#ifndef SSJB_LONG_PER_LANE
+#define SSJB_LONG_PER_LANE 4
+#endif
+constexpr uint32_t kLongPerLane = SSJB_LONG_PER_LANE;  // candidate tokens per lane per step
 
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     uint32_t v;
@@ -1240,24 +1243,33 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                 bool met;
                 uint32_t ov = 0;
                 if (use_bm) {
-                    // 64 candidate tokens per step (2 per lane, coalesced), the next step's
-                    // in flight; tokens past |s| read as 0xFFFFFFFF and clamp onto the
-                    // bitmap's zero word
+                    // 32 * kLongPerLane candidate tokens per step (token j + u*32 + lane in
+                    // lane `lane`, coalesced), the next step's in flight; tokens past |s| read
+                    // as 0xFFFFFFFF and clamp onto the bitmap's zero word; per-lane counts are
+                    // summed with one warp reduction
+                    constexpr uint32_t U = kLongPerLane, STEP = 32 * U;
                     const uint32_t slack_r = m - sreq, slack_s = sn - sreq;
                     uint32_t j = 0;
                     bool decided = false;
                     met = false;
-                    uint32_t a0 = lane < sn ? __ldg(s + lane) : 0xFFFFFFFFu;
-                    uint32_t a1 = 32 + lane < sn ? __ldg(s + 32 + lane) : 0xFFFFFFFFu;
+                    uint32_t a[U];
+#pragma unroll
+                    for (uint32_t u = 0; u < U; ++u)
+                        a[u] = u * 32 + lane < sn ? __ldg(s + u * 32 + lane) : 0xFFFFFFFFu;
                     for (;;) {
-                        const uint32_t n0 = j + 64 + lane < sn ? __ldg(s + j + 64 + lane) : 0xFFFFFFFFu;
-                        const uint32_t n1 = j + 96 + lane < sn ? __ldg(s + j + 96 + lane) : 0xFFFFFFFFu;
-                        const uint32_t e0 = min(a0 - lo, nbits), e1 = min(a1 - lo, nbits);
-                        const uint32_t w0 = lds_u32(bits_s + ((e0 >> 5) << 2));
-                        const uint32_t w1 = lds_u32(bits_s + ((e1 >> 5) << 2));
-                        ov += __popc(__ballot_sync(0xffffffffu, (w0 >> (e0 & 31)) & 1u)) +
-                              __popc(__ballot_sync(0xffffffffu, (w1 >> (e1 & 31)) & 1u));
-                        j += 64;
+                        uint32_t nx[U];
+#pragma unroll
+                        for (uint32_t u = 0; u < U; ++u)
+                            nx[u] = j + STEP + u * 32 + lane < sn ? __ldg(s + j + STEP + u * 32 + lane)
+                                                                  : 0xFFFFFFFFu;
+                        uint32_t c = 0;
+#pragma unroll
+                        for (uint32_t u = 0; u < U; ++u) {
+                            const uint32_t e = min(a[u] - lo, nbits);
+                            c += (lds_u32(bits_s + ((e >> 5) << 2)) >> (e & 31)) & 1u;
+                        }
+                        ov += __reduce_add_sync(0xffffffffu, c);
+                        j += STEP;
                         if (j >= sn) break;
                         if (kOut != kOutResults && ov >= sreq) {
                             met = true;
@@ -1265,7 +1277,7 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                             break;
                         }
                         if (ov < sreq) {
-                            const uint32_t tl = __shfl_sync(0xffffffffu, a1, 31);
+                            const uint32_t tl = __shfl_sync(0xffffffffu, a[U - 1], 31);
                             const uint32_t dl = tl - lo;
                             uint32_t i;
                             if (tl < lo) i = 0;
@@ -1277,8 +1289,8 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                                 break;
                             }
                         }
-                        a0 = n0;
-                        a1 = n1;
+#pragma unroll
+                        for (uint32_t u = 0; u < U; ++u) a[u] = nx[u];
                     }
                     if (!decided) met = ov >= sreq;
                     if (!met) ov = 0;
