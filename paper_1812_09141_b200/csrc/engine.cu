@@ -118,6 +118,8 @@ struct ChunkSlot {
     uint32_t* ddefer = nullptr;          // long-pair slots (strategy A)
     size_t capDf = 0;
     unsigned long long* ddefer_n = nullptr;  // kCounters counters per piece
+    uint32_t* dbmlist = nullptr;         // slices with a probe bitmap (strategy A)
+    size_t capBL = 0;
     ssjb::RunDesc* druns = nullptr;      // runs of long slices (strategy A)
     size_t capRu = 0;
     uint32_t* dshort = nullptr;          // short tiles (strategy A)
@@ -175,6 +177,8 @@ struct ssj_engine {
     uint32_t* dev_defer = nullptr;
     size_t dev_defer_cap = 0;
     unsigned long long* dev_defer_n = nullptr;  // kCounters
+    uint32_t* dev_bmlist = nullptr;
+    size_t dev_bmlist_cap = 0;
     ssjb::RunDesc* dev_runs = nullptr;
     size_t dev_runs_cap = 0;
     uint32_t* dev_short = nullptr;
@@ -318,9 +322,11 @@ int upload(ssj_engine& e, void* dst, const void* src, size_t bytes, cudaStream_t
 uint64_t bitmap_words_for(uint64_t nC) { return std::max<uint64_t>(4ull << 20, nC / 8); }
 
 int ensure_tile_scratch(ssjb::SliceDesc** slices, size_t* capS, uint32_t** bits, size_t* capB,
-                        uint32_t** rank, size_t* capR, uint32_t n_slices, uint64_t nC) {
+                        uint32_t** rank, size_t* capR, uint32_t** list, size_t* capL,
+                        uint32_t n_slices, uint64_t nC) {
     int rc;
     if ((rc = ensure_device(slices, capS, std::max<size_t>(n_slices, 1)))) return rc;
+    if ((rc = ensure_device(list, capL, std::max<size_t>(n_slices, 1)))) return rc;
     const uint64_t words = bitmap_words_for(nC);
     if ((rc = ensure_device(bits, capB, words))) return rc;
     if ((rc = ensure_device(rank, capR, words))) return rc;
@@ -371,7 +377,7 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
     if (out == ssjb::kOutFlags && (rc = ensure_device(&s.dflags, &s.capF, nC))) return rc;
     const bool tiles = e.strategy.kind == SSJ_STRATEGY_A;
     if (tiles && (rc = ensure_tile_scratch(&s.dslices, &s.capS, &s.dbits, &s.capB, &s.drank,
-                                           &s.capR, n_slices, nC)))
+                                           &s.capR, &s.dbmlist, &s.capBL, n_slices, nC)))
         return rc;
     if (tiles && (rc = ensure_device(&s.ddefer, &s.capDf, std::max<size_t>(nC, 1)))) return rc;
     if (tiles && (rc = ensure_device(&s.druns, &s.capRu, 2 * (size_t)n_tiles + 2))) return rc;
@@ -412,6 +418,7 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
         p.slices = s.dslices;
         p.bm_bits = s.dbits;
         p.bm_rank = s.drank;
+        p.bm_list = s.dbmlist;
         p.bm_cap = bitmap_words_for(nC);
     }
 
@@ -506,6 +513,7 @@ void destroy_slot(ChunkSlot& s) {
     cudaFree(s.ddefer);
     cudaFree(s.ddefer_n);
     cudaFree(s.druns);
+    cudaFree(s.dbmlist);
     cudaFree(s.dshort);
     cudaFree(s.dacc);
     cudaFreeHost(s.hacc);
@@ -812,6 +820,7 @@ void ssj_engine_destroy(ssj_engine* e) {
     cudaFree(e->dev_defer);
     cudaFree(e->dev_defer_n);
     cudaFree(e->dev_runs);
+    cudaFree(e->dev_bmlist);
     cudaFree(e->dev_short);
     cudaFree(e->d_req_tab);
     cudaFree(e->d_heads);
@@ -1010,6 +1019,7 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
     const bool tiles = e->strategy.kind == SSJ_STRATEGY_A;
     if (tiles && (rc = ensure_tile_scratch(&e->dev_slices, &e->dev_slices_cap, &e->dev_bits,
                                            &e->dev_bits_cap, &e->dev_rank, &e->dev_rank_cap,
+                                           &e->dev_bmlist, &e->dev_bmlist_cap,
                                            n_slices, nC)))
         return rc;
     if (tiles && (rc = ensure_device(&e->dev_defer, &e->dev_defer_cap, std::max<size_t>(nC, 1))))
@@ -1033,6 +1043,7 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
         p.slices = e->dev_slices;
         p.bm_bits = e->dev_bits;
         p.bm_rank = e->dev_rank;
+        p.bm_list = e->dev_bmlist;
         p.bm_cap = bitmap_words_for(nC);
         p.defer = e->dev_defer;
         p.defer_n = e->dev_defer_n;

@@ -144,6 +144,8 @@ __global__ void prep_kernel(const KParams p) {
                         const unsigned long long off = atomicAdd(p.acc + kAccBitmapWords, (unsigned long long)na);
                         if (off + na <= p.bm_cap) {
                             d0.w = (uint32_t)off;
+                            if (p.bm_list)
+                                p.bm_list[atomicAdd(p.acc + kAccBitmapSlices, 1ull)] = (uint32_t)idx;
                             d1.x = lo;
                             d1.y = nw;
                         }
@@ -168,9 +170,11 @@ __global__ void bitmap_kernel(const KParams p) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t e = warp; e < p.n_slices; e += n_warps) {
+    // one warp per slice listed by prep_kernel
+    const uint64_t n_list = *(volatile unsigned long long*)(p.acc + kAccBitmapSlices);
+    for (uint64_t it = warp; it < n_list; it += n_warps) {
+        const uint32_t e = __ldg(p.bm_list + it);
         const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(p.slices + e));
-        if (d0.w == kNone) continue;
         const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(p.slices + e) + 1);
         uint32_t* bits = p.bm_bits + d0.w;
         uint32_t* rank = p.bm_rank + d0.w;

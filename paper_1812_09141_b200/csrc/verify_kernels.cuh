@@ -83,8 +83,9 @@ struct SliceDesc {
 };
 
 // Result-block words (SSJ_RESULT_WORDS = 8): 0 count, 1 error bits, 2..4 stats,
-// 5 bitmap words allocated in this chunk.
+// 5 bitmap words allocated in this chunk, 6 slices given a bitmap.
 constexpr int kAccBitmapWords = 5;
+constexpr int kAccBitmapSlices = 6;  // 6: slices given a bitmap in this chunk
 
 // Everything a verification kernel needs. Device pointers only.
 struct KParams {
@@ -105,6 +106,7 @@ struct KParams {
     uint32_t* bm_bits;              // probe membership bitmaps (word = 32 tokens)
     uint32_t* bm_rank;              // probe tokens below each bitmap word
     uint64_t bm_cap;                // bitmap words available (0 = no bitmaps)
+    uint32_t* bm_list;              // slices given a bitmap (count in acc[kAccBitmapSlices])
     uint32_t* defer;                // strategy A: slices with long pairs (this segment)
     unsigned long long* defer_n;    // their count (this launch's segment)
     uint64_t defer_cap;
