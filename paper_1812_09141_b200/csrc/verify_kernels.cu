@@ -1146,7 +1146,10 @@ __global__ void path_kernel(const KParams p, const uint32_t rcap) {
 // load), membership lookups, popc(ballot), and the reference's bound (verify.hpp:58) at the
 // exact merge position after the step's last token (rank lookup). Probes spanning more than
 // kMaxBitmapWords words walk the merge path (path_pair) instead.
-constexpr uint32_t kLongThreads = 512;
+#ifndef SSJB_LONG_THREADS
+#define SSJB_LONG_THREADS 512
+#endif
+constexpr uint32_t kLongThreads = SSJB_LONG_THREADS;
 #ifndef SSJB_LONG_PER_LANE
 #define SSJB_LONG_PER_LANE 4
 #endif
@@ -1172,7 +1175,6 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
     const uint32_t rank_s = (uint32_t)__cvta_generic_to_shared(rank);
     using Scan = cub::BlockScan<uint32_t, kLongThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
-    constexpr uint32_t kPer = kMaxBitmapWords / kLongThreads;  // words per thread in the scan
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr uint32_t W = kLongThreads / 32;
     const uint64_t n_items = min((uint64_t)*p.defer_n, p.defer_cap);
@@ -1198,17 +1200,15 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                 atomicOr(bits + (d >> 5), 1u << (d & 31));
             }
             __syncthreads();
-            uint32_t c[kPer], x[kPer];
-#pragma unroll
-            for (uint32_t q = 0; q < kPer; ++q) {
-                const uint32_t w = tid * kPer + q;
-                c[q] = w < nw ? __popc(bits[w]) : 0u;
-            }
-            Scan(scan_tmp).ExclusiveSum(c, x);
-#pragma unroll
-            for (uint32_t q = 0; q < kPer; ++q) {
-                const uint32_t w = tid * kPer + q;
-                if (w < nw) rank[w] = x[q];
+            // rank: thread t owns words [t*per, t*per + per) of the nw words
+            const uint32_t per = (nw + kLongThreads - 1) / kLongThreads;
+            uint32_t tot = 0;
+            for (uint32_t q = 0, w = tid * per; q < per && w < nw; ++q, ++w) tot += __popc(bits[w]);
+            uint32_t x;
+            Scan(scan_tmp).ExclusiveSum(tot, x);
+            for (uint32_t q = 0, w = tid * per; q < per && w < nw; ++q, ++w) {
+                rank[w] = x;
+                x += __popc(bits[w]);
             }
             __syncthreads();
         }
@@ -1510,7 +1510,7 @@ cudaError_t launch_long_t(const KParams& p, uint64_t seg_lo, uint64_t seg_hi, cu
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLongSmemBytes);
         attr = true;
     }
-    k<<<sm_count() * 2, kLongThreads, kLongSmemBytes, st>>>(p, seg_lo, seg_hi);
+    k<<<sm_count() * (1024 / kLongThreads) * 2, kLongThreads, kLongSmemBytes, st>>>(p, seg_lo, seg_hi);
     return cudaGetLastError();
 }
 
