@@ -447,3 +447,32 @@ def test_gpu_pair_decoding(ssj, gpu, oracle, name):
             assert np.array_equal(pairs, want[order]), key
             assert np.array_equal(ovs, ref["overlaps"][slots][order]), key
             assert st.pairs_verified == chunk.C.size
+
+
+@pytest.mark.parametrize("shape", [
+    # DBLP-like: long slices -> runs, > 4M candidates -> the host path uploads C in segments
+    dict(sets=45_000, min_size=40, max_size=120, universe=7200, zipf_tokens=True,
+         token_skew=1.0, duplicate_fraction=0.02, max_edits=2, distinct_tokens=True),
+    # KOSARAK-like: tiny slices of long-tailed sets -> short tiles + the long-pair pass
+    dict(sets=500_000, min_size=2, max_size=2500, zipf_sizes=True, size_skew=1.9,
+         universe=41_000, zipf_tokens=True, token_skew=0.6, duplicate_fraction=0.05,
+         max_edits=2),
+])
+def test_large_segmented_chunks_vs_oracle(ssj, gpu, oracle, shape):
+    """Whole-join AllPairs chunks of the bench shapes through every output path: the host
+    call (C uploaded in segments, runs clipped at segment boundaries), the device call and
+    results mode -- flags, counts and overlaps identical to the C oracle."""
+    coll = ssj.synth_collection(99, ssj.SynthConfig(**shape))
+    pred = ssj.jaccard(4, 5) if shape["universe"] == 7200 else ssj.jaccard(3, 4)
+    chunk, _ = ssj.generate_candidates(coll, pred, ssj.Algorithm.AllPairs)
+    assert chunk.C.size > 0
+    ref = oracle.verify_chunk(coll.tokens, coll.offsets, chunk.C, chunk.C_O,
+                              oracle.pred(J, pred.threshold.num, pred.threshold.den),
+                              want_overlaps=True)
+    with engine(ssj, coll, pred, "A", 1) as eng:
+        out = eng.verify_chunk(chunk)
+        assert out.count == ref["count"]
+        assert np.array_equal(out.flags, ref["flags"])
+        slots, ovs = eng.verify_chunk_results(chunk)
+        want = np.nonzero(ref["flags"])[0]
+        assert np.array_equal(slots, want) and np.array_equal(ovs, ref["overlaps"][want])
