@@ -87,6 +87,14 @@ __device__ __forceinline__ bool verify_pair(const KParams& p, const uint32_t* r,
     return merge_thread<kOut == kOutResults>(r, m, s4, n, (uint32_t)req, w0, w1, ov);
 }
 
+// 8 consecutive tokens (32 bytes, 32-byte aligned) in one 256-bit load.
+__device__ __forceinline__ void ld_tokens8(const uint32_t* __restrict__ s, uint32_t t[8]) {
+    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]),
+                   "=r"(t[6]), "=r"(t[7])
+                 : "l"(s));
+}
+
 // A pair longer than kLongPair tokens is left to long_slice_kernel: the first pass marks its
 // slice once per chunk segment (tag = segment index + 1 in the slice descriptor's spare word)
 // and lists it; long_slice_kernel re-derives the slice's long pairs from C.
@@ -273,7 +281,7 @@ __device__ __forceinline__ bool verify_bitmap(const uint32_t* __restrict__ bits,
 // 5-step shuffle binary search over those ends. Slice descriptors, probe bitmaps and probe
 // tokens are read through L1 (lanes of a tile share them). Long candidates are deferred to
 // long_kernel exactly as in tile_kernel.
-template <int kOut, bool kStats>
+template <int kOut, bool kStats, bool kPacked>
 __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile, unsigned& count,
                                           unsigned& prunes, unsigned& verified) {
     constexpr int kItems = SSJB_TILE_ITEMS;
@@ -299,9 +307,23 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
         for (int q = 0; q < kItems; ++q) cand[q] = my0 + q < slot1 ? __ldg(p.C + my0 + q) : 0u;
     }
     uint2 sd[kItems];
+    uint32_t hr[kPacked ? kItems : 1][8];  // kPacked: the candidates' head records
+    if (kPacked) {
+        // one 256-bit load per candidate: first 8 tokens, CSR position and |s|
 #pragma unroll
-    for (int q = 0; q < kItems; ++q)
-        sd[q] = cand[q] < p.n_sets ? __ldg(p.sets + cand[q]) : make_uint2(0, 0);
+        for (int q = 0; q < kItems; ++q) {
+            if (cand[q] < p.n_sets) {
+                ld_tokens8(reinterpret_cast<const uint32_t*>(p.heads + 2 * (size_t)cand[q]), hr[q]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) hr[q][u] = 0;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < kItems; ++q)
+            sd[q] = cand[q] < p.n_sets ? __ldg(p.sets + cand[q]) : make_uint2(0, 0);
+    }
 
     const uint32_t e0 = __ldg(p.tile_first + tile);
     uint32_t ns = 0;
@@ -315,7 +337,7 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
     const uint32_t beg0 = (e0 && e0 < p.n_slices) ? __ldg(p.C_O + 2 * (size_t)e0 - 1) : 0u;
 
     uint4 nw0, nw1;
-    {
+    if (!kPacked) {
         const uint4* s4 = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[0].x * 8);
         nw0 = __ldg(s4);
         nw1 = __ldg(s4 + 1);
@@ -325,11 +347,22 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
 #pragma unroll
     for (int q = 0; q < kItems; ++q) {
         const uint64_t slot = my0 + q;
-        const uint4 cw0 = nw0, cw1 = nw1;
-        if (q + 1 < kItems) {
-            const uint4* s4n = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[q + 1].x * 8);
-            nw0 = __ldg(s4n);
-            nw1 = __ldg(s4n + 1);
+        uint4 cw0, cw1;
+        if (kPacked) {
+            sd[q].x = __byte_perm(__byte_perm(hr[q][0], hr[q][1], 0x0073), __byte_perm(hr[q][2], hr[q][3], 0x0073), 0x5410);
+            sd[q].y = __byte_perm(__byte_perm(hr[q][4], hr[q][5], 0x0073), __byte_perm(hr[q][6], hr[q][7], 0x0073), 0x5410);
+            cw0 = make_uint4(hr[q][0] & kHeadTokenMask, hr[q][1] & kHeadTokenMask,
+                             hr[q][2] & kHeadTokenMask, hr[q][3] & kHeadTokenMask);
+            cw1 = make_uint4(hr[q][4] & kHeadTokenMask, hr[q][5] & kHeadTokenMask,
+                             hr[q][6] & kHeadTokenMask, hr[q][7] & kHeadTokenMask);
+        } else {
+            cw0 = nw0;
+            cw1 = nw1;
+            if (q + 1 < kItems) {
+                const uint4* s4n = reinterpret_cast<const uint4*>(p.tokens + (size_t)sd[q + 1].x * 8);
+                nw0 = __ldg(s4n);
+                nw1 = __ldg(s4n + 1);
+            }
         }
         // slice of this slot: number of the tile's slice ends <= slot (all lanes shuffle)
         uint32_t li = 0;
@@ -437,14 +470,14 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
 // tokens are read through L1 (lanes of a tile share them). Long candidates are deferred to
 // long_kernel. Persistent over the segment's short-tile list; slots of slices with
 // >= kRunMinSlice candidates are left to run_kernel.
-template <int kOut, bool kStats>
+template <int kOut, bool kStats, bool kPacked>
 __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) warp_tile_kernel(const KParams p) {
     const uint64_t n = min((uint64_t)*p.short_n, p.short_cap);
     const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     unsigned count = 0, prunes = 0, verified = 0;
     for (uint64_t w = gw; w < n; w += n_warps)
-        warp_tile<kOut, kStats>(p, __ldg(p.short_tiles + w), count, prunes, verified);
+        warp_tile<kOut, kStats, kPacked>(p, __ldg(p.short_tiles + w), count, prunes, verified);
     acc_add(p.acc, 0, count);
     if (kStats) {
         acc_add(p.acc, 2, verified);
@@ -515,13 +548,6 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// 8 consecutive tokens (32 bytes, 32-byte aligned) in one 256-bit load.
-__device__ __forceinline__ void ld_tokens8(const uint32_t* __restrict__ s, uint32_t t[8]) {
-    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]),
-                   "=r"(t[6]), "=r"(t[7])
-                 : "l"(s));
-}
 
 // Per-run uniform state (every thread holds the same values).
 struct RunState {
@@ -1150,6 +1176,9 @@ __global__ void path_kernel(const KParams p, const uint32_t rcap) {
 #define SSJB_LONG_THREADS 512
 #endif
 constexpr uint32_t kLongThreads = SSJB_LONG_THREADS;
+#ifndef SSJB_LONG_FIRST
+#define SSJB_LONG_FIRST 128  // tokens of a long pair's first step (32 or 32 * kLongPerLane)
+#endif
 #ifndef SSJB_LONG_PER_LANE
 #define SSJB_LONG_PER_LANE 4
 #endif
@@ -1251,21 +1280,23 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                     // lane `lane`, coalesced), the next step's in flight; tokens past |s| read
                     // as 0xFFFFFFFF and clamp onto the bitmap's zero word; per-lane counts are
                     // summed with one warp reduction
-                    constexpr uint32_t U = kLongPerLane, STEP = 32 * U;
+                    // the first step covers SSJB_LONG_FIRST tokens, the following ones
+                    // 32 * kLongPerLane
+                    constexpr uint32_t U = kLongPerLane;
                     const uint32_t slack_r = m - sreq, slack_s = sn - sreq;
-                    uint32_t j = 0;
+                    uint32_t j = 0, width = SSJB_LONG_FIRST;
                     bool decided = false;
                     met = false;
                     uint32_t a[U];
 #pragma unroll
                     for (uint32_t u = 0; u < U; ++u)
-                        a[u] = u * 32 + lane < sn ? __ldg(s + u * 32 + lane) : 0xFFFFFFFFu;
+                        a[u] = u * 32 < width && u * 32 + lane < sn ? __ldg(s + u * 32 + lane) : 0xFFFFFFFFu;
                     for (;;) {
+                        const uint32_t jn = j + width;  // next step: [jn, jn + 32 * U)
                         uint32_t nx[U];
 #pragma unroll
                         for (uint32_t u = 0; u < U; ++u)
-                            nx[u] = j + STEP + u * 32 + lane < sn ? __ldg(s + j + STEP + u * 32 + lane)
-                                                                  : 0xFFFFFFFFu;
+                            nx[u] = jn + u * 32 + lane < sn ? __ldg(s + jn + u * 32 + lane) : 0xFFFFFFFFu;
                         uint32_t c = 0;
 #pragma unroll
                         for (uint32_t u = 0; u < U; ++u) {
@@ -1273,7 +1304,7 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                             c += (lds_u32(bits_s + ((e >> 5) << 2)) >> (e & 31)) & 1u;
                         }
                         ov += __reduce_add_sync(0xffffffffu, c);
-                        j += STEP;
+                        j = jn;
                         if (j >= sn) break;
                         if (kOut != kOutResults && ov >= sreq) {
                             met = true;
@@ -1281,7 +1312,7 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                             break;
                         }
                         if (ov < sreq) {
-                            const uint32_t tl = __shfl_sync(0xffffffffu, a[U - 1], 31);
+                            const uint32_t tl = __shfl_sync(0xffffffffu, width == 32 * U ? a[U - 1] : a[0], 31);
                             const uint32_t dl = tl - lo;
                             uint32_t i;
                             if (tl < lo) i = 0;
@@ -1295,6 +1326,7 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                         }
 #pragma unroll
                         for (uint32_t u = 0; u < U; ++u) a[u] = nx[u];
+                        width = 32 * U;
                     }
                     if (!decided) met = ov >= sreq;
                     if (!met) ov = 0;
@@ -1485,7 +1517,10 @@ cudaError_t launch_tiles_t(const KParams& p, uint32_t tile_begin, uint32_t tile_
         attr[p.heads ? 1 : 0] = true;
     }
     rk<<<sms * kRunMinBlocks, kRunThreads, kRunSmemBytes, st>>>(p);
-    warp_tile_kernel<kOut, kStats><<<sms * kTileMinBlocks, kThreadsA, 0, st>>>(p);
+    if (p.heads)
+        warp_tile_kernel<kOut, kStats, true><<<sms * kTileMinBlocks, kThreadsA, 0, st>>>(p);
+    else
+        warp_tile_kernel<kOut, kStats, false><<<sms * kTileMinBlocks, kThreadsA, 0, st>>>(p);
     return cudaGetLastError();
 }
 
