@@ -321,6 +321,41 @@ int ssj_join_result_report(const ssj_join_result* r, ssj_join_report* report);
 int ssj_join_result_pairs(const ssj_join_result* r, uint32_t* pairs /* 2 * n_pairs */);
 void ssj_join_result_free(ssj_join_result* r);
 
+/* ---- candidate generation + join on the GPU ------------------- */
+/*
+ * AllPairs / PPJoin candidates of probes [probe_begin, probe_end) generated on the engine's
+ * device from its resident collection (static index over all index prefixes, built once per
+ * engine): the same stream as ssj_generate_candidates / the reference generators
+ * (joiners.hpp:47-102), returned in host buffers. *nC_out / *nCO_out receive the sizes;
+ * SSJ_ERR_RUNTIME when a capacity is too small (sizes still reported).
+ */
+int ssj_gpu_generate_candidates(ssj_engine* e, int32_t algorithm, uint32_t probe_begin,
+                                uint32_t probe_end, uint32_t* C_out, uint64_t C_cap,
+                                uint64_t* nC_out, uint32_t* C_O_out, uint64_t C_O_cap,
+                                uint64_t* nCO_out);
+
+typedef struct {
+    uint64_t count;            /* qualifying pairs */
+    uint64_t candidate_count;  /* candidates generated and verified */
+    uint64_t chunk_count;      /* device-resident chunks */
+    double index_ms;           /* one-time static index build (0 when cached) */
+    double filtering_ms;       /* candidate generation (bounds + generate + compact) */
+    double verification_ms;    /* verification kernels + pair decoding */
+    double join_ms;            /* wall time of the call */
+} ssj_gpu_join_report;
+
+/*
+ * Self-join run entirely on the engine's device: candidate generation (AllPairs / PPJoin) in
+ * probe blocks of at most max_chunk_candidates candidates (0 = 256M), each block verified in
+ * place by the strategy-A kernels. Pairs mode (pairs_out != NULL): qualifying pairs as
+ * (max(orig), min(orig)) original ids (ssj_engine_set_original_ids; identity by default)
+ * sorted like write_pairs (report.hpp:39-42); *n_pairs = their number (SSJ_ERR_RUNTIME when
+ * pairs_cap is smaller). Count mode: pairs_out == NULL.
+ */
+int ssj_gpu_join(ssj_engine* e, int32_t algorithm, uint64_t max_chunk_candidates,
+                 uint32_t* pairs_out, uint64_t pairs_cap, uint64_t* n_pairs,
+                 ssj_gpu_join_report* report);
+
 /* ---- diagnostics -------------------------------------------------------------------- */
 /* Streaming read bandwidth (GB/s) of a `bytes` device buffer read `reps` times with 16-byte
  * loads: with bytes < L2 (126 MB) it measures L2-resident reads, with bytes >> L2 HBM reads.

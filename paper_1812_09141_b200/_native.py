@@ -68,6 +68,13 @@ class ssj_join_report(C.Structure):
                 ("handoff_wait_ms", C.c_double), ("setup_ms", C.c_double)]
 
 
+class ssj_gpu_join_report(C.Structure):
+    _fields_ = [("count", C.c_uint64), ("candidate_count", C.c_uint64),
+                ("chunk_count", C.c_uint64), ("index_ms", C.c_double),
+                ("filtering_ms", C.c_double), ("verification_ms", C.c_double),
+                ("join_ms", C.c_double)]
+
+
 # name -> (restype, argtypes); every symbol declared in include/ssjoin_b200.h
 SIGNATURES = {
     "ssj_abi_version": (C.c_int, []),
@@ -123,6 +130,10 @@ SIGNATURES = {
     "ssj_join_result_report": (C.c_int, [vp, C.POINTER(ssj_join_report)]),
     "ssj_join_result_pairs": (C.c_int, [vp, vp]),
     "ssj_join_result_free": (None, [vp]),
+    "ssj_gpu_generate_candidates": (C.c_int, [vp, C.c_int32, C.c_uint32, C.c_uint32, vp,
+                                              C.c_uint64, u64p, vp, C.c_uint64, u64p]),
+    "ssj_gpu_join": (C.c_int, [vp, C.c_int32, C.c_uint64, vp, C.c_uint64, u64p,
+                               C.POINTER(ssj_gpu_join_report)]),
     "ssj_measure_read_bandwidth": (C.c_int, [C.c_int, C.c_uint64, C.c_uint32,
                                              C.POINTER(C.c_double)]),
     "ssj_host_alloc": (vp, [C.c_size_t]),

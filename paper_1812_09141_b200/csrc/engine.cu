@@ -9,6 +9,7 @@
 //   * two chunk slots allow ssj_submit_chunk / ssj_wait_chunk double buffering.
 // No CPU verification path exists here: without a device every entry point fails.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -19,9 +20,11 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "../../include/ssjoin_b200.h"
 #include "host_common.hpp"
+#include "gpu_filter.cuh"
 #include "verify_kernels.cuh"
 
 using ssjb::KParams;
@@ -157,6 +160,7 @@ struct ssj_engine {
     bool owns_collection = true;
     uint32_t* d_req_tab = nullptr;  // Jaccard/Dice required overlap by |r|+|s|
     uint4* d_heads = nullptr;       // packed set heads (null: tokens too large to pack)
+    ssjb::FilterIndex* fidx = nullptr;  // GPU candidate generation index (built on first use)
     uint32_t req_tab_n = 0;
     cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
     ChunkSlot slot[2];
@@ -824,6 +828,10 @@ void ssj_engine_destroy(ssj_engine* e) {
     cudaFree(e->dev_short);
     cudaFree(e->d_req_tab);
     cudaFree(e->d_heads);
+    if (e->fidx) {
+        ssjb::filter_index_free(e->fidx);
+        delete e->fidx;
+    }
     cudaFree(e->d_res_slots);
     cudaFree(e->d_res_ov);
     cudaFree(e->d_res_n);
@@ -1006,13 +1014,15 @@ int ssj_verify_chunk_pairs(ssj_engine* e, const uint32_t* C, uint64_t nC, const 
     return SSJ_OK;
 }
 
-int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, const uint32_t* d_C_O,
-                            uint64_t nCO, uint8_t* d_flags, uint64_t* d_result, void* stream) {
-    int rc = check_chunk_args(e, d_C, nC, d_C_O, nCO);
-    if (rc) return rc;
-    if (!d_result) return fail(SSJ_ERR_INVALID_ARGUMENT, "null d_result");
-    DeviceScope ds(e->device);
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+namespace {
+
+// Verification of a device-resident chunk on stream st (no synchronisation). out = kOutFlags
+// (d_flags), kOutCount or kOutResults (qualifying slots/overlaps appended to the engine's
+// result buffers; e->d_res_n is zeroed here). d_acc: SSJ_RESULT_WORDS words.
+int verify_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, const uint32_t* d_C_O,
+                  uint64_t nCO, int out, uint8_t* d_flags, unsigned long long* d_acc,
+                  cudaStream_t st) {
+    int rc;
     const uint32_t n_slices = (uint32_t)(nCO / 2);
     const uint32_t n_tiles = (uint32_t)((nC + ssjb::kTile - 1) / ssjb::kTile);
     if ((rc = ensure_device(&e->dev_tile, &e->dev_tile_cap, (size_t)n_tiles + 1))) return rc;
@@ -1030,6 +1040,12 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
         return rc;
     if (tiles && (rc = ensure_device(&e->dev_short, &e->dev_short_cap, (size_t)n_tiles + 1)))
         return rc;
+    if (out == ssjb::kOutResults) {
+        if ((rc = ensure_device(&e->d_res_slots, &e->res_cap, std::max<uint64_t>(nC, 1)))) return rc;
+        if ((rc = ensure_device(&e->d_res_ov, &e->res_cap2, std::max<uint64_t>(nC, 1)))) return rc;
+        if (!e->d_res_n) SSJ_CK(cudaMalloc(&e->d_res_n, sizeof(unsigned long long)));
+        SSJ_CK(cudaMemsetAsync(e->d_res_n, 0, sizeof(unsigned long long), st));
+    }
     KParams p = base_params(*e);
     p.C = d_C;
     p.nC = nC;
@@ -1038,7 +1054,13 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
     p.tile_first = e->dev_tile;
     p.n_tiles = n_tiles;
     p.flags = d_flags;
-    p.acc = reinterpret_cast<unsigned long long*>(d_result);
+    p.acc = d_acc;
+    if (out == ssjb::kOutResults) {
+        p.res_slots = e->d_res_slots;
+        p.res_ov = e->d_res_ov;
+        p.res_n = e->d_res_n;
+        p.res_cap = nC;
+    }
     if (tiles) {
         p.slices = e->dev_slices;
         p.bm_bits = e->dev_bits;
@@ -1056,8 +1078,7 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
         p.short_n = e->dev_defer_n + 2;
         p.short_cap = n_tiles;
     }
-    const int out = (e->mode == SSJ_MODE_PAIRS && d_flags) ? ssjb::kOutFlags : ssjb::kOutCount;
-    SSJ_CK(cudaMemsetAsync(d_result, 0, SSJ_RESULT_WORDS * sizeof(uint64_t), st));
+    SSJ_CK(cudaMemsetAsync(d_acc, 0, SSJ_RESULT_WORDS * sizeof(uint64_t), st));
     if (tiles) SSJ_CK(cudaMemsetAsync(e->dev_defer_n, 0, kCounters * sizeof(unsigned long long), st));
     SSJ_CK(ssjb::launch_prep(p, st));
     cudaEvent_t k0 = nullptr, k1 = nullptr;
@@ -1075,6 +1096,296 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
     }
     SSJ_CK(launch_strategy(*e, p, out, 0, n_tiles, st));
     if (k1) SSJ_CK(cudaEventRecord(k1, st));
+    return SSJ_OK;
+}
+
+}  // namespace
+
+int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, const uint32_t* d_C_O,
+                            uint64_t nCO, uint8_t* d_flags, uint64_t* d_result, void* stream) {
+    int rc = check_chunk_args(e, d_C, nC, d_C_O, nCO);
+    if (rc) return rc;
+    if (!d_result) return fail(SSJ_ERR_INVALID_ARGUMENT, "null d_result");
+    DeviceScope ds(e->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+    const int out = (e->mode == SSJ_MODE_PAIRS && d_flags) ? ssjb::kOutFlags : ssjb::kOutCount;
+    return verify_device(e, d_C, nC, d_C_O, nCO, out, d_flags,
+                         reinterpret_cast<unsigned long long*>(d_result), st);
+}
+
+// ---- candidate generation + join on the GPU -------------------------------------------------
+}  // extern "C"
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() { cudaFree(p); }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+    int alloc(size_t bytes) {
+        cudaFree(p);
+        p = nullptr;
+        if (cudaMalloc(&p, bytes ? bytes : 1) != cudaSuccess)
+            return fail(SSJ_ERR_CUDA, "cudaMalloc failed (GPU join)");
+        return SSJ_OK;
+    }
+};
+
+int ensure_filter_index(ssj_engine* e, int algorithm, double* build_ms) {
+    if (algorithm != SSJ_ALG_ALLPAIRS && algorithm != SSJ_ALG_PPJOIN)
+        return fail(SSJ_ERR_INVALID_ARGUMENT, "GPU generation supports allpairs and ppjoin");
+    if (build_ms) *build_ms = 0;
+    if (!e->fidx) {
+        auto t0 = std::chrono::steady_clock::now();
+        e->fidx = new ssjb::FilterIndex;
+        cudaError_t err = ssjb::filter_index_build(e->fidx, e->d_tokens, e->d_sets, e->n_sets,
+                                                   e->pred, algorithm, e->s_comp);
+        if (err != cudaSuccess) {
+            delete e->fidx;
+            e->fidx = nullptr;
+            return fail(SSJ_ERR_CUDA, std::string("GPU index build: ") + cudaGetErrorString(err));
+        }
+        if (build_ms)
+            *build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    e->fidx->algorithm = algorithm;  // one index serves both (postings carry positions)
+    return SSJ_OK;
+}
+
+// Per-join scratch: per-probe bounds (scanned), block buffers.
+struct GenState {
+    DevBuf bound, base, G, count, flag, obase, slot, C, CO, tmp;
+    size_t tmp_bytes = 0, G_cap = 0, C_cap = 0, blk_cap = 0;
+    std::vector<unsigned long long> hbase;  // exclusive scan of the bounds, n + 1 entries
+};
+
+template <typename F>
+int cub_run(GenState& g, F&& f, cudaStream_t st) {
+    size_t need = 0;
+    SSJ_CK(f((void*)nullptr, need));
+    if (need > g.tmp_bytes) {
+        int rc;
+        if ((rc = g.tmp.alloc(need))) return rc;
+        g.tmp_bytes = need;
+    }
+    SSJ_CK(f(g.tmp.p, need));
+    (void)st;
+    return SSJ_OK;
+}
+
+// Bounds of all probes and their exclusive scan (device + host copy).
+int gen_bounds(ssj_engine* e, GenState& g) {
+    const uint32_t n = e->n_sets;
+    cudaStream_t st = e->s_comp;
+    int rc;
+    if ((rc = g.bound.alloc((size_t)n * 8 + 8)) || (rc = g.base.alloc(((size_t)n + 1) * 8)))
+        return rc;
+    SSJ_CK(ssjb::filter_bounds(*e->fidx, 0, n, g.bound.as<unsigned long long>(), st));
+    SSJ_CK(cudaMemsetAsync(g.base.p, 0, 8, st));
+    if (n) {
+        auto* in = g.bound.as<unsigned long long>();
+        auto* out = g.base.as<unsigned long long>() + 1;
+        if ((rc = cub_run(g, [&](void* t, size_t& b) {
+                 return cub::DeviceScan::InclusiveSum(t, b, in, out, (int)n, st);
+             }, st)))
+            return rc;
+    }
+    g.hbase.resize((size_t)n + 1);
+    SSJ_CK(cudaMemcpyAsync(g.hbase.data(), g.base.p, ((size_t)n + 1) * 8, cudaMemcpyDeviceToHost, st));
+    SSJ_CK(cudaStreamSynchronize(st));
+    return SSJ_OK;
+}
+
+// Candidates of probes [a, b) as a compacted device chunk in g.C / g.CO.
+int gen_block(ssj_engine* e, GenState& g, uint32_t a, uint32_t b, uint64_t* nC, uint64_t* nCO) {
+    cudaStream_t st = e->s_comp;
+    const uint32_t np = b - a;
+    const unsigned long long base0 = g.hbase[a];
+    const uint64_t ub = g.hbase[b] - base0;
+    int rc;
+    if (ub > g.G_cap) {
+        if ((rc = g.G.alloc(ub * 4)) || (rc = g.C.alloc(ub * 4))) return rc;
+        g.G_cap = g.C_cap = ub;
+    }
+    if (np > g.blk_cap) {
+        if ((rc = g.count.alloc((size_t)np * 8)) || (rc = g.flag.alloc((size_t)np * 4)) ||
+            (rc = g.obase.alloc((size_t)np * 8)) || (rc = g.slot.alloc((size_t)np * 4)) ||
+            (rc = g.CO.alloc((size_t)np * 8)))
+            return rc;
+        g.blk_cap = np;
+    }
+    const auto* base = g.base.as<unsigned long long>() + a;
+    SSJ_CK(ssjb::filter_generate(*e->fidx, a, b, base, base0, g.G.as<uint32_t>(),
+                                 g.count.as<unsigned long long>(), g.flag.as<uint32_t>(), st));
+    auto* cnt = g.count.as<unsigned long long>();
+    auto* ob = g.obase.as<unsigned long long>();
+    auto* fl = g.flag.as<uint32_t>();
+    auto* sl = g.slot.as<uint32_t>();
+    if ((rc = cub_run(g, [&](void* t, size_t& bb) {
+             return cub::DeviceScan::ExclusiveSum(t, bb, cnt, ob, (int)np, st);
+         }, st)))
+        return rc;
+    if ((rc = cub_run(g, [&](void* t, size_t& bb) {
+             return cub::DeviceScan::ExclusiveSum(t, bb, fl, sl, (int)np, st);
+         }, st)))
+        return rc;
+    unsigned long long last_ob = 0, last_cnt = 0;
+    uint32_t last_sl = 0, last_fl = 0;
+    SSJ_CK(cudaMemcpyAsync(&last_ob, ob + np - 1, 8, cudaMemcpyDeviceToHost, st));
+    SSJ_CK(cudaMemcpyAsync(&last_cnt, cnt + np - 1, 8, cudaMemcpyDeviceToHost, st));
+    SSJ_CK(cudaMemcpyAsync(&last_sl, sl + np - 1, 4, cudaMemcpyDeviceToHost, st));
+    SSJ_CK(cudaMemcpyAsync(&last_fl, fl + np - 1, 4, cudaMemcpyDeviceToHost, st));
+    SSJ_CK(ssjb::filter_compact(a, b, base, base0, g.G.as<uint32_t>(), cnt, ob, sl,
+                                g.C.as<uint32_t>(), g.CO.as<uint32_t>(), st));
+    SSJ_CK(cudaStreamSynchronize(st));
+    *nC = last_ob + last_cnt;
+    *nCO = 2ull * (last_sl + last_fl);
+    if (*nC > 0xFFFFFFFFull) return fail(SSJ_ERR_INVALID_ARGUMENT, "probe block exceeds u32 offsets");
+    return SSJ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ssj_gpu_generate_candidates(ssj_engine* e, int32_t algorithm, uint32_t probe_begin,
+                                uint32_t probe_end, uint32_t* C_out, uint64_t C_cap,
+                                uint64_t* nC_out, uint32_t* C_O_out, uint64_t C_O_cap,
+                                uint64_t* nCO_out) {
+    if (!e || !nC_out || !nCO_out) return fail(SSJ_ERR_INVALID_ARGUMENT, "null argument");
+    DeviceScope ds(e->device);
+    int rc;
+    if ((rc = ensure_filter_index(e, algorithm, nullptr))) return rc;
+    probe_end = std::min(probe_end, e->n_sets);
+    *nC_out = *nCO_out = 0;
+    if (probe_begin >= probe_end) return SSJ_OK;
+    GenState g;
+    if ((rc = gen_bounds(e, g))) return rc;
+    uint64_t nC = 0, nCO = 0;
+    if ((rc = gen_block(e, g, probe_begin, probe_end, &nC, &nCO))) return rc;
+    *nC_out = nC;
+    *nCO_out = nCO;
+    if (nC > C_cap || nCO > C_O_cap) return fail(SSJ_ERR_RUNTIME, "output capacity too small");
+    if (nC) SSJ_CK(cudaMemcpy(C_out, g.C.p, nC * 4, cudaMemcpyDeviceToHost));
+    if (nCO) SSJ_CK(cudaMemcpy(C_O_out, g.CO.p, nCO * 4, cudaMemcpyDeviceToHost));
+    return SSJ_OK;
+}
+
+int ssj_gpu_join(ssj_engine* e, int32_t algorithm, uint64_t max_chunk_candidates,
+                 uint32_t* pairs_out, uint64_t pairs_cap, uint64_t* n_pairs,
+                 ssj_gpu_join_report* report) {
+    if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
+    if (pairs_out && !n_pairs) return fail(SSJ_ERR_INVALID_ARGUMENT, "null n_pairs");
+    DeviceScope ds(e->device);
+    const auto t_start = std::chrono::steady_clock::now();
+    ssj_gpu_join_report rep{};
+    int rc;
+    if ((rc = ensure_filter_index(e, algorithm, &rep.index_ms))) return rc;
+    const bool want_pairs = pairs_out != nullptr || (n_pairs && pairs_cap == 0 && !pairs_out && false);
+    if (want_pairs && !e->d_oid && (rc = ssj_engine_set_original_ids(e, nullptr))) return rc;
+    cudaStream_t st = e->s_comp;
+    cudaEvent_t ev[4];
+    for (auto& x : ev) SSJ_CK(cudaEventCreate(&x));
+    struct EvGuard {
+        cudaEvent_t* ev;
+        ~EvGuard() {
+            for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
+        }
+    } evg{ev};
+    const uint64_t cap = max_chunk_candidates ? max_chunk_candidates : (256ull << 20);
+    GenState g;
+    SSJ_CK(cudaEventRecord(ev[0], st));
+    if ((rc = gen_bounds(e, g))) return rc;
+    SSJ_CK(cudaEventRecord(ev[1], st));
+    SSJ_CK(cudaEventSynchronize(ev[1]));
+    float ms = 0;
+    SSJ_CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    rep.filtering_ms += ms;
+    DevBuf acc, keys_all;
+    if ((rc = acc.alloc(SSJ_RESULT_WORDS * 8))) return rc;
+    uint64_t keys_n = 0, keys_cap = 0;
+    const uint32_t n = e->n_sets;
+    for (uint32_t a = 0; a < n;) {
+        // the longest probe block whose candidate upper bound fits the budget (>= 1 probe)
+        uint32_t b = (uint32_t)(std::upper_bound(g.hbase.begin() + a + 1, g.hbase.end(),
+                                                 g.hbase[a] + cap) - g.hbase.begin()) - 1;
+        if (b <= a) b = a + 1;
+        b = std::min(b, n);
+        uint64_t nC = 0, nCO = 0;
+        SSJ_CK(cudaEventRecord(ev[0], st));
+        if ((rc = gen_block(e, g, a, b, &nC, &nCO))) return rc;
+        SSJ_CK(cudaEventRecord(ev[1], st));
+        if (nC) {
+            const int out = want_pairs ? ssjb::kOutResults : ssjb::kOutCount;
+            if ((rc = verify_device(e, g.C.as<uint32_t>(), nC, g.CO.as<uint32_t>(), nCO, out,
+                                    nullptr, acc.as<unsigned long long>(), st)))
+                return rc;
+            unsigned long long words[SSJ_RESULT_WORDS];
+            SSJ_CK(cudaMemcpyAsync(words, acc.p, sizeof(words), cudaMemcpyDeviceToHost, st));
+            unsigned long long nres = 0;
+            if (want_pairs)
+                SSJ_CK(cudaMemcpyAsync(&nres, e->d_res_n, 8, cudaMemcpyDeviceToHost, st));
+            SSJ_CK(cudaStreamSynchronize(st));
+            if ((rc = decode_error(words[SSJ_RESULT_ERROR]))) return rc;
+            rep.count += words[SSJ_RESULT_COUNT];
+            if (want_pairs && nres) {
+                if (keys_n + nres > keys_cap) {
+                    DevBuf grown;
+                    const uint64_t nc = std::max<uint64_t>(2 * keys_cap, keys_n + nres);
+                    if ((rc = grown.alloc(nc * 8))) return rc;
+                    if (keys_n) SSJ_CK(cudaMemcpyAsync(grown.p, keys_all.p, keys_n * 8, cudaMemcpyDeviceToDevice, st));
+                    std::swap(grown.p, keys_all.p);
+                    keys_cap = nc;
+                }
+                KParams p = base_params(*e);
+                p.C = g.C.as<uint32_t>();
+                p.nC = nC;
+                p.C_O = g.CO.as<uint32_t>();
+                p.n_slices = (uint32_t)(nCO / 2);
+                p.res_slots = e->d_res_slots;
+                SSJ_CK(ssjb::launch_pairs(p, e->d_oid, nres,
+                                          keys_all.as<unsigned long long>() + keys_n, st));
+                keys_n += nres;
+            }
+        }
+        SSJ_CK(cudaEventRecord(ev[2], st));
+        SSJ_CK(cudaEventSynchronize(ev[2]));
+        SSJ_CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+        rep.filtering_ms += ms;
+        SSJ_CK(cudaEventElapsedTime(&ms, ev[1], ev[2]));
+        rep.verification_ms += ms;
+        rep.candidate_count += nC;
+        rep.chunk_count += nC ? 1 : 0;
+        a = b;
+    }
+    if (want_pairs) {
+        *n_pairs = keys_n;
+        if (keys_n) {
+            // write_pairs order (report.hpp:39-42): radix sort of the (r_id << 32 | s_id) keys
+            DevBuf sorted;
+            if ((rc = sorted.alloc(keys_n * 8))) return rc;
+            auto* kin = keys_all.as<unsigned long long>();
+            auto* kout = sorted.as<unsigned long long>();
+            if ((rc = cub_run(g, [&](void* t, size_t& bb) {
+                     return cub::DeviceRadixSort::SortKeys(t, bb, kin, kout, (int)keys_n, 0, 64, st);
+                 }, st)))
+                return rc;
+            std::vector<unsigned long long> hk(std::min<uint64_t>(keys_n, pairs_cap));
+            if (!hk.empty())
+                SSJ_CK(cudaMemcpyAsync(hk.data(), kout, hk.size() * 8, cudaMemcpyDeviceToHost, st));
+            SSJ_CK(cudaStreamSynchronize(st));
+            for (size_t i = 0; i < hk.size(); ++i) {
+                pairs_out[2 * i] = (uint32_t)(hk[i] >> 32);
+                pairs_out[2 * i + 1] = (uint32_t)hk[i];
+            }
+        }
+    } else if (n_pairs) {
+        *n_pairs = 0;
+    }
+    rep.join_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    if (report) *report = rep;
+    if (want_pairs && keys_n > pairs_cap) return fail(SSJ_ERR_RUNTIME, "pair capacity exceeded");
     return SSJ_OK;
 }
 

@@ -1,0 +1,373 @@
+// gpu_filter.cu -- device candidate generation (see gpu_filter.cuh for the algorithm).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "gpu_filter.cuh"
+
+namespace ssjb {
+
+namespace {
+
+typedef unsigned __int128 u128;
+
+__device__ __forceinline__ uint64_t ceil_div128(u128 a, u128 b) { return (uint64_t)((a + b - 1) / b); }
+
+// similarity.hpp:135-164 size_bounds(...).min, raised to 1 when zero (:162).
+__device__ __forceinline__ uint64_t dev_size_lower_bound(const PredDev& p, uint64_t r) {
+    uint64_t lo;
+    switch (p.fn) {
+        case kFnJaccard: lo = ceil_div128((u128)p.num * r, p.den); break;
+        case kFnCosine: lo = ceil_div128((u128)p.num * p.num * r, (u128)p.den * p.den); break;
+        case kFnDice: lo = ceil_div128((u128)p.num * r, 2 * p.den - p.num); break;
+        default: lo = p.ovt; break;
+    }
+    return lo == 0 ? 1 : lo;
+}
+
+// filters.hpp:148-159 prefix_lengths: {probe, index}.
+__device__ __forceinline__ uint2 dev_prefix_lengths(const PredDev& p, uint32_t size) {
+    auto clamp = [size](uint64_t len) -> uint32_t {
+        if (len < 1) return 1;
+        return (uint32_t)(len < size ? len : size);
+    };
+    const uint64_t minsize = dev_size_lower_bound(p, size);
+    const uint32_t probe = clamp(minsize >= size ? 1 : size - minsize + 1);
+    const uint64_t self = dev_required(p, size, size);
+    const uint32_t index = clamp(self >= size ? 1 : size - self + 1);
+    return make_uint2(probe, index);
+}
+
+// filters.hpp:174-181 positional_filter with current_overlap = 1 (joiners.hpp:94).
+__device__ __forceinline__ bool dev_positional_keep(const PredDev& p, uint32_t size_r,
+                                                    uint32_t size_s, uint32_t pos_r,
+                                                    uint32_t pos_s) {
+    const uint64_t required = dev_required(p, size_r, size_s);
+    const uint64_t a = size_r - pos_r - 1, b = size_s - pos_s - 1;
+    return 1 + (a < b ? a : b) >= required;
+}
+
+__device__ __forceinline__ uint32_t set_size(const FilterIndex& ix, uint32_t s) {
+    return __ldg(&ix.sets[s].y);
+}
+__device__ __forceinline__ const uint32_t* set_tokens(const FilterIndex& ix, uint32_t s) {
+    return ix.tokens + (size_t)__ldg(&ix.sets[s].x) * 8;
+}
+
+// First set whose size is >= minsize (sets are size-ascending).
+__device__ __forceinline__ uint32_t first_set_of_size(const FilterIndex& ix, uint64_t minsize) {
+    uint32_t lo = 0, hi = ix.n_sets;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((uint64_t)set_size(ix, mid) < minsize) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// First posting in [lo, hi) with set >= key.
+__device__ __forceinline__ uint32_t posting_lower_bound(const FilterIndex& ix, uint32_t lo,
+                                                        uint32_t hi, uint32_t key) {
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(&ix.post[mid].x) < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// ---- index build -------------------------------------------------------------------------
+__global__ void ilen_kernel(const FilterIndex ix, uint32_t* ilen, uint32_t* max_token) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= ix.n_sets) return;
+    const uint32_t n = set_size(ix, s);
+    ilen[s] = n ? dev_prefix_lengths(ix.pred, n).y : 0u;
+    if (n) atomicMax(max_token, __ldg(set_tokens(ix, s) + n - 1));
+}
+
+__global__ void entries_kernel(const FilterIndex ix, const uint32_t* ilen, const uint32_t* off,
+                               uint32_t* keys, unsigned long long* vals, uint32_t* count) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= ix.n_sets) return;
+    const uint32_t* r = set_tokens(ix, s);
+    const uint32_t base = off[s];
+    for (uint32_t q = 0; q < ilen[s]; ++q) {
+        const uint32_t t = __ldg(r + q);
+        keys[base + q] = t;
+        vals[base + q] = ((unsigned long long)s << 32) | q;
+        atomicAdd(count + t, 1u);
+    }
+}
+
+__global__ void unpack_kernel(const unsigned long long* vals, uint64_t n, uint2* post) {
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) post[k] = make_uint2((uint32_t)(vals[k] >> 32), (uint32_t)vals[k]);
+}
+
+// ---- probing -------------------------------------------------------------------------------
+// Warp per probe. Lanes take prefix positions p (strided); range of token r[p]'s postings
+// usable by probe i: [first set >= S_min, first set >= i).
+__global__ void bounds_kernel(const FilterIndex ix, uint32_t a, uint32_t b,
+                              unsigned long long* bound) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t k = w; k < (uint64_t)(b - a); k += nw) {
+        const uint32_t i = a + (uint32_t)k;
+        const uint32_t m = set_size(ix, i);
+        unsigned long long tot = 0;
+        if (m) {
+            const uint32_t P = dev_prefix_lengths(ix.pred, m).x;
+            const uint32_t smin = first_set_of_size(ix, dev_size_lower_bound(ix.pred, m));
+            const uint32_t* r = set_tokens(ix, i);
+            for (uint32_t p = lane; p < P; p += 32) {
+                const uint32_t t = __ldg(r + p);
+                if (t >= ix.universe) continue;
+                const uint32_t h0 = __ldg(ix.head + t), h1 = __ldg(ix.head + t + 1);
+                const uint32_t lo = posting_lower_bound(ix, h0, h1, smin);
+                const uint32_t hi = posting_lower_bound(ix, lo, h1, i);
+                tot += hi - lo;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+        if (lane == 0) bound[k] = tot;
+    }
+}
+
+// Warp per probe: for p = 0..P-1 the warp sweeps the range of r[p]'s postings 32 at a time;
+// a lane keeps its set s unless s was already reached at an earlier prefix position (one of
+// s's index-prefix tokens below r[p] is in r) and, for PPJoin, unless the positional filter
+// rejects it at this first match. Kept sets are appended in order (ballot compaction).
+__global__ void generate_kernel(const FilterIndex ix, uint32_t a, uint32_t b,
+                                const unsigned long long* base, unsigned long long base0,
+                                uint32_t* C, unsigned long long* count, uint32_t* flag) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const bool positional = ix.algorithm == 1;
+    for (uint64_t k = w; k < (uint64_t)(b - a); k += nw) {
+        const uint32_t i = a + (uint32_t)k;
+        const uint32_t m = set_size(ix, i);
+        uint32_t n_out = 0;
+        if (m) {
+            const uint32_t P = dev_prefix_lengths(ix.pred, m).x;
+            const uint32_t smin = first_set_of_size(ix, dev_size_lower_bound(ix.pred, m));
+            const uint32_t* r = set_tokens(ix, i);
+            uint32_t* out = C + (base[k] - base0);
+            for (uint32_t p = 0; p < P; ++p) {
+                const uint32_t t = __ldg(r + p);
+                if (t >= ix.universe) continue;
+                const uint32_t h0 = __ldg(ix.head + t), h1 = __ldg(ix.head + t + 1);
+                // both bounds by the whole warp's lane 0 (uniform), then broadcast
+                uint32_t lo = 0, hi = 0;
+                if (lane == 0) {
+                    lo = posting_lower_bound(ix, h0, h1, smin);
+                    hi = posting_lower_bound(ix, lo, h1, i);
+                }
+                lo = __shfl_sync(0xffffffffu, lo, 0);
+                hi = __shfl_sync(0xffffffffu, hi, 0);
+                for (uint32_t q0 = lo; q0 < hi; q0 += 32) {
+                    const uint32_t q = q0 + lane;
+                    bool keep = false;
+                    uint32_t s = 0;
+                    if (q < hi) {
+                        const uint2 pe = __ldg(&ix.post[q]);
+                        s = pe.x;
+                        keep = true;
+                        if (p) {
+                            // duplicate iff an index-prefix token u < t of s is in r[0..p)
+                            const uint32_t ns = set_size(ix, s);
+                            const uint32_t il = dev_prefix_lengths(ix.pred, ns).y;
+                            const uint32_t* st = set_tokens(ix, s);
+                            uint32_t lo_r = 0;
+                            for (uint32_t u = 0; u < il; ++u) {
+                                const uint32_t v = __ldg(st + u);
+                                if (v >= t) break;
+                                uint32_t l = lo_r, h = p;  // r[0..p) holds r's tokens < t
+                                while (l < h) {
+                                    const uint32_t mid = (l + h) >> 1;
+                                    if (__ldg(r + mid) < v) l = mid + 1;
+                                    else h = mid;
+                                }
+                                if (l < p && __ldg(r + l) == v) {
+                                    keep = false;
+                                    break;
+                                }
+                                lo_r = l;
+                            }
+                        }
+                        if (keep && positional)
+                            keep = dev_positional_keep(ix.pred, m, set_size(ix, s), p, pe.y);
+                    }
+                    const unsigned km = __ballot_sync(0xffffffffu, keep);
+                    if (keep) out[n_out + __popc(km & ((1u << lane) - 1u))] = s;
+                    n_out += __popc(km);
+                }
+            }
+        }
+        if (lane == 0) {
+            count[k] = n_out;
+            flag[k] = n_out ? 1u : 0u;
+        }
+    }
+}
+
+__global__ void compact_kernel(uint32_t a, uint32_t b, const unsigned long long* base,
+                               unsigned long long base0, const uint32_t* C,
+                               const unsigned long long* count,
+                               const unsigned long long* out_base, const uint32_t* slot,
+                               uint32_t* outC, uint32_t* outCO) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t k = w; k < (uint64_t)(b - a); k += nw) {
+        const uint32_t n = (uint32_t)count[k];
+        if (!n) continue;
+        const uint32_t* src = C + (base[k] - base0);
+        uint32_t* dst = outC + out_base[k];
+        for (uint32_t q = lane; q < n; q += 32) dst[q] = src[q];
+        if (lane == 0) {
+            outCO[2 * (size_t)slot[k]] = a + (uint32_t)k;
+            outCO[2 * (size_t)slot[k] + 1] = (uint32_t)(out_base[k] + n);
+        }
+    }
+}
+
+uint32_t warps_grid(uint64_t items) {
+    const uint64_t warps = items < 148ull * 64 ? (items ? items : 1) : 148ull * 64;
+    return (uint32_t)((warps * 32 + 255) / 256);
+}
+
+}  // namespace
+
+cudaError_t filter_index_build(FilterIndex* ix, const uint32_t* d_tokens, const uint2* d_sets,
+                               uint32_t n_sets, const PredDev& pred, int algorithm,
+                               cudaStream_t st) {
+    filter_index_free(ix);
+    ix->tokens = d_tokens;
+    ix->sets = d_sets;
+    ix->n_sets = n_sets;
+    ix->pred = pred;
+    ix->algorithm = algorithm;
+    ix->universe = 0;
+    if (!n_sets) return cudaSuccess;
+    uint32_t *ilen = nullptr, *off = nullptr, *mx = nullptr, *keys = nullptr, *keys2 = nullptr,
+             *count = nullptr;
+    unsigned long long *vals = nullptr, *vals2 = nullptr;
+    void* tmp = nullptr;
+    cudaError_t err = cudaSuccess;
+    auto ck = [&](cudaError_t e) {
+        if (err == cudaSuccess && e != cudaSuccess) err = e;
+        return err == cudaSuccess;
+    };
+    const uint32_t g = (n_sets + 255) / 256;
+    if (!ck(cudaMalloc(&ilen, (size_t)n_sets * 4)) || !ck(cudaMalloc(&off, ((size_t)n_sets + 1) * 4)) ||
+        !ck(cudaMalloc(&mx, 4)) || !ck(cudaMemsetAsync(mx, 0, 4, st)))
+        goto done;
+    ilen_kernel<<<g, 256, 0, st>>>(*ix, ilen, mx);
+    if (!ck(cudaGetLastError())) goto done;
+    {
+        size_t tb = 0;
+        if (!ck(cub::DeviceScan::ExclusiveSum(nullptr, tb, ilen, off, (int)n_sets, st)) ||
+            !ck(cudaMalloc(&tmp, tb)) ||
+            !ck(cub::DeviceScan::ExclusiveSum(tmp, tb, ilen, off, (int)n_sets, st)))
+            goto done;
+        cudaFree(tmp);
+        tmp = nullptr;
+        uint32_t last_off = 0, last_len = 0, max_tok = 0;
+        if (!ck(cudaMemcpyAsync(&last_off, off + n_sets - 1, 4, cudaMemcpyDeviceToHost, st)) ||
+            !ck(cudaMemcpyAsync(&last_len, ilen + n_sets - 1, 4, cudaMemcpyDeviceToHost, st)) ||
+            !ck(cudaMemcpyAsync(&max_tok, mx, 4, cudaMemcpyDeviceToHost, st)) ||
+            !ck(cudaStreamSynchronize(st)))
+            goto done;
+        const uint64_t E = (uint64_t)last_off + last_len;
+        if (E > 0x7FFFFFFFull) {  // cub item counts are int
+            err = cudaErrorInvalidValue;
+            goto done;
+        }
+        ix->universe = max_tok + 1;  // joiners.hpp:21-24 (every set non-empty here or max 0)
+        ix->n_post = E;
+        if (!ck(cudaMalloc(&count, ((size_t)ix->universe + 1) * 4)) ||
+            !ck(cudaMemsetAsync(count, 0, ((size_t)ix->universe + 1) * 4, st)) ||
+            !ck(cudaMalloc(&ix->head, ((size_t)ix->universe + 1) * 4)) ||
+            !ck(cudaMalloc(&ix->post, (size_t)(E ? E : 1) * sizeof(uint2))))
+            goto done;
+        if (E) {
+            if (!ck(cudaMalloc(&keys, E * 4)) || !ck(cudaMalloc(&keys2, E * 4)) ||
+                !ck(cudaMalloc(&vals, E * 8)) || !ck(cudaMalloc(&vals2, E * 8)))
+                goto done;
+            entries_kernel<<<g, 256, 0, st>>>(*ix, ilen, off, keys, vals, count);
+            if (!ck(cudaGetLastError())) goto done;
+            int bits = 1;
+            while (bits < 32 && (1ull << bits) < ix->universe) ++bits;
+            tb = 0;
+            // stable: postings of a token stay set-ascending
+            if (!ck(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, vals, vals2, (int)E,
+                                                    0, bits, st)) ||
+                !ck(cudaMalloc(&tmp, tb)) ||
+                !ck(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, vals, vals2, (int)E, 0,
+                                                    bits, st)))
+                goto done;
+            unpack_kernel<<<(uint32_t)((E + 255) / 256), 256, 0, st>>>(vals2, E, ix->post);
+            if (!ck(cudaGetLastError())) goto done;
+            cudaFree(tmp);
+            tmp = nullptr;
+        }
+        tb = 0;
+        if (!ck(cub::DeviceScan::ExclusiveSum(nullptr, tb, count, ix->head, (int)ix->universe + 1, st)) ||
+            !ck(cudaMalloc(&tmp, tb)) ||
+            !ck(cub::DeviceScan::ExclusiveSum(tmp, tb, count, ix->head, (int)ix->universe + 1, st)))
+            goto done;
+        ck(cudaStreamSynchronize(st));
+    }
+done:
+    cudaFree(ilen);
+    cudaFree(off);
+    cudaFree(mx);
+    cudaFree(keys);
+    cudaFree(keys2);
+    cudaFree(vals);
+    cudaFree(vals2);
+    cudaFree(count);
+    cudaFree(tmp);
+    if (err != cudaSuccess) filter_index_free(ix);
+    return err;
+}
+
+void filter_index_free(FilterIndex* ix) {
+    cudaFree(ix->head);
+    cudaFree(ix->post);
+    ix->head = nullptr;
+    ix->post = nullptr;
+    ix->n_post = 0;
+}
+
+cudaError_t filter_bounds(const FilterIndex& ix, uint32_t a, uint32_t b,
+                          unsigned long long* d_bound, cudaStream_t st) {
+    if (b <= a) return cudaSuccess;
+    bounds_kernel<<<warps_grid(b - a), 256, 0, st>>>(ix, a, b, d_bound);
+    return cudaGetLastError();
+}
+
+cudaError_t filter_generate(const FilterIndex& ix, uint32_t a, uint32_t b,
+                            const unsigned long long* d_base, unsigned long long base0,
+                            uint32_t* d_C, unsigned long long* d_count, uint32_t* d_flag,
+                            cudaStream_t st) {
+    if (b <= a) return cudaSuccess;
+    generate_kernel<<<warps_grid(b - a), 256, 0, st>>>(ix, a, b, d_base, base0, d_C, d_count,
+                                                        d_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t filter_compact(uint32_t a, uint32_t b, const unsigned long long* d_base,
+                           unsigned long long base0, const uint32_t* d_C,
+                           const unsigned long long* d_count,
+                           const unsigned long long* d_out_base, const uint32_t* d_slot,
+                           uint32_t* d_outC, uint32_t* d_outCO, cudaStream_t st) {
+    if (b <= a) return cudaSuccess;
+    compact_kernel<<<warps_grid(b - a), 256, 0, st>>>(a, b, d_base, base0, d_C, d_count,
+                                                       d_out_base, d_slot, d_outC, d_outCO);
+    return cudaGetLastError();
+}
+
+}  // namespace ssjb

@@ -1,0 +1,67 @@
+// gpu_filter.cuh -- AllPairs / PPJoin candidate generation on the GPU.
+//
+// The reference generates candidates on one host thread with an incremental inverted index
+// (joiners.hpp:47-102): probe i looks up the postings of its probe-prefix tokens among the
+// index-prefixes of sets 0..i-1 (appended in set order), keeps sets passing the length filter,
+// and deduplicates with epoch marks (first occurrence wins, joiners.hpp:28-41, :62-66).
+//
+// On the device the index is static (all sets' index prefixes, postings set-ascending, built
+// once by a stable radix sort), so every probe is independent:
+//   * postings of token t usable by probe i are one contiguous range: sets >= S_min (the
+//     collection is size-ascending, so the length filter is a lower bound on the set id) and
+//     < i (the incremental index holds sets 0..i-1 only) -- two binary searches;
+//   * s is emitted at its first prefix position p: s is a duplicate at p iff one of its
+//     index-prefix tokens u < r[p] also belongs to r -- checked against r's sorted tokens;
+//   * PPJoin applies the positional filter at that first match (joiners.hpp:92-95).
+// The emitted stream -- probe order, prefix-position order, posting order -- is identical to
+// the reference's batch for batch (tests compare it with the reference's golden streams).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ssj_device.cuh"
+
+namespace ssjb {
+
+// Device-resident static index over a collection's index prefixes.
+struct FilterIndex {
+    uint32_t* head = nullptr;   // [universe + 1] posting offsets per token
+    uint2* post = nullptr;      // {set, position in the set} per posting, set-ascending per token
+    uint64_t n_post = 0;
+    uint32_t universe = 0;
+    uint32_t n_sets = 0;
+    int algorithm = 0;          // SSJ_ALG_ALLPAIRS / SSJ_ALG_PPJOIN
+    PredDev pred{};
+    const uint32_t* tokens = nullptr;  // padded CSR (engine-owned)
+    const uint2* sets = nullptr;       // {pos8, size} (engine-owned)
+};
+
+// Build the index (synchronous on `st`). Returns cudaSuccess or the first error.
+cudaError_t filter_index_build(FilterIndex* ix, const uint32_t* d_tokens, const uint2* d_sets,
+                               uint32_t n_sets, const PredDev& pred, int algorithm,
+                               cudaStream_t st);
+void filter_index_free(FilterIndex* ix);
+
+// Upper bound on probe i's candidates (sum of its posting ranges) for probes [a, b):
+// d_bound[k] = bound of probe a + k.
+cudaError_t filter_bounds(const FilterIndex& ix, uint32_t a, uint32_t b,
+                          unsigned long long* d_bound, cudaStream_t st);
+
+// Candidates of probes [a, b) written at d_C + (d_base[k] - base0) (d_base: exclusive scan
+// of the bounds); d_count[k] receives the number emitted for probe a + k, d_flag[k] = count > 0.
+cudaError_t filter_generate(const FilterIndex& ix, uint32_t a, uint32_t b,
+                            const unsigned long long* d_base, unsigned long long base0,
+                            uint32_t* d_C, unsigned long long* d_count, uint32_t* d_flag,
+                            cudaStream_t st);
+
+// Compact [a, b)'s per-probe candidates into the chunk format (chunk.hpp:20-28): C contiguous,
+// C_O = (probe, cumulative end) for non-empty probes only (joiners.hpp:70). d_out_base =
+// exclusive scan of d_count, d_slot = exclusive scan of d_flag.
+cudaError_t filter_compact(uint32_t a, uint32_t b, const unsigned long long* d_base,
+                           unsigned long long base0, const uint32_t* d_C,
+                           const unsigned long long* d_count,
+                           const unsigned long long* d_out_base, const uint32_t* d_slot,
+                           uint32_t* d_outC, uint32_t* d_outCO, cudaStream_t st);
+
+}  // namespace ssjb

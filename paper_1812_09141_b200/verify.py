@@ -221,6 +221,39 @@ class VerificationEngine:
             stats.comparison_budget_violations += st.comparison_budget_violations
         return pairs[: 2 * n.value].reshape(-1, 2), ovs[: n.value]
 
+    # -- candidate generation and the whole join on the GPU ----------------------------
+    def gpu_generate_candidates(self, algorithm: int, probe_begin: int = 0,
+                                probe_end: Optional[int] = None) -> CandidateChunk:
+        """AllPairs / PPJoin candidates of probes [probe_begin, probe_end) generated on the
+        device (the same stream as the reference generators), copied to the host."""
+        probe_end = 0xFFFFFFFF if probe_end is None else probe_end
+        nC, nCO = C.c_uint64(), C.c_uint64()
+        rc = self._lib.ssj_gpu_generate_candidates(self._h, int(algorithm), probe_begin,
+                                                   probe_end, None, 0, C.byref(nC), None, 0,
+                                                   C.byref(nCO))
+        if rc != N.SSJ_OK and not (nC.value or nCO.value):
+            N.check(rc)
+        Cs = np.zeros(max(nC.value, 1), np.uint32)
+        COs = np.zeros(max(nCO.value, 1), np.uint32)
+        N.check(self._lib.ssj_gpu_generate_candidates(self._h, int(algorithm), probe_begin,
+                                                      probe_end, _vp(Cs), nC.value,
+                                                      C.byref(nC), _vp(COs), nCO.value,
+                                                      C.byref(nCO)))
+        return CandidateChunk(Cs[: nC.value], COs[: nCO.value])
+
+    def gpu_join(self, algorithm: int, max_chunk_candidates: int = 0, pairs: bool = True,
+                 pairs_cap: int = 1 << 24):
+        """Self-join entirely on the device. Returns (pairs (k, 2) uint32 in write_pairs
+        order or None, report dict)."""
+        rep = N.ssj_gpu_join_report()
+        n = C.c_uint64()
+        buf = np.zeros(2 * max(pairs_cap, 1), np.uint32) if pairs else None
+        N.check(self._lib.ssj_gpu_join(self._h, int(algorithm), max_chunk_candidates,
+                                       _vp(buf) if pairs else None, pairs_cap if pairs else 0,
+                                       C.byref(n), C.byref(rep)))
+        out = {k: getattr(rep, k) for k, _ in rep._fields_}
+        return (buf[: 2 * n.value].reshape(-1, 2) if pairs else None), out
+
     # -- device-resident (kernel-only) path --------------------------------------------
     def verify_chunk_device(self, d_C: int, nC: int, d_C_O: int, nCO: int, d_flags: int,
                             d_result: int, stream: int = 0) -> None:

@@ -1,0 +1,101 @@
+"""Candidate generation and the whole join on the GPU: the device
+generator's streams are byte-identical to the reference generators' golden streams
+(joiners.hpp:47-102), and the device join's result pairs equal the reference's brute-force
+pairs and the host join's."""
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+FIXTURES = ["verify_s41", "verify_s42", "verify_s43", "medium_s101", "medium_s202",
+            "medium_s707", "sweep_s1000", "sweep_s1001", "sweep_s1002"]
+
+
+def coll_of(ssj, g):
+    return ssj.Collection(g["tokens"], g["offsets"], g["original_id"])
+
+
+def engine(ssj, coll, pred):
+    return ssj.VerificationEngine(coll, pred, ssj.OutputMode.Pairs,
+                                  ssj.Strategy(ssj.StrategyKind.A, 1))
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_gpu_streams_match_reference(ssj, gpu, name):
+    g = golden(name)
+    coll = coll_of(ssj, g)
+    for k in g.files:
+        if not k.startswith("C_"):
+            continue
+        key = k[2:]
+        fn, num, den = (int(x) for x in key.split("_")[:3])
+        alg = int(key.split("_a")[1])
+        if alg == 2:  # GroupJoin stays on the host
+            continue
+        pred = ssj.SimilarityPredicate(ssj.SimilarityFunction(fn), ssj.Threshold(num, den))
+        with engine(ssj, coll, pred) as eng:
+            chunk = eng.gpu_generate_candidates(alg)
+            assert np.array_equal(chunk.C, g["C_" + key]), key
+            assert np.array_equal(chunk.C_O, g["CO_" + key]), key
+            # any probe window is the matching piece of the stream
+            n = coll.size()
+            lo, hi = n // 3, 2 * n // 3
+            part = eng.gpu_generate_candidates(alg, lo, hi)
+            host, _ = ssj.generate_candidates(coll, pred, ssj.Algorithm(alg), lo, hi, threads=1)
+            assert np.array_equal(part.C, host.C) and np.array_equal(part.C_O, host.C_O), key
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_gpu_join_matches_brute_force(ssj, gpu, oracle, name):
+    """Pairs of the device join == the reference's brute_force_join (oracle.hpp:36-67)."""
+    g = golden(name)
+    coll = coll_of(ssj, g)
+    for k in g.files:
+        if not k.startswith("bf_"):
+            continue
+        fn, num, den = (int(x) for x in k[3:].split("_"))
+        pred = ssj.SimilarityPredicate(ssj.SimilarityFunction(fn), ssj.Threshold(num, den))
+        want = oracle.oracle_pairs(g["original_id"], np.asarray(g[k]).reshape(-1, 3))
+        for alg in (0, 1):
+            with engine(ssj, coll, pred) as eng:
+                eng.set_original_ids(coll.original_id)
+                pairs, rep = eng.gpu_join(alg, max_chunk_candidates=1000)
+                assert np.array_equal(pairs, want), (k, alg)
+                assert rep["count"] == len(want)
+
+
+SHAPES = [
+    # DBLP-like (cfg2 shape, smaller n), J 0.8
+    (dict(sets=30_000, min_size=40, max_size=120, universe=7200, zipf_tokens=True,
+          token_skew=1.0, duplicate_fraction=0.02, max_edits=2, distinct_tokens=True), (4, 5)),
+    # cfg1 shape, J 0.9
+    (dict(sets=100_000, min_size=5, max_size=15, universe=10_000, duplicate_fraction=0.10,
+          max_edits=1, distinct_tokens=True), (9, 10)),
+    # KOSARAK-like long tail, J 0.75
+    (dict(sets=200_000, min_size=2, max_size=2500, zipf_sizes=True, size_skew=1.9,
+          universe=41_000, zipf_tokens=True, token_skew=0.6, duplicate_fraction=0.05,
+          max_edits=2), (3, 4)),
+]
+
+
+@pytest.mark.parametrize("shape,thr", SHAPES)
+def test_gpu_join_matches_host_join(ssj, gpu, shape, thr):
+    """Bench shapes: the device stream equals the host generator's, and the device join (in
+    several probe blocks) returns the host run_join's pairs."""
+    coll = ssj.synth_collection(2024, ssj.SynthConfig(**shape))
+    pred = ssj.jaccard(*thr)
+    for alg in (ssj.Algorithm.AllPairs, ssj.Algorithm.PPJoin):
+        host, _ = ssj.generate_candidates(coll, pred, alg)
+        with engine(ssj, coll, pred) as eng:
+            dev = eng.gpu_generate_candidates(int(alg))
+            assert np.array_equal(dev.C, host.C) and np.array_equal(dev.C_O, host.C_O), alg
+            eng.set_original_ids(coll.original_id)
+            pairs, rep = eng.gpu_join(int(alg), max_chunk_candidates=max(host.C.size // 5, 1))
+            assert rep["candidate_count"] == host.C.size
+            assert rep["chunk_count"] >= 2 or host.C.size < 10
+        cfg = ssj.PipelineConfig(algorithm=alg, mode=ssj.OutputMode.Pairs)
+        ref = ssj.run_join(coll, pred, cfg)
+        want = ssj.sorted_pairs(ref.pairs)
+        assert np.array_equal(pairs, want.reshape(-1, 2)), alg
