@@ -241,6 +241,47 @@ def cpu_reference_rate(coll, pred_t, chunk, sample, reps=3):
     return nC / sec, 1, "port", nC, res["count"], idx
 
 
+def gpu_join_shards(ssj, args, rank, world, local, dev):
+    """BASELINE cfg5 (or --join-workload) self-join run entirely on the GPUs: rank r joins
+    probe shard r of N (equal candidate upper bounds, no exchange step); counts summed, time
+    = max over ranks of the join call (device filtering + verification + pair decoding)."""
+    import torch
+    synth_kw, pred_t, algorithm, desc = WORKLOADS[args.join_workload]
+    coll = ssj.synth_collection(args.seed, ssj.SynthConfig(**synth_kw))
+    pred = ssj.jaccard(*pred_t)
+    alg = 0 if algorithm == "allpairs" else 1
+    eng = ssj.VerificationEngine(coll, pred, ssj.OutputMode.Pairs,
+                                 ssj.Strategy(ssj.StrategyKind.Auto, 32), device=local)
+    eng.set_original_ids(coll.original_id)
+    eng.gpu_join(alg, pairs=False, shard=0, n_shards=max(world, 1) * 64)  # index build, warm-up
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    _, rep = eng.gpu_join(alg, pairs=True, pairs_cap=1 << 22, shard=rank, n_shards=world)
+    eng.close()
+    vals = torch.tensor([rep["join_ms"], float(rep["count"]), float(rep["candidate_count"]),
+                         rep["filtering_ms"], rep["verification_ms"]], dtype=torch.float64,
+                        device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        mx = vals.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vals.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    else:
+        mx = sm = vals
+    ms = float(mx[0].item())
+    return {"workload": desc, "n_sets": coll.size(), "threshold": f"{pred_t[0]}/{pred_t[1]}",
+            "algorithm": algorithm, "n_gpus": world, "join_ms": ms,
+            "count": int(sm[1].item()), "candidates": int(sm[2].item()),
+            "candidates_per_s": float(sm[2].item()) / (ms / 1e3) if ms else None,
+            "filtering_ms_max": float(mx[3].item()), "verification_ms_max": float(mx[4].item()),
+            "path": "ssj_gpu_join_shard: static index on the device, candidate generation and "
+                    "verification in device-resident chunks, pairs decoded + sorted on the "
+                    "device (pairs mode); rank r = probe shard r of N, no exchange step",
+            "reference": "profiles/r1_join_e2e.json: the reference CPU run_join on cfg5"}
+
+
 def run_reference_arm(args):
     rank, world, local = dist_env()
     if rank != 0:
@@ -310,6 +351,8 @@ def main():
     ap.add_argument("--ref-sample", type=float, default=24e6)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--join-workload", default="cfg5",
+                    help="workload of the extra whole-join measurement on the GPU ('none' = off)")
     args = ap.parse_args()
     args.ref_sample = int(args.ref_sample)
     if args.candidates is None:
@@ -435,6 +478,14 @@ def main():
         e2e_s = float(t.item())
     e2e_value = (total_pairs / args.steps) * args.e2e_steps / e2e_s
 
+    # ---- the whole join on the GPU(s): device filtering + verification, probe shards -----
+    join = None
+    if args.join_workload != "none":
+        try:
+            join = gpu_join_shards(ssj, args, rank, world, local, dev)
+        except Exception as e:  # reported, never fatal
+            join = {"error": str(e)[:300]}
+
     # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------------------
     cpu = None
     parity = None
@@ -492,6 +543,7 @@ def main():
                     "d2h_bytes_per_step": int(nC + 64), "steps": args.e2e_steps,
                     "path": "ssj_verify_chunk (C ABI) from pinned host buffers, flags D2H"},
             "gpu_launches": int(args.steps * eng.launches_per_chunk(nC, nCO)),
+            "join": join,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -355,6 +355,12 @@ typedef struct {
 int ssj_gpu_join(ssj_engine* e, int32_t algorithm, uint64_t max_chunk_candidates,
                  uint32_t* pairs_out, uint64_t pairs_cap, uint64_t* n_pairs,
                  ssj_gpu_join_report* report);
+/* Shard `shard` of `n_shards` of the same join (multi-GPU: one engine per device, no
+ * exchange step): the probes are cut into n_shards contiguous ranges of equal candidate
+ * upper bound; the shards' pairs are disjoint and their union is ssj_gpu_join's. */
+int ssj_gpu_join_shard(ssj_engine* e, int32_t algorithm, uint32_t shard, uint32_t n_shards,
+                       uint64_t max_chunk_candidates, uint32_t* pairs_out, uint64_t pairs_cap,
+                       uint64_t* n_pairs, ssj_gpu_join_report* report);
 
 /* ---- diagnostics -------------------------------------------------------------------- */
 /* Streaming read bandwidth (GB/s) of a `bytes` device buffer read `reps` times with 16-byte

@@ -134,6 +134,8 @@ SIGNATURES = {
                                               C.c_uint64, u64p, vp, C.c_uint64, u64p]),
     "ssj_gpu_join": (C.c_int, [vp, C.c_int32, C.c_uint64, vp, C.c_uint64, u64p,
                                C.POINTER(ssj_gpu_join_report)]),
+    "ssj_gpu_join_shard": (C.c_int, [vp, C.c_int32, C.c_uint32, C.c_uint32, C.c_uint64, vp,
+                                     C.c_uint64, u64p, C.POINTER(ssj_gpu_join_report)]),
     "ssj_measure_read_bandwidth": (C.c_int, [C.c_int, C.c_uint64, C.c_uint32,
                                              C.POINTER(C.c_double)]),
     "ssj_host_alloc": (vp, [C.c_size_t]),

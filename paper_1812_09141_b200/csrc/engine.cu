@@ -1118,6 +1118,8 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
 
 namespace {
 
+typedef unsigned __int128 u128_host;
+
 struct DevBuf {
     void* p = nullptr;
     ~DevBuf() { cudaFree(p); }
@@ -1275,14 +1277,22 @@ int ssj_gpu_generate_candidates(ssj_engine* e, int32_t algorithm, uint32_t probe
 int ssj_gpu_join(ssj_engine* e, int32_t algorithm, uint64_t max_chunk_candidates,
                  uint32_t* pairs_out, uint64_t pairs_cap, uint64_t* n_pairs,
                  ssj_gpu_join_report* report) {
+    return ssj_gpu_join_shard(e, algorithm, 0, 1, max_chunk_candidates, pairs_out, pairs_cap,
+                              n_pairs, report);
+}
+
+int ssj_gpu_join_shard(ssj_engine* e, int32_t algorithm, uint32_t shard, uint32_t n_shards,
+                       uint64_t max_chunk_candidates, uint32_t* pairs_out, uint64_t pairs_cap,
+                       uint64_t* n_pairs, ssj_gpu_join_report* report) {
     if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
+    if (n_shards == 0 || shard >= n_shards) return fail(SSJ_ERR_INVALID_ARGUMENT, "bad shard");
     if (pairs_out && !n_pairs) return fail(SSJ_ERR_INVALID_ARGUMENT, "null n_pairs");
     DeviceScope ds(e->device);
     const auto t_start = std::chrono::steady_clock::now();
     ssj_gpu_join_report rep{};
     int rc;
     if ((rc = ensure_filter_index(e, algorithm, &rep.index_ms))) return rc;
-    const bool want_pairs = pairs_out != nullptr || (n_pairs && pairs_cap == 0 && !pairs_out && false);
+    const bool want_pairs = pairs_out != nullptr;
     if (want_pairs && !e->d_oid && (rc = ssj_engine_set_original_ids(e, nullptr))) return rc;
     cudaStream_t st = e->s_comp;
     cudaEvent_t ev[4];
@@ -1305,8 +1315,17 @@ int ssj_gpu_join(ssj_engine* e, int32_t algorithm, uint64_t max_chunk_candidates
     DevBuf acc, keys_all;
     if ((rc = acc.alloc(SSJ_RESULT_WORDS * 8))) return rc;
     uint64_t keys_n = 0, keys_cap = 0;
-    const uint32_t n = e->n_sets;
-    for (uint32_t a = 0; a < n;) {
+    // this shard's probes: equal shares of the total candidate upper bound
+    const uint64_t total = g.hbase[e->n_sets];
+    auto cut = [&](uint32_t k) -> uint32_t {
+        if (k == 0) return 0;
+        if (k >= n_shards) return e->n_sets;
+        const unsigned long long target = (unsigned long long)((u128_host)total * k / n_shards);
+        return (uint32_t)(std::lower_bound(g.hbase.begin(), g.hbase.end(), target) - g.hbase.begin());
+    };
+    const uint32_t p_begin = std::min(cut(shard), e->n_sets);
+    const uint32_t n = std::max(p_begin, std::min(cut(shard + 1), e->n_sets));
+    for (uint32_t a = p_begin; a < n;) {
         // the longest probe block whose candidate upper bound fits the budget (>= 1 probe)
         uint32_t b = (uint32_t)(std::upper_bound(g.hbase.begin() + a + 1, g.hbase.end(),
                                                  g.hbase[a] + cap) - g.hbase.begin()) - 1;

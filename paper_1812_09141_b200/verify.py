@@ -242,15 +242,17 @@ class VerificationEngine:
         return CandidateChunk(Cs[: nC.value], COs[: nCO.value])
 
     def gpu_join(self, algorithm: int, max_chunk_candidates: int = 0, pairs: bool = True,
-                 pairs_cap: int = 1 << 24):
-        """Self-join entirely on the device. Returns (pairs (k, 2) uint32 in write_pairs
-        order or None, report dict)."""
+                 pairs_cap: int = 1 << 24, shard: int = 0, n_shards: int = 1):
+        """Self-join (or shard `shard` of `n_shards` of it) entirely on the device. Returns
+        (pairs (k, 2) uint32 in write_pairs order or None, report dict)."""
         rep = N.ssj_gpu_join_report()
         n = C.c_uint64()
         buf = np.zeros(2 * max(pairs_cap, 1), np.uint32) if pairs else None
-        N.check(self._lib.ssj_gpu_join(self._h, int(algorithm), max_chunk_candidates,
-                                       _vp(buf) if pairs else None, pairs_cap if pairs else 0,
-                                       C.byref(n), C.byref(rep)))
+        N.check(self._lib.ssj_gpu_join_shard(self._h, int(algorithm), shard, n_shards,
+                                             max_chunk_candidates,
+                                             _vp(buf) if pairs else None,
+                                             pairs_cap if pairs else 0, C.byref(n),
+                                             C.byref(rep)))
         out = {k: getattr(rep, k) for k, _ in rep._fields_}
         return (buf[: 2 * n.value].reshape(-1, 2) if pairs else None), out
 

@@ -99,3 +99,20 @@ def test_gpu_join_matches_host_join(ssj, gpu, shape, thr):
         ref = ssj.run_join(coll, pred, cfg)
         want = ssj.sorted_pairs(ref.pairs)
         assert np.array_equal(pairs, want.reshape(-1, 2)), alg
+
+
+def test_gpu_join_shards_partition_the_join(ssj, gpu):
+    """Shards (one per GPU in a multi-GPU run) are disjoint and together give the join."""
+    coll = ssj.synth_collection(7, ssj.SynthConfig(**SHAPES[0][0]))
+    pred = ssj.jaccard(4, 5)
+    with engine(ssj, coll, pred) as eng:
+        eng.set_original_ids(coll.original_id)
+        full, rep = eng.gpu_join(0)
+        parts, cands = [], 0
+        for k in range(3):
+            pk, rk = eng.gpu_join(0, shard=k, n_shards=3)
+            parts.append(pk)
+            cands += rk["candidate_count"]
+        assert cands == rep["candidate_count"]
+        got = ssj.sorted_pairs(np.concatenate(parts))
+        assert np.array_equal(got, full)
