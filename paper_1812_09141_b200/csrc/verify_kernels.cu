@@ -598,7 +598,11 @@ __device__ __forceinline__ uint32_t count8(const uint8_t* __restrict__ map,
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const uint32_t d = min(t[q] - lo, R);
+#if SSJB_RUN_MAP_BITS
+        if (kMap) c += (reinterpret_cast<const uint32_t*>(map)[d >> 5] >> (d & 31)) & 1u;
+#else
         if (kMap) c += map[d];
+#endif
         else c += (__ldg(bits + (d >> 5)) >> (d & 31)) & 1u;
     }
     return c;
@@ -939,7 +943,14 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
                 for (uint32_t u = tid; u * 16 <= range; u += T)
                     reinterpret_cast<uint4*>(mp)[u] = make_uint4(0, 0, 0, 0);
                 __syncthreads();
+#if SSJB_RUN_MAP_BITS
+                for (uint32_t i = tid; i < R0.rsize; i += T) {
+                    const uint32_t d = __ldg(r + i) - R0.lo;
+                    atomicOr(reinterpret_cast<uint32_t*>(mp) + (d >> 5), 1u << (d & 31));
+                }
+#else
                 for (uint32_t i = tid; i < R0.rsize; i += T) mp[__ldg(r + i) - R0.lo] = 1;
+#endif
                 __syncthreads();
             }
 

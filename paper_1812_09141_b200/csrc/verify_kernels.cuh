@@ -41,6 +41,9 @@ constexpr uint32_t kLongPair = 256;            // candidates longer than this go
 #ifndef SSJB_RUN_BLOCK
 #define SSJB_RUN_BLOCK 16
 #endif
+#ifndef SSJB_RUN_MAP_BITS
+#define SSJB_RUN_MAP_BITS 0  // 1: the probe map in shared memory is a bitmap (slower: ALU)
+#endif
 #ifndef SSJB_RUN_THREADS
 #define SSJB_RUN_THREADS 256
 #endif
