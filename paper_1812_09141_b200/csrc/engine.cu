@@ -1152,6 +1152,7 @@ int ensure_filter_index(ssj_engine* e, int algorithm, double* build_ms) {
             *build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
     e->fidx->algorithm = algorithm;  // one index serves both (postings carry positions)
+    e->fidx->heads = e->d_heads;
     return SSJ_OK;
 }
 

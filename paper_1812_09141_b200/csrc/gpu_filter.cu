@@ -138,10 +138,42 @@ __global__ void bounds_kernel(const FilterIndex ix, uint32_t a, uint32_t b,
 // a lane keeps its set s unless s was already reached at an earlier prefix position (one of
 // s's index-prefix tokens below r[p] is in r) and, for PPJoin, unless the positional filter
 // rejects it at this first match. Kept sets are appended in order (ballot compaction).
-__global__ void generate_kernel(const FilterIndex ix, uint32_t a, uint32_t b,
-                                const unsigned long long* base, unsigned long long base0,
-                                uint32_t* C, unsigned long long* count, uint32_t* flag) {
+// The posting ranges of 32 prefix positions are found at once (one binary-search pair per
+// lane), r's first kGenRStage tokens are staged in the warp's shared memory for the dedup
+// searches, and s's first 8 tokens come from its packed head record in one 256-bit load.
+constexpr uint32_t kGenThreads = 256;
+constexpr uint32_t kGenRStage = 256;
+
+__device__ __forceinline__ void ld8(const uint32_t* __restrict__ s, uint32_t t[8]) {
+    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]),
+                   "=r"(t[6]), "=r"(t[7])
+                 : "l"(s));
+}
+
+// is v one of r[lo..p)? r staged in rs (first kGenRStage tokens) or global. Returns the
+// lower-bound position (>= lo) through *pos.
+__device__ __forceinline__ bool in_r(const uint32_t* __restrict__ rs,
+                                     const uint32_t* __restrict__ r, uint32_t lo, uint32_t p,
+                                     uint32_t v, uint32_t* pos) {
+    uint32_t l = lo, h = p;
+    while (l < h) {
+        const uint32_t mid = (l + h) >> 1;
+        const uint32_t x = mid < kGenRStage ? rs[mid] : __ldg(r + mid);
+        if (x < v) l = mid + 1;
+        else h = mid;
+    }
+    *pos = l;
+    return l < p && (l < kGenRStage ? rs[l] : __ldg(r + l)) == v;
+}
+
+__global__ void __launch_bounds__(kGenThreads, 4)
+    generate_kernel(const FilterIndex ix, uint32_t a, uint32_t b, const unsigned long long* base,
+                    unsigned long long base0, uint32_t* C, unsigned long long* count,
+                    uint32_t* flag) {
+    __shared__ uint32_t rstage[kGenThreads / 32][kGenRStage];
     const uint32_t lane = threadIdx.x & 31;
+    uint32_t* const rs = rstage[threadIdx.x >> 5];
     const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const bool positional = ix.algorithm == 1;
@@ -153,55 +185,77 @@ __global__ void generate_kernel(const FilterIndex ix, uint32_t a, uint32_t b,
             const uint32_t P = dev_prefix_lengths(ix.pred, m).x;
             const uint32_t smin = first_set_of_size(ix, dev_size_lower_bound(ix.pred, m));
             const uint32_t* r = set_tokens(ix, i);
+            __syncwarp();
+            for (uint32_t u = lane; u < min(P, kGenRStage); u += 32) rs[u] = __ldg(r + u);
+            __syncwarp();
             uint32_t* out = C + (base[k] - base0);
-            for (uint32_t p = 0; p < P; ++p) {
-                const uint32_t t = __ldg(r + p);
-                if (t >= ix.universe) continue;
-                const uint32_t h0 = __ldg(ix.head + t), h1 = __ldg(ix.head + t + 1);
-                // both bounds by the whole warp's lane 0 (uniform), then broadcast
-                uint32_t lo = 0, hi = 0;
-                if (lane == 0) {
-                    lo = posting_lower_bound(ix, h0, h1, smin);
-                    hi = posting_lower_bound(ix, lo, h1, i);
-                }
-                lo = __shfl_sync(0xffffffffu, lo, 0);
-                hi = __shfl_sync(0xffffffffu, hi, 0);
-                for (uint32_t q0 = lo; q0 < hi; q0 += 32) {
-                    const uint32_t q = q0 + lane;
-                    bool keep = false;
-                    uint32_t s = 0;
-                    if (q < hi) {
-                        const uint2 pe = __ldg(&ix.post[q]);
-                        s = pe.x;
-                        keep = true;
-                        if (p) {
-                            // duplicate iff an index-prefix token u < t of s is in r[0..p)
-                            const uint32_t ns = set_size(ix, s);
-                            const uint32_t il = dev_prefix_lengths(ix.pred, ns).y;
-                            const uint32_t* st = set_tokens(ix, s);
-                            uint32_t lo_r = 0;
-                            for (uint32_t u = 0; u < il; ++u) {
-                                const uint32_t v = __ldg(st + u);
-                                if (v >= t) break;
-                                uint32_t l = lo_r, h = p;  // r[0..p) holds r's tokens < t
-                                while (l < h) {
-                                    const uint32_t mid = (l + h) >> 1;
-                                    if (__ldg(r + mid) < v) l = mid + 1;
-                                    else h = mid;
-                                }
-                                if (l < p && __ldg(r + l) == v) {
-                                    keep = false;
-                                    break;
-                                }
-                                lo_r = l;
-                            }
-                        }
-                        if (keep && positional)
-                            keep = dev_positional_keep(ix.pred, m, set_size(ix, s), p, pe.y);
+            for (uint32_t p0 = 0; p0 < P; p0 += 32) {
+                // ranges of prefix positions p0 + lane
+                uint32_t my_lo = 0, my_hi = 0, my_t = 0;
+                if (p0 + lane < P) {
+                    my_t = __ldg(r + p0 + lane);
+                    if (my_t < ix.universe) {
+                        const uint32_t h0 = __ldg(ix.head + my_t), h1 = __ldg(ix.head + my_t + 1);
+                        my_lo = posting_lower_bound(ix, h0, h1, smin);
+                        my_hi = posting_lower_bound(ix, my_lo, h1, i);
                     }
-                    const unsigned km = __ballot_sync(0xffffffffu, keep);
-                    if (keep) out[n_out + __popc(km & ((1u << lane) - 1u))] = s;
-                    n_out += __popc(km);
+                }
+                const uint32_t pend = min(32u, P - p0);
+                for (uint32_t pl = 0; pl < pend; ++pl) {
+                    const uint32_t p = p0 + pl;
+                    const uint32_t lo = __shfl_sync(0xffffffffu, my_lo, pl);
+                    const uint32_t hi = __shfl_sync(0xffffffffu, my_hi, pl);
+                    const uint32_t t = __shfl_sync(0xffffffffu, my_t, pl);
+                    for (uint32_t q0 = lo; q0 < hi; q0 += 32) {
+                        const uint32_t q = q0 + lane;
+                        bool keep = false;
+                        uint32_t s = 0;
+                        if (q < hi) {
+                            const uint2 pe = __ldg(&ix.post[q]);
+                            s = pe.x;
+                            keep = true;
+                            // duplicate iff an index-prefix token v < t of s is in r[0..p)
+                            if (p && pe.y) {  // pe.y = position of t in s: tokens before it are < t
+                                uint32_t lo_r = 0, pos;
+                                if (ix.heads) {
+                                    uint32_t hv[8];
+                                    ld8(reinterpret_cast<const uint32_t*>(ix.heads + 2 * (size_t)s), hv);
+                                    const uint32_t lim = min(pe.y, 8u);
+#pragma unroll
+                                    for (uint32_t u = 0; u < 8; ++u) {
+                                        if (u < lim && keep) {
+                                            if (in_r(rs, r, lo_r, p, hv[u] & kHeadTokenMask, &pos)) keep = false;
+                                            lo_r = pos;
+                                        }
+                                    }
+                                    if (keep && pe.y > 8) {
+                                        const uint32_t* st = set_tokens(ix, s);
+                                        for (uint32_t u = 8; u < pe.y; ++u) {
+                                            if (in_r(rs, r, lo_r, p, __ldg(st + u), &pos)) {
+                                                keep = false;
+                                                break;
+                                            }
+                                            lo_r = pos;
+                                        }
+                                    }
+                                } else {
+                                    const uint32_t* st = set_tokens(ix, s);
+                                    for (uint32_t u = 0; u < pe.y; ++u) {
+                                        if (in_r(rs, r, lo_r, p, __ldg(st + u), &pos)) {
+                                            keep = false;
+                                            break;
+                                        }
+                                        lo_r = pos;
+                                    }
+                                }
+                            }
+                            if (keep && positional)
+                                keep = dev_positional_keep(ix.pred, m, set_size(ix, s), p, pe.y);
+                        }
+                        const unsigned km = __ballot_sync(0xffffffffu, keep);
+                        if (keep) out[n_out + __popc(km & ((1u << lane) - 1u))] = s;
+                        n_out += __popc(km);
+                    }
                 }
             }
         }
@@ -354,8 +408,8 @@ cudaError_t filter_generate(const FilterIndex& ix, uint32_t a, uint32_t b,
                             uint32_t* d_C, unsigned long long* d_count, uint32_t* d_flag,
                             cudaStream_t st) {
     if (b <= a) return cudaSuccess;
-    generate_kernel<<<warps_grid(b - a), 256, 0, st>>>(ix, a, b, d_base, base0, d_C, d_count,
-                                                        d_flag);
+    generate_kernel<<<warps_grid(b - a), kGenThreads, 0, st>>>(ix, a, b, d_base, base0, d_C,
+                                                                d_count, d_flag);
     return cudaGetLastError();
 }
 

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include "ssj_device.cuh"
+#include "verify_kernels.cuh"
 
 namespace ssjb {
 
@@ -35,6 +36,7 @@ struct FilterIndex {
     PredDev pred{};
     const uint32_t* tokens = nullptr;  // padded CSR (engine-owned)
     const uint2* sets = nullptr;       // {pos8, size} (engine-owned)
+    const uint4* heads = nullptr;      // packed head records (engine-owned, nullable)
 };
 
 // Build the index (synchronous on `st`). Returns cudaSuccess or the first error.
