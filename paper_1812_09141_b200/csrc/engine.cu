@@ -146,6 +146,29 @@ namespace ssjh {
 int set_error(int code, const std::string& msg) { return fail(code, msg); }
 }  // namespace ssjh
 
+// Device scratch of the GPU join (cached on the engine across calls).
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() { cudaFree(p); }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+    int alloc(size_t bytes) {
+        cudaFree(p);
+        p = nullptr;
+        if (cudaMalloc(&p, bytes ? bytes : 1) != cudaSuccess)
+            return ssjh::set_error(SSJ_ERR_CUDA, "cudaMalloc failed (GPU join)");
+        return SSJ_OK;
+    }
+};
+
+// Per-join scratch: per-probe bounds (scanned), block buffers.
+struct GenState {
+    DevBuf bound, base, G, count, flag, obase, slot, C, CO, tmp;
+    size_t tmp_bytes = 0, G_cap = 0, C_cap = 0, blk_cap = 0;
+    std::vector<unsigned long long> hbase;  // exclusive scan of the bounds, n + 1 entries
+};
+
+
 struct ssj_engine {
     int device = 0;
     ssj_predicate hpred{};
@@ -161,6 +184,7 @@ struct ssj_engine {
     uint32_t* d_req_tab = nullptr;  // Jaccard/Dice required overlap by |r|+|s|
     uint4* d_heads = nullptr;       // packed set heads (null: tokens too large to pack)
     ssjb::FilterIndex* fidx = nullptr;  // GPU candidate generation index (built on first use)
+    GenState* gen = nullptr;            // its bounds and block buffers
     uint32_t req_tab_n = 0;
     cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
     ChunkSlot slot[2];
@@ -832,6 +856,7 @@ void ssj_engine_destroy(ssj_engine* e) {
         ssjb::filter_index_free(e->fidx);
         delete e->fidx;
     }
+    delete e->gen;
     cudaFree(e->d_res_slots);
     cudaFree(e->d_res_ov);
     cudaFree(e->d_res_n);
@@ -1120,20 +1145,6 @@ namespace {
 
 typedef unsigned __int128 u128_host;
 
-struct DevBuf {
-    void* p = nullptr;
-    ~DevBuf() { cudaFree(p); }
-    template <typename T>
-    T* as() const { return static_cast<T*>(p); }
-    int alloc(size_t bytes) {
-        cudaFree(p);
-        p = nullptr;
-        if (cudaMalloc(&p, bytes ? bytes : 1) != cudaSuccess)
-            return fail(SSJ_ERR_CUDA, "cudaMalloc failed (GPU join)");
-        return SSJ_OK;
-    }
-};
-
 int ensure_filter_index(ssj_engine* e, int algorithm, double* build_ms) {
     if (algorithm != SSJ_ALG_ALLPAIRS && algorithm != SSJ_ALG_PPJOIN)
         return fail(SSJ_ERR_INVALID_ARGUMENT, "GPU generation supports allpairs and ppjoin");
@@ -1155,13 +1166,6 @@ int ensure_filter_index(ssj_engine* e, int algorithm, double* build_ms) {
     e->fidx->heads = e->d_heads;
     return SSJ_OK;
 }
-
-// Per-join scratch: per-probe bounds (scanned), block buffers.
-struct GenState {
-    DevBuf bound, base, G, count, flag, obase, slot, C, CO, tmp;
-    size_t tmp_bytes = 0, G_cap = 0, C_cap = 0, blk_cap = 0;
-    std::vector<unsigned long long> hbase;  // exclusive scan of the bounds, n + 1 entries
-};
 
 template <typename F>
 int cub_run(GenState& g, F&& f, cudaStream_t st) {
@@ -1263,8 +1267,9 @@ int ssj_gpu_generate_candidates(ssj_engine* e, int32_t algorithm, uint32_t probe
     probe_end = std::min(probe_end, e->n_sets);
     *nC_out = *nCO_out = 0;
     if (probe_begin >= probe_end) return SSJ_OK;
-    GenState g;
-    if ((rc = gen_bounds(e, g))) return rc;
+    if (!e->gen) e->gen = new GenState;
+    GenState& g = *e->gen;
+    if (g.hbase.empty() && (rc = gen_bounds(e, g))) return rc;
     uint64_t nC = 0, nCO = 0;
     if ((rc = gen_block(e, g, probe_begin, probe_end, &nC, &nCO))) return rc;
     *nC_out = nC;
@@ -1305,9 +1310,10 @@ int ssj_gpu_join_shard(ssj_engine* e, int32_t algorithm, uint32_t shard, uint32_
         }
     } evg{ev};
     const uint64_t cap = max_chunk_candidates ? max_chunk_candidates : (256ull << 20);
-    GenState g;
+    if (!e->gen) e->gen = new GenState;
+    GenState& g = *e->gen;
     SSJ_CK(cudaEventRecord(ev[0], st));
-    if ((rc = gen_bounds(e, g))) return rc;
+    if (g.hbase.empty() && (rc = gen_bounds(e, g))) return rc;  // per engine: fixed collection
     SSJ_CK(cudaEventRecord(ev[1], st));
     SSJ_CK(cudaEventSynchronize(ev[1]));
     float ms = 0;
