@@ -152,54 +152,6 @@ reject:
     return false;
 }
 
-// Thread-per-pair merge as one branch-light loop (every lane runs the same instruction
-// stream; lanes differ only in trip count). Three down-counters replace the reference's
-// two-sided test (verify.hpp:57-58):
-//   need  = required - overlap              (0  -> met)
-//   rem_r = (m - required + 1) - miss_r     (0  -> overlap + (m - i) < required)
-//   rem_s = (n - required + 1) - miss_s     (0  -> overlap + (n - j) < required)
-// While none is 0, i = overlap + miss_r <= m - 1 and j <= n - 1, so no exhaustion test is
-// needed and r[i], s[j] stay in bounds.
-//   r : probe tokens (shared or global), s : candidate tokens (global), b0 = s[0] prefetched
-//   1 <= req <= min(m, n)
-// With kFull the merge of a met pair is completed and *ov_out = |r ∩ s|.
-template <bool kFull>
-__device__ __forceinline__ bool merge_unified(const uint32_t* __restrict__ r, uint32_t m,
-                                              const uint32_t* __restrict__ s, uint32_t n,
-                                              uint32_t req, uint32_t b0, uint32_t* ov_out) {
-    int need = (int)req;
-    int rem_r = (int)(m - req) + 1;
-    int rem_s = (int)(n - req) + 1;
-    uint32_t i = 0, j = 0;
-    uint32_t a = r[0], b = b0;
-    for (;;) {
-        const bool lt = a < b, gt = a > b;
-        i += !gt;
-        j += !lt;
-        need -= !(lt | gt);
-        rem_r -= lt;
-        rem_s -= gt;
-        if (need == 0 || rem_r == 0 || rem_s == 0) break;
-        a = r[i];
-        b = __ldg(s + j);
-    }
-    const bool met = need == 0;
-    if (kFull) {
-        uint32_t ov = req - (uint32_t)need;
-        if (met) {
-            while (i < m && j < n) {
-                a = r[i];
-                b = __ldg(s + j);
-                ov += (a == b);
-                i += (a <= b);
-                j += (b <= a);
-            }
-        }
-        *ov_out = met ? ov : 0;
-    }
-    return met;
-}
-
 // Full overlap (no early exit) for a qualifying pair: used by the cooperative kernels'
 // results mode, thread-sequential over global memory.
 __device__ __forceinline__ uint32_t full_overlap_seq(const uint32_t* __restrict__ r, uint32_t m,
