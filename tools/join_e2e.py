@@ -64,13 +64,19 @@ def main():
         eng.set_original_ids(coll.original_id)
         setup = 1e3 * (time.perf_counter() - t0)
         t1 = time.perf_counter()
+        _, first = eng.gpu_join(int(alg), pairs=args.mode == "pairs")  # builds the index
+        first_wall = 1e3 * (time.perf_counter() - t1)
+        t1 = time.perf_counter()
         pairs, rep = eng.gpu_join(int(alg), pairs=args.mode == "pairs")
         wall = 1e3 * (time.perf_counter() - t1)
         eng.close()
         r = {"count": rep["count"], "candidates": rep["candidate_count"],
              "chunks": rep["chunk_count"], "join_ms": rep["join_ms"],
-             "index_ms": rep["index_ms"], "filtering_ms": rep["filtering_ms"],
-             "verification_ms": rep["verification_ms"], "setup_ms": setup, "wall_ms": wall}
+             "filtering_ms": rep["filtering_ms"], "verification_ms": rep["verification_ms"],
+             "first_call_join_ms": first["join_ms"], "index_ms": first["index_ms"],
+             "first_call_wall_ms": first_wall, "setup_ms": setup, "wall_ms": wall,
+             "note": "join_ms: second call (index and scratch cached on the engine); "
+                     "first_call_join_ms includes the static index build and allocations"}
         return r
 
     ssj.run_join(ssj.Collection.from_sets([[1, 2], [1, 2]]), pred)  # warm the CUDA context
