@@ -281,9 +281,27 @@ __device__ __forceinline__ bool verify_bitmap(const uint32_t* __restrict__ bits,
 // 5-step shuffle binary search over those ends. Slice descriptors, probe bitmaps and probe
 // tokens are read through L1 (lanes of a tile share them). Long candidates are deferred to
 // long_kernel exactly as in tile_kernel.
+// The tile's loads that do not depend on other loads: the lane's C ids and the tile's first
+// and last slice (prefetched one tile ahead by warp_tile_kernel).
+struct TilePre {
+    uint32_t cand[SSJB_TILE_ITEMS];
+    uint32_t e0, e1;
+};
+
+__device__ __forceinline__ void tile_prefetch(const KParams& p, uint32_t tile, TilePre& t) {
+    constexpr int kItems = SSJB_TILE_ITEMS;
+    const uint64_t slot0 = (uint64_t)tile * kTile;
+    const uint64_t slot1 = min(slot0 + (uint64_t)kTile, p.nC);
+    const uint64_t my0 = slot0 + (uint64_t)(threadIdx.x & 31) * kItems;
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) t.cand[q] = my0 + q < slot1 ? __ldg(p.C + my0 + q) : 0u;
+    t.e0 = slot0 < p.nC ? __ldg(p.tile_first + tile) : kNone;
+    t.e1 = slot0 < p.nC ? __ldg(p.tile_first + tile + 1) : kNone;
+}
+
 template <int kOut, bool kStats, bool kPacked>
-__device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile, unsigned& count,
-                                          unsigned& prunes, unsigned& verified) {
+__device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile, const TilePre& pre,
+                                          unsigned& count, unsigned& prunes, unsigned& verified) {
     constexpr int kItems = SSJB_TILE_ITEMS;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t slot0 = (uint64_t)tile * kTile;
@@ -292,20 +310,8 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
     const uint64_t my0 = slot0 + (uint64_t)lane * kItems;
 
     uint32_t cand[kItems];
-    if (kItems % 4 == 0 && my0 + kItems <= slot1 && ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0)) {
-        const uint4* c4 = reinterpret_cast<const uint4*>(p.C + my0);
 #pragma unroll
-        for (int q = 0; q < kItems / 4; ++q) {
-            const uint4 v = __ldg(c4 + q);
-            cand[4 * q] = v.x;
-            cand[4 * q + 1] = v.y;
-            cand[4 * q + 2] = v.z;
-            cand[4 * q + 3] = v.w;
-        }
-    } else {
-#pragma unroll
-        for (int q = 0; q < kItems; ++q) cand[q] = my0 + q < slot1 ? __ldg(p.C + my0 + q) : 0u;
-    }
+    for (int q = 0; q < kItems; ++q) cand[q] = pre.cand[q];
     uint2 sd[kItems];
     uint32_t hr[kPacked ? kItems : 1][8];  // kPacked: the candidates' head records
     if (kPacked) {
@@ -325,10 +331,10 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
             sd[q] = cand[q] < p.n_sets ? __ldg(p.sets + cand[q]) : make_uint2(0, 0);
     }
 
-    const uint32_t e0 = __ldg(p.tile_first + tile);
+    const uint32_t e0 = pre.e0;
     uint32_t ns = 0;
     if (e0 < p.n_slices) {
-        uint32_t e_hi = __ldg(p.tile_first + tile + 1);
+        uint32_t e_hi = pre.e1;
         if (e_hi >= p.n_slices) e_hi = p.n_slices - 1;
         ns = e_hi - e0 + 1;
     }
@@ -476,8 +482,22 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) warp_tile_kernel(co
     const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     unsigned count = 0, prunes = 0, verified = 0;
-    for (uint64_t w = gw; w < n; w += n_warps)
-        warp_tile<kOut, kStats, kPacked>(p, __ldg(p.short_tiles + w), count, prunes, verified);
+    // software pipeline over the warp's tiles: the next tile's C ids and slice bounds are in
+    // flight while this tile is verified, the tile after next's index one step earlier
+    uint32_t tile = gw < n ? __ldg(p.short_tiles + gw) : 0u;
+    uint32_t tile_n = gw + n_warps < n ? __ldg(p.short_tiles + gw + n_warps) : 0u;
+    TilePre cur;
+    if (gw < n) tile_prefetch(p, tile, cur);
+    for (uint64_t w = gw; w < n; w += n_warps) {
+        TilePre nxt;
+        const bool more = w + n_warps < n;
+        if (more) tile_prefetch(p, tile_n, nxt);
+        const uint32_t tile_nn = w + 2 * n_warps < n ? __ldg(p.short_tiles + w + 2 * n_warps) : 0u;
+        warp_tile<kOut, kStats, kPacked>(p, tile, cur, count, prunes, verified);
+        if (more) cur = nxt;
+        tile = tile_n;
+        tile_n = tile_nn;
+    }
     acc_add(p.acc, 0, count);
     if (kStats) {
         acc_add(p.acc, 2, verified);
