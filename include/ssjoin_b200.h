@@ -327,7 +327,9 @@ void ssj_join_result_free(ssj_join_result* r);
  * device from its resident collection (static index over all index prefixes, built once per
  * engine): the same stream as ssj_generate_candidates / the reference generators
  * (joiners.hpp:47-102), returned in host buffers. *nC_out / *nCO_out receive the sizes;
- * SSJ_ERR_RUNTIME when a capacity is too small (sizes still reported).
+ * SSJ_ERR_RUNTIME when a capacity is too small (sizes still reported). The collection must be
+ * in the reference's preprocessed order (sizes non-decreasing, collection.hpp:115-119),
+ * else SSJ_ERR_INVALID_ARGUMENT.
  */
 int ssj_gpu_generate_candidates(ssj_engine* e, int32_t algorithm, uint32_t probe_begin,
                                 uint32_t probe_end, uint32_t* C_out, uint64_t C_cap,

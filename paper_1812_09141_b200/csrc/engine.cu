@@ -1151,6 +1151,18 @@ int ensure_filter_index(ssj_engine* e, int algorithm, double* build_ms) {
     if (build_ms) *build_ms = 0;
     if (!e->fidx) {
         auto t0 = std::chrono::steady_clock::now();
+        // the static index relies on the reference's collection order (collection.hpp:115-119:
+        // sizes non-decreasing), like the incremental index's length filter does
+        if (e->n_sets) {
+            std::vector<uint2> sd(e->n_sets);
+            SSJ_CK(cudaMemcpy(sd.data(), e->d_sets, (size_t)e->n_sets * sizeof(uint2),
+                              cudaMemcpyDeviceToHost));
+            for (uint32_t i = 1; i < e->n_sets; ++i)
+                if (sd[i].y < sd[i - 1].y)
+                    return fail(SSJ_ERR_INVALID_ARGUMENT,
+                                "GPU generation needs the collection in preprocessed (size, "
+                                "lexicographic) order");
+        }
         e->fidx = new ssjb::FilterIndex;
         cudaError_t err = ssjb::filter_index_build(e->fidx, e->d_tokens, e->d_sets, e->n_sets,
                                                    e->pred, algorithm, e->s_comp);

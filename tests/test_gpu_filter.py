@@ -116,3 +116,44 @@ def test_gpu_join_shards_partition_the_join(ssj, gpu):
         assert cands == rep["candidate_count"]
         got = ssj.sorted_pairs(np.concatenate(parts))
         assert np.array_equal(got, full)
+
+
+def test_gpu_generation_edge_cases(ssj, gpu):
+    """Empty sets, large tokens (no packed head records: the dedup reads the CSR), a single
+    set, and empty probe windows: device streams equal the host generator's."""
+    rng = np.random.default_rng(3)
+    sets = [sorted(rng.choice(5000, size=int(rng.integers(1, 30)), replace=False).tolist())
+            for _ in range(800)]
+    sets += [list(s) for s in sets[:200]]  # duplicates -> qualifying pairs
+    # the reference's collection order (collection.hpp:115-119), plus empty sets first
+    sets = [[], []] + sorted(sets, key=lambda x: (len(x), x))
+    base = ssj.Collection.from_sets(sets)
+    for shift in (0, 1 << 28):
+        toks = (base.tokens.astype(np.uint64) + shift).astype(np.uint32)
+        coll = ssj.Collection(toks, base.offsets, base.original_id)
+        pred = ssj.jaccard(3, 5)
+        for alg in (0, 1):
+            host, _ = ssj.generate_candidates(coll, pred, ssj.Algorithm(alg), threads=1)
+            with engine(ssj, coll, pred) as eng:
+                dev = eng.gpu_generate_candidates(alg)
+                assert np.array_equal(dev.C, host.C) and np.array_equal(dev.C_O, host.C_O)
+                empty = eng.gpu_generate_candidates(alg, 5, 5)
+                assert empty.C.size == 0 and empty.C_O.size == 0
+                eng.set_original_ids(coll.original_id)
+                pairs, rep = eng.gpu_join(alg, max_chunk_candidates=2000)
+            ref = ssj.run_join(coll, pred, ssj.PipelineConfig(algorithm=ssj.Algorithm(alg),
+                                                              mode=ssj.OutputMode.Pairs))
+            assert np.array_equal(pairs, ssj.sorted_pairs(ref.pairs).reshape(-1, 2))
+    one = ssj.Collection.from_sets([[1, 2, 3]])
+    with engine(ssj, one, ssj.jaccard(1, 2)) as eng:
+        pairs, rep = eng.gpu_join(0)
+        assert pairs.shape == (0, 2) and rep["count"] == 0 and rep["candidate_count"] == 0
+
+
+def test_gpu_join_requires_reference_order(ssj, gpu):
+    """The generators rely on the preprocessed (size, lex) order like the reference's
+    (collection.hpp:115-119); an unordered collection is rejected, not joined wrongly."""
+    coll = ssj.Collection.from_sets([[1, 2, 3, 4], [1, 2]])
+    with engine(ssj, coll, ssj.jaccard(1, 2)) as eng:
+        with pytest.raises(ValueError):
+            eng.gpu_join(0)
