@@ -95,6 +95,9 @@ def test_gpu_join_matches_host_join(ssj, gpu, shape, thr):
             pairs, rep = eng.gpu_join(int(alg), max_chunk_candidates=max(host.C.size // 5, 1))
             assert rep["candidate_count"] == host.C.size
             assert rep["chunk_count"] >= 2 or host.C.size < 10
+            # count mode (no pair decoding) agrees
+            _, rep_c = eng.gpu_join(int(alg), pairs=False)
+            assert rep_c["count"] == len(pairs) == rep["count"]
         cfg = ssj.PipelineConfig(algorithm=alg, mode=ssj.OutputMode.Pairs)
         ref = ssj.run_join(coll, pred, cfg)
         want = ssj.sorted_pairs(ref.pairs)
