@@ -657,8 +657,9 @@ __device__ __forceinline__ bool bm_continue(const uint8_t* __restrict__ map,
             } else if (d >= nbits) {
                 i = m;
             } else {
-                const uint32_t w = __ldg(bits + (d >> 5));
-                i = __ldg(rank + (d >> 5)) + __popc(w & ((2u << (d & 31)) - 1u));
+                const uint32_t w = kMap ? bits[d >> 5] : __ldg(bits + (d >> 5));
+                const uint32_t rk = kMap ? rank[d >> 5] : __ldg(rank + (d >> 5));
+                i = rk + __popc(w & ((2u << (d & 31)) - 1u));
             }
             if (i - ov > slack_r || j - ov > slack_s) {
                 if (kFull) *ov_out = 0;
@@ -691,7 +692,9 @@ __device__ __forceinline__ bool warp_defer(const KParams& p, bool want, uint32_t
 template <int kOut, bool kStats, bool kMap, bool kPacked, bool kReg>
 __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
                                            const uint32_t* pos8, const uint32_t* nn,
-                                           const uint8_t* __restrict__ map, uint4* hd,
+                                           const uint8_t* __restrict__ map,
+                                           const uint32_t* __restrict__ bits,
+                                           const uint32_t* __restrict__ rank, uint4* hd,
                                            const uint32_t (&hr)[kRunItems][8],
                                            unsigned& count, unsigned& prunes,
                                            unsigned& verified) {
@@ -699,8 +702,6 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
     constexpr uint32_t T = kRunThreads, I = kRunItems;
     const uint32_t lane = threadIdx.x & 31, tid = threadIdx.x;
     const uint32_t m = R.rsize, lo = R.lo, nbits = R.nw * 32u;
-    const uint32_t* bits = p.bm_bits + R.bofs;
-    const uint32_t* rank = p.bm_rank + R.bofs;
     uint32_t nq = 0;
 #pragma unroll
     for (uint32_t q = 0; q < I; ++q) {
@@ -844,7 +845,8 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
     constexpr uint32_t NBS = kReg ? 1 : NB;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint4* const hbase = reinterpret_cast<uint4*>(rsh) + warp * (NBS * HB);  // [bufs][item][lane][half]
-    uint8_t* const s_map = reinterpret_cast<uint8_t*>(rsh + T * I * 8 * NBS);  // [2][kRunMapBytes]
+    // [2][kRunMapBuf]: probe byte map, then its bitmap words and ranks (for the exact bound)
+    uint8_t* const s_map = reinterpret_cast<uint8_t*>(rsh + T * I * 8 * NBS);
     const uint32_t nr = (uint32_t)min((uint64_t)*p.runs_n, p.runs_cap);
     // this CTA's runs: blocks blockIdx.x, blockIdx.x + G, ... of kRunBlock consecutive runs
     const uint32_t stride = (gridDim.x - 1) * kRunBlock;
@@ -957,7 +959,7 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
             if (use_map && R0.slice != map_slice) {
                 mb ^= 1u;
                 map_slice = R0.slice;
-                uint8_t* mp = s_map + mb * kRunMapBytes;
+                uint8_t* mp = s_map + mb * kRunMapBuf;
                 const uint32_t range = R0.nw * 32u;
                 const uint32_t* r = p.tokens + (size_t)R0.rpos8 * 8;
                 for (uint32_t u = tid; u * 16 <= range; u += T)
@@ -971,6 +973,12 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
 #else
                 for (uint32_t i = tid; i < R0.rsize; i += T) mp[__ldg(r + i) - R0.lo] = 1;
 #endif
+                // the probe's bitmap words and ranks (built by bitmap_kernel) for the bound
+                uint32_t* sb = reinterpret_cast<uint32_t*>(mp + kRunMapBytes);
+                for (uint32_t w = tid; w < R0.nw; w += T) {
+                    sb[w] = __ldg(p.bm_bits + R0.bofs + w);
+                    sb[kRunMapWords + w] = __ldg(p.bm_rank + R0.bofs + w);
+                }
                 __syncthreads();
             }
 
@@ -1008,10 +1016,15 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
                 }
             }
             if (use_map) {
-                run_bitmap<kOut, kStats, true, kPacked, kReg>(p, R0, pos8, nn, s_map + mb * kRunMapBytes,
-                                                              hd, hr, count, prunes, verified);
+                const uint8_t* mp = s_map + mb * kRunMapBuf;
+                const uint32_t* sb = reinterpret_cast<const uint32_t*>(mp + kRunMapBytes);
+                run_bitmap<kOut, kStats, true, kPacked, kReg>(p, R0, pos8, nn, mp, sb,
+                                                              sb + kRunMapWords, hd, hr, count,
+                                                              prunes, verified);
             } else if (R0.bofs != kNone) {
-                run_bitmap<kOut, kStats, false, kPacked, kReg>(p, R0, pos8, nn, nullptr, hd, hr,
+                run_bitmap<kOut, kStats, false, kPacked, kReg>(p, R0, pos8, nn, nullptr,
+                                                               p.bm_bits + R0.bofs,
+                                                               p.bm_rank + R0.bofs, hd, hr,
                                                                count, prunes, verified);
             } else {
                 run_merge<kOut, kStats, kPacked, kReg>(p, R0, pos8, nn, hd, count, prunes, verified);

@@ -55,7 +55,9 @@ constexpr uint32_t kRunItems = SSJB_RUN_ITEMS;          // slots per thread per 
 constexpr uint32_t kRun = kRunThreads * kRunItems;      // slots per run
 constexpr uint32_t kRunMinSlice = SSJB_RUN_MIN_SLICE;
 constexpr uint32_t kRunMapRange = 8160;                 // probe token range held as a byte map
-constexpr uint32_t kRunMapBytes = 8192;                 // per map buffer (range + empty entry)
+constexpr uint32_t kRunMapBytes = 8192;                 // byte map (range + empty entry)
+constexpr uint32_t kRunMapWords = kRunMapRange / 32 + 1;  // the probe's bitmap words / ranks
+constexpr uint32_t kRunMapBuf = kRunMapBytes + 2 * ((kRunMapWords + 3) & ~3u) * 4;
 constexpr int kRunMinBlocks = SSJB_RUN_MIN_BLOCKS;
 constexpr uint32_t kRunBlock = SSJB_RUN_BLOCK;          // consecutive runs per CTA turn
 // shared memory: two candidate-head buffers per warp [buf][item][lane] 32 bytes (the
@@ -65,7 +67,7 @@ constexpr uint32_t kRunBlock = SSJB_RUN_BLOCK;          // consecutive runs per 
 #endif
 constexpr uint32_t kRunHeadBufs = SSJB_RUN_HEAD_BUFS;  // 2: heads of run k+1 fetched during run k
 constexpr size_t kRunSmemBytes =
-    (size_t)kRunThreads * kRunItems * 32 * (kRunHeadBufs ? kRunHeadBufs : 1) + 2 * kRunMapBytes;
+    (size_t)kRunThreads * kRunItems * 32 * (kRunHeadBufs ? kRunHeadBufs : 1) + 2 * kRunMapBuf;
 
 struct RunDesc {
     uint32_t slice;  // slice index
