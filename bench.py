@@ -253,7 +253,8 @@ def gpu_join_shards(ssj, args, rank, world, local, dev):
     eng = ssj.VerificationEngine(coll, pred, ssj.OutputMode.Pairs,
                                  ssj.Strategy(ssj.StrategyKind.Auto, 32), device=local)
     eng.set_original_ids(coll.original_id)
-    eng.gpu_join(alg, pairs=False, shard=0, n_shards=max(world, 1) * 64)  # index build, warm-up
+    # warm-up: the same call (static index build, bounds and buffer allocations are cached)
+    eng.gpu_join(alg, pairs=True, pairs_cap=1 << 22, shard=rank, n_shards=world)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
