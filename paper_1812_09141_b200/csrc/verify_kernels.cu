@@ -1332,15 +1332,18 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                     bool decided = false;
                     met = false;
                     uint32_t a[U];
+                    const uint32_t* sl = s + lane;  // loads at sl + j + u*32: immediate offsets
 #pragma unroll
                     for (uint32_t u = 0; u < U; ++u)
-                        a[u] = u * 32 < width && u * 32 + lane < sn ? __ldg(s + u * 32 + lane) : 0xFFFFFFFFu;
+                        a[u] = u * 32 < width && u * 32 + lane < sn ? __ldg(sl + u * 32) : 0xFFFFFFFFu;
                     for (;;) {
                         const uint32_t jn = j + width;  // next step: [jn, jn + 32 * U)
+                        const int rem = (int)sn - (int)(jn + lane);  // tokens left for this lane
+                        const uint32_t* ps = sl + jn;
                         uint32_t nx[U];
 #pragma unroll
                         for (uint32_t u = 0; u < U; ++u)
-                            nx[u] = jn + u * 32 + lane < sn ? __ldg(s + jn + u * 32 + lane) : 0xFFFFFFFFu;
+                            nx[u] = (int)(u * 32) < rem ? __ldg(ps + u * 32) : 0xFFFFFFFFu;
                         uint32_t c = 0;
 #pragma unroll
                         for (uint32_t u = 0; u < U; ++u) {
