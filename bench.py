@@ -366,11 +366,18 @@ def main():
     import paper_1812_09141_b200 as ssj
 
     rank, world, local = dist_env()
+    # one GPU per rank; with fewer visible GPUs than ranks (a functional check of the
+    # multi-rank path on a single GPU) ranks share devices and use gloo instead of NCCL
+    ndev = max(torch.cuda.device_count(), 1)
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if ndev >= world:
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     synth_kw, pred_t, algorithm, desc = WORKLOADS[args.workload]
     t0 = time.perf_counter()
