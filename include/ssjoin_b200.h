@@ -280,7 +280,9 @@ typedef struct {
     ssj_strategy strategy;    /* default {Auto, 32} */
     uint32_t workers;         /* validated >= 1 like the reference; the grid replaces the pool */
     int32_t device;           /* CUDA device of the verification engine */
-    uint32_t filter_threads;  /* H0 generation threads; 1 = the reference's sequential loop */
+    uint32_t filter_threads;  /* H0 generation threads; 1 = the reference's sequential loop;
+                                 SSJ_FILTER_ON_GPU = generation on the engine's device
+                                 (AllPairs / PPJoin: the whole join runs as ssj_gpu_join) */
     uint32_t reserved;
     ssj_chunk_observer observer;
     void* observer_user;
@@ -306,6 +308,8 @@ typedef struct {
     double setup_ms;          /* ours: engine creation incl. the one-time collection upload
                                  (before join_ms starts, like pipeline.hpp:314) */
 } ssj_join_report;
+
+#define SSJ_FILTER_ON_GPU 0xFFFFFFFFu
 
 typedef struct ssj_join_result ssj_join_result;
 /* Fills the reference's PipelineConfig defaults. */

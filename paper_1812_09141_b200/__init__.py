@@ -13,7 +13,7 @@ from .collection import (KUNBOUNDED_BUDGET, CandidateChunk, ChunkBuilder, Collec
                          DecodedSlice, decode, preprocess_precoded)
 from .similarity import (SimilarityFunction, SimilarityPredicate, Threshold,
                          equivalent_overlap, jaccard)
-from .pipeline import (Algorithm, JoinReport, PhaseTimings, PipelineConfig, SynthConfig,
+from .pipeline import (FILTER_ON_GPU, Algorithm, JoinReport, PhaseTimings, PipelineConfig, SynthConfig,
                        generate_candidates, generate_candidates_windows, preprocess_precoded_native, run_join, sorted_pairs,
                        synth_collection, write_pairs)
 from .verify import (OutputMode, PinnedBuffer, Strategy, StrategyKind, VerificationEngine,

@@ -222,6 +222,46 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
     if (pairs_mode && (rc = ssj_engine_set_original_ids(engine.e, original_id))) return rc;
     report.setup_ms = ms_since(setup_start);
 
+    if (cfg->filter_threads == SSJ_FILTER_ON_GPU) {
+        // H0 on the device: candidates are generated, verified and decoded there
+        if (cfg->algorithm == SSJ_ALG_GROUPJOIN)
+            return ssjh::set_error(SSJ_ERR_INVALID_ARGUMENT,
+                                   "GPU filtering supports allpairs and ppjoin");
+        if (cfg->observer)
+            return ssjh::set_error(SSJ_ERR_INVALID_ARGUMENT,
+                                   "chunk_observer needs host chunks (GPU filtering keeps them on "
+                                   "the device)");
+        const auto join_start = Clock::now();
+        const uint64_t max_chunk = budget == UINT64_MAX ? 0 : std::max<uint64_t>(budget / 4, 1);
+        ssj_gpu_join_report gr{};
+        uint64_t n = 0;
+        std::vector<uint32_t> pairs;
+        if (pairs_mode) {
+            // a generous first capacity; rerun only when the result is larger
+            const uint64_t cap0 = std::max<uint64_t>(1u << 20, n_sets);
+            pairs.resize(2 * cap0);
+            rc = ssj_gpu_join(engine.e, cfg->algorithm, max_chunk, pairs.data(), cap0, &n, &gr);
+            if (rc && n > cap0) {
+                pairs.resize(2 * n);
+                rc = ssj_gpu_join(engine.e, cfg->algorithm, max_chunk, pairs.data(), n, &n, &gr);
+            }
+            if (rc) return rc;
+            pairs.resize(2 * n);
+        } else if ((rc = ssj_gpu_join(engine.e, cfg->algorithm, max_chunk, nullptr, 0, &n, &gr))) {
+            return rc;
+        }
+        report.count = gr.count;
+        report.candidate_count = gr.candidate_count;
+        report.chunk_count = gr.chunk_count;
+        report.filtering_ms = gr.index_ms + gr.filtering_ms;
+        report.verification_ms = gr.verification_ms;
+        result->pairs = std::move(pairs);
+        report.n_pairs = result->pairs.size() / 2;
+        report.join_ms = ms_since(join_start);
+        *out = result.release();
+        return SSJ_OK;
+    }
+
     ChunkPool pool(3);
     Handoff to_dispatcher;
     std::mutex h2_mutex;

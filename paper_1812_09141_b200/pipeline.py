@@ -19,6 +19,9 @@ from .similarity import SimilarityPredicate
 from .verify import OutputMode, Strategy, StrategyKind, VerificationOutput
 
 
+FILTER_ON_GPU = 0xFFFFFFFF  # PipelineConfig.filter_threads: generate candidates on the device
+
+
 class Algorithm(IntEnum):
     """pipeline.hpp:25"""
     AllPairs = 0
@@ -36,7 +39,7 @@ class PipelineConfig:
     workers: int = 1
     chunk_observer: Optional[Callable[[CandidateChunk, VerificationOutput], None]] = None
     device: int = 0
-    filter_threads: int = 1
+    filter_threads: int = 1  # FILTER_ON_GPU: candidate generation on the device too
 
 
 @dataclass

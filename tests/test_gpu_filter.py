@@ -160,3 +160,20 @@ def test_gpu_join_requires_reference_order(ssj, gpu):
     with engine(ssj, coll, ssj.jaccard(1, 2)) as eng:
         with pytest.raises(ValueError):
             eng.gpu_join(0)
+
+
+def test_run_join_with_gpu_filtering(ssj, gpu):
+    """run_join (the reference's driver interface) with filter_threads = FILTER_ON_GPU gives
+    the same report counts and pairs as with host filtering."""
+    coll = ssj.synth_collection(11, ssj.SynthConfig(**SHAPES[0][0]))
+    pred = ssj.jaccard(4, 5)
+    for alg in (ssj.Algorithm.AllPairs, ssj.Algorithm.PPJoin):
+        for mode in (ssj.OutputMode.Pairs, ssj.OutputMode.Count):
+            host = ssj.run_join(coll, pred, ssj.PipelineConfig(algorithm=alg, mode=mode))
+            dev = ssj.run_join(coll, pred, ssj.PipelineConfig(algorithm=alg, mode=mode,
+                                                              filter_threads=ssj.FILTER_ON_GPU))
+            assert dev.count == host.count and dev.candidate_count == host.candidate_count
+            assert np.array_equal(ssj.sorted_pairs(dev.pairs), ssj.sorted_pairs(host.pairs))
+    with pytest.raises(ValueError):
+        ssj.run_join(coll, pred, ssj.PipelineConfig(algorithm=ssj.Algorithm.GroupJoin,
+                                                    filter_threads=ssj.FILTER_ON_GPU))
