@@ -333,7 +333,8 @@ void ssj_join_result_free(ssj_join_result* r);
  * (joiners.hpp:47-102), returned in host buffers. *nC_out / *nCO_out receive the sizes;
  * SSJ_ERR_RUNTIME when a capacity is too small (sizes still reported). The collection must be
  * in the reference's preprocessed order (sizes non-decreasing, collection.hpp:115-119),
- * else SSJ_ERR_INVALID_ARGUMENT.
+ * else SSJ_ERR_INVALID_ARGUMENT. GroupJoin (whole collection only): its phase-1 stream
+ * (groupjoin_generate's sink batches, joiners.hpp:160-171).
  */
 int ssj_gpu_generate_candidates(ssj_engine* e, int32_t algorithm, uint32_t probe_begin,
                                 uint32_t probe_end, uint32_t* C_out, uint64_t C_cap,
@@ -343,6 +344,7 @@ int ssj_gpu_generate_candidates(ssj_engine* e, int32_t algorithm, uint32_t probe
 typedef struct {
     uint64_t count;            /* qualifying pairs */
     uint64_t candidate_count;  /* candidates generated and verified */
+    uint64_t intra_group_pairs; /* GroupJoin phase-2 pairs (the reference's host-verified pairs) */
     uint64_t chunk_count;      /* device-resident chunks */
     double index_ms;           /* one-time static index build (0 when cached) */
     double filtering_ms;       /* candidate generation (bounds + generate + compact) */
@@ -351,9 +353,10 @@ typedef struct {
 } ssj_gpu_join_report;
 
 /*
- * Self-join run entirely on the engine's device: candidate generation (AllPairs / PPJoin) in
- * probe blocks of at most max_chunk_candidates candidates (0 = 256M), each block verified in
- * place by the strategy-A kernels. Pairs mode (pairs_out != NULL): qualifying pairs as
+ * Self-join run entirely on the engine's device: candidate generation (AllPairs / PPJoin /
+ * GroupJoin) in probe (group) blocks of at most max_chunk_candidates candidate upper bound
+ * (0 = 256M), each block verified in place by the strategy-A kernels; GroupJoin's
+ * intra-group pairs (phase 2) are generated and verified on the device too. Pairs mode (pairs_out != NULL): qualifying pairs as
  * (max(orig), min(orig)) original ids (ssj_engine_set_original_ids; identity by default)
  * sorted like write_pairs (report.hpp:39-42); *n_pairs = their number (SSJ_ERR_RUNTIME when
  * pairs_cap is smaller). Count mode: pairs_out == NULL.
@@ -363,7 +366,8 @@ int ssj_gpu_join(ssj_engine* e, int32_t algorithm, uint64_t max_chunk_candidates
                  ssj_gpu_join_report* report);
 /* Shard `shard` of `n_shards` of the same join (multi-GPU: one engine per device, no
  * exchange step): the probes are cut into n_shards contiguous ranges of equal candidate
- * upper bound; the shards' pairs are disjoint and their union is ssj_gpu_join's. */
+ * upper bound; the shards' pairs are disjoint and their union is ssj_gpu_join's.
+ * GroupJoin runs as one shard. */
 int ssj_gpu_join_shard(ssj_engine* e, int32_t algorithm, uint32_t shard, uint32_t n_shards,
                        uint64_t max_chunk_candidates, uint32_t* pairs_out, uint64_t pairs_cap,
                        uint64_t* n_pairs, ssj_gpu_join_report* report);

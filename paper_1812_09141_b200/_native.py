@@ -70,6 +70,7 @@ class ssj_join_report(C.Structure):
 
 class ssj_gpu_join_report(C.Structure):
     _fields_ = [("count", C.c_uint64), ("candidate_count", C.c_uint64),
+                ("intra_group_pairs", C.c_uint64),
                 ("chunk_count", C.c_uint64), ("index_ms", C.c_double),
                 ("filtering_ms", C.c_double), ("verification_ms", C.c_double),
                 ("join_ms", C.c_double)]

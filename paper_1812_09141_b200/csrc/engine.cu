@@ -164,6 +164,8 @@ struct DevBuf {
 // Per-join scratch: per-probe bounds (scanned), block buffers.
 struct GenState {
     DevBuf bound, base, G, count, flag, obase, slot, C, CO, tmp;
+    DevBuf per, cand, coff;  // GroupJoin expansion
+    size_t gj_cap = 0, gjC_cap = 0, gjCO_cap = 0;
     size_t tmp_bytes = 0, G_cap = 0, C_cap = 0, blk_cap = 0;
     std::vector<unsigned long long> hbase;  // exclusive scan of the bounds, n + 1 entries
 };
@@ -185,6 +187,8 @@ struct ssj_engine {
     uint4* d_heads = nullptr;       // packed set heads (null: tokens too large to pack)
     ssjb::FilterIndex* fidx = nullptr;  // GPU candidate generation index (built on first use)
     GenState* gen = nullptr;            // its bounds and block buffers
+    ssjb::GroupIndex* gidx = nullptr;   // GroupJoin groups + representative index (first use)
+    GenState* gen_g = nullptr;          // GroupJoin: bounds over groups and block buffers
     uint32_t req_tab_n = 0;
     cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
     ChunkSlot slot[2];
@@ -857,6 +861,11 @@ void ssj_engine_destroy(ssj_engine* e) {
         delete e->fidx;
     }
     delete e->gen;
+    if (e->gidx) {
+        ssjb::group_index_free(e->gidx);
+        delete e->gidx;
+    }
+    delete e->gen_g;
     cudaFree(e->d_res_slots);
     cudaFree(e->d_res_ov);
     cudaFree(e->d_res_n);
@@ -1193,14 +1202,38 @@ int cub_run(GenState& g, F&& f, cudaStream_t st) {
     return SSJ_OK;
 }
 
+int ensure_group_index(ssj_engine* e, double* build_ms) {
+    if (build_ms) *build_ms = 0;
+    if (e->gidx) return SSJ_OK;
+    int rc;
+    if ((rc = ensure_filter_index(e, SSJ_ALG_PPJOIN, nullptr))) return rc;  // also checks the order
+    auto t0 = std::chrono::steady_clock::now();
+    e->gidx = new ssjb::GroupIndex;
+    cudaError_t err = ssjb::group_index_build(e->gidx, e->d_tokens, e->d_sets, e->n_sets, e->pred,
+                                              e->s_comp);
+    if (err != cudaSuccess) {
+        delete e->gidx;
+        e->gidx = nullptr;
+        return fail(SSJ_ERR_CUDA, std::string("GroupJoin index build: ") + cudaGetErrorString(err));
+    }
+    if (build_ms)
+        *build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return SSJ_OK;
+}
+
+int gen_bounds_ix(ssj_engine* e, const ssjb::FilterIndex& ix, uint32_t n, GenState& g);
+
 // Bounds of all probes and their exclusive scan (device + host copy).
 int gen_bounds(ssj_engine* e, GenState& g) {
-    const uint32_t n = e->n_sets;
+    return gen_bounds_ix(e, *e->fidx, e->n_sets, g);
+}
+
+int gen_bounds_ix(ssj_engine* e, const ssjb::FilterIndex& ix, uint32_t n, GenState& g) {
     cudaStream_t st = e->s_comp;
     int rc;
     if ((rc = g.bound.alloc((size_t)n * 8 + 8)) || (rc = g.base.alloc(((size_t)n + 1) * 8)))
         return rc;
-    SSJ_CK(ssjb::filter_bounds(*e->fidx, 0, n, g.bound.as<unsigned long long>(), st));
+    SSJ_CK(ssjb::filter_bounds(ix, 0, n, g.bound.as<unsigned long long>(), st));
     SSJ_CK(cudaMemsetAsync(g.base.p, 0, 8, st));
     if (n) {
         auto* in = g.bound.as<unsigned long long>();
@@ -1217,15 +1250,26 @@ int gen_bounds(ssj_engine* e, GenState& g) {
 }
 
 // Candidates of probes [a, b) as a compacted device chunk in g.C / g.CO.
+int gen_block_ix(ssj_engine* e, const ssjb::FilterIndex& ix, GenState& g, uint32_t a, uint32_t b,
+                 uint64_t* nC, uint64_t* nCO, bool compact);
 int gen_block(ssj_engine* e, GenState& g, uint32_t a, uint32_t b, uint64_t* nC, uint64_t* nCO) {
+    return gen_block_ix(e, *e->fidx, g, a, b, nC, nCO, true);
+}
+
+int gen_block_ix(ssj_engine* e, const ssjb::FilterIndex& ix, GenState& g, uint32_t a, uint32_t b,
+                 uint64_t* nC, uint64_t* nCO, bool compact) {
     cudaStream_t st = e->s_comp;
     const uint32_t np = b - a;
     const unsigned long long base0 = g.hbase[a];
     const uint64_t ub = g.hbase[b] - base0;
     int rc;
     if (ub > g.G_cap) {
-        if ((rc = g.G.alloc(ub * 4)) || (rc = g.C.alloc(ub * 4))) return rc;
-        g.G_cap = g.C_cap = ub;
+        if ((rc = g.G.alloc(ub * 4))) return rc;
+        g.G_cap = ub;
+    }
+    if (ub > g.C_cap) {
+        if ((rc = g.C.alloc(ub * 4))) return rc;
+        g.C_cap = ub;
     }
     if (np > g.blk_cap) {
         if ((rc = g.count.alloc((size_t)np * 8)) || (rc = g.flag.alloc((size_t)np * 4)) ||
@@ -1233,10 +1277,15 @@ int gen_block(ssj_engine* e, GenState& g, uint32_t a, uint32_t b, uint64_t* nC, 
             (rc = g.CO.alloc((size_t)np * 8)))
             return rc;
         g.blk_cap = np;
+        g.gjCO_cap = 2ull * np;
     }
     const auto* base = g.base.as<unsigned long long>() + a;
-    SSJ_CK(ssjb::filter_generate(*e->fidx, a, b, base, base0, g.G.as<uint32_t>(),
+    SSJ_CK(ssjb::filter_generate(ix, a, b, base, base0, g.G.as<uint32_t>(),
                                  g.count.as<unsigned long long>(), g.flag.as<uint32_t>(), st));
+    if (!compact) {  // GroupJoin: the matched lists stay in g.G / g.count (expanded later)
+        *nC = *nCO = 0;
+        return SSJ_OK;
+    }
     auto* cnt = g.count.as<unsigned long long>();
     auto* ob = g.obase.as<unsigned long long>();
     auto* fl = g.flag.as<uint32_t>();
@@ -1264,6 +1313,106 @@ int gen_block(ssj_engine* e, GenState& g, uint32_t a, uint32_t b, uint64_t* nC, 
     return SSJ_OK;
 }
 
+template <typename T>
+int ensure_buf(DevBuf& b, size_t& cap, uint64_t need) {
+    if (need <= cap && b.p) return SSJ_OK;
+    const uint64_t n = std::max<uint64_t>(need, cap + cap / 2);
+    int rc;
+    if ((rc = b.alloc(n * sizeof(T)))) return rc;
+    cap = n;
+    return SSJ_OK;
+}
+
+// GroupJoin phase 1 of groups [a, b) (joiners.hpp:144-171): matched groups of every group
+// (PPJoin over the representatives), expanded to member batches -> g.C / g.CO.
+int gj_phase1(ssj_engine* e, GenState& g, uint32_t a, uint32_t b, uint64_t* nC, uint64_t* nCO) {
+    const ssjb::GroupIndex& gi = *e->gidx;
+    cudaStream_t st = e->s_comp;
+    int rc;
+    uint64_t unused = 0;
+    if ((rc = gen_block_ix(e, gi.ix, g, a, b, &unused, &unused, false))) return rc;
+    const uint32_t np = b - a;
+    if ((rc = ensure_buf<unsigned long long>(g.per, g.gj_cap, np))) return rc;
+    if ((rc = g.cand.alloc((size_t)np * 8)) || (rc = g.coff.alloc((size_t)np * 8))) return rc;
+    const auto* base = g.base.as<unsigned long long>() + a;
+    const unsigned long long base0 = g.hbase[a];
+    auto* per = g.per.as<unsigned long long>();
+    auto* cand = g.cand.as<unsigned long long>();
+    auto* coff = g.coff.as<unsigned long long>();
+    auto* nbat = g.flag.as<uint32_t>();
+    auto* soff = g.slot.as<uint32_t>();
+    SSJ_CK(ssjb::group_sizes(gi, a, b, base, base0, g.G.as<uint32_t>(),
+                             g.count.as<unsigned long long>(), per, cand, nbat, st));
+    if ((rc = cub_run(g, [&](void* t, size_t& bb) {
+             return cub::DeviceScan::ExclusiveSum(t, bb, cand, coff, (int)np, st);
+         }, st)))
+        return rc;
+    if ((rc = cub_run(g, [&](void* t, size_t& bb) {
+             return cub::DeviceScan::ExclusiveSum(t, bb, nbat, soff, (int)np, st);
+         }, st)))
+        return rc;
+    unsigned long long lc = 0, lo = 0;
+    uint32_t ls = 0, lb = 0;
+    SSJ_CK(cudaMemcpyAsync(&lo, coff + np - 1, 8, cudaMemcpyDeviceToHost, st));
+    SSJ_CK(cudaMemcpyAsync(&lc, cand + np - 1, 8, cudaMemcpyDeviceToHost, st));
+    SSJ_CK(cudaMemcpyAsync(&ls, soff + np - 1, 4, cudaMemcpyDeviceToHost, st));
+    SSJ_CK(cudaMemcpyAsync(&lb, nbat + np - 1, 4, cudaMemcpyDeviceToHost, st));
+    SSJ_CK(cudaStreamSynchronize(st));
+    *nC = lo + lc;
+    *nCO = 2ull * (ls + lb);
+    if (*nC > 0xFFFFFFFFull) return fail(SSJ_ERR_INVALID_ARGUMENT, "group block exceeds u32 offsets");
+    if ((rc = ensure_buf<uint32_t>(g.C, g.C_cap, *nC)) ||
+        (rc = ensure_buf<uint32_t>(g.CO, g.gjCO_cap, *nCO)))
+        return rc;
+    SSJ_CK(ssjb::group_expand(gi, a, b, base, base0, g.G.as<uint32_t>(),
+                              g.count.as<unsigned long long>(), per, coff, soff,
+                              g.C.as<uint32_t>(), g.CO.as<uint32_t>(), st));
+    SSJ_CK(cudaStreamSynchronize(st));
+    return SSJ_OK;
+}
+
+// GroupJoin phase 2 of groups [a, b) (joiners.hpp:175-179): the pairs inside every group as a
+// chunk (probe first + i, candidates first .. first + i - 1) -> g.C / g.CO.
+int gj_phase2(ssj_engine* e, GenState& g, uint32_t a, uint32_t b, uint64_t* nC, uint64_t* nCO) {
+    const ssjb::GroupIndex& gi = *e->gidx;
+    cudaStream_t st = e->s_comp;
+    int rc;
+    const uint32_t np = b - a;
+    if ((rc = g.cand.alloc((size_t)np * 8)) || (rc = g.coff.alloc((size_t)np * 8)) ||
+        (rc = g.flag.alloc((size_t)np * 4)) || (rc = g.slot.alloc((size_t)np * 4)))
+        return rc;
+    g.blk_cap = 0;  // flag / slot were re-sized here
+    auto* cand = g.cand.as<unsigned long long>();
+    auto* coff = g.coff.as<unsigned long long>();
+    auto* islc = g.flag.as<uint32_t>();
+    auto* soff = g.slot.as<uint32_t>();
+    SSJ_CK(ssjb::group_intra_sizes(gi, a, b, cand, islc, st));
+    if ((rc = cub_run(g, [&](void* t, size_t& bb) {
+             return cub::DeviceScan::ExclusiveSum(t, bb, cand, coff, (int)np, st);
+         }, st)))
+        return rc;
+    if ((rc = cub_run(g, [&](void* t, size_t& bb) {
+             return cub::DeviceScan::ExclusiveSum(t, bb, islc, soff, (int)np, st);
+         }, st)))
+        return rc;
+    unsigned long long lc = 0, lo = 0;
+    uint32_t ls = 0, lb = 0;
+    SSJ_CK(cudaMemcpyAsync(&lo, coff + np - 1, 8, cudaMemcpyDeviceToHost, st));
+    SSJ_CK(cudaMemcpyAsync(&lc, cand + np - 1, 8, cudaMemcpyDeviceToHost, st));
+    SSJ_CK(cudaMemcpyAsync(&ls, soff + np - 1, 4, cudaMemcpyDeviceToHost, st));
+    SSJ_CK(cudaMemcpyAsync(&lb, islc + np - 1, 4, cudaMemcpyDeviceToHost, st));
+    SSJ_CK(cudaStreamSynchronize(st));
+    *nC = lo + lc;
+    *nCO = 2ull * (ls + lb);
+    if (*nC > 0xFFFFFFFFull) return fail(SSJ_ERR_INVALID_ARGUMENT, "intra-group pairs exceed u32 offsets");
+    if ((rc = ensure_buf<uint32_t>(g.C, g.C_cap, *nC)) ||
+        (rc = ensure_buf<uint32_t>(g.CO, g.gjCO_cap, *nCO)))
+        return rc;
+    SSJ_CK(ssjb::group_intra(gi, a, b, coff, soff, g.C.as<uint32_t>(), g.CO.as<uint32_t>(), st));
+    SSJ_CK(cudaStreamSynchronize(st));
+    return SSJ_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1275,15 +1424,30 @@ int ssj_gpu_generate_candidates(ssj_engine* e, int32_t algorithm, uint32_t probe
     if (!e || !nC_out || !nCO_out) return fail(SSJ_ERR_INVALID_ARGUMENT, "null argument");
     DeviceScope ds(e->device);
     int rc;
-    if ((rc = ensure_filter_index(e, algorithm, nullptr))) return rc;
     probe_end = std::min(probe_end, e->n_sets);
     *nC_out = *nCO_out = 0;
-    if (probe_begin >= probe_end) return SSJ_OK;
-    if (!e->gen) e->gen = new GenState;
-    GenState& g = *e->gen;
-    if (g.hbase.empty() && (rc = gen_bounds(e, g))) return rc;
     uint64_t nC = 0, nCO = 0;
-    if ((rc = gen_block(e, g, probe_begin, probe_end, &nC, &nCO))) return rc;
+    GenState* gp = nullptr;
+    if (algorithm == SSJ_ALG_GROUPJOIN) {
+        // phase 1 over all groups (the stream is per group; windows do not apply)
+        if (probe_begin != 0 || probe_end != e->n_sets)
+            return fail(SSJ_ERR_INVALID_ARGUMENT, "GroupJoin generation covers the whole collection");
+        if ((rc = ensure_group_index(e, nullptr))) return rc;
+        if (!e->gen_g) e->gen_g = new GenState;
+        gp = e->gen_g;
+        const uint32_t G = e->gidx->n_groups;
+        if (!G) return SSJ_OK;
+        if (gp->hbase.empty() && (rc = gen_bounds_ix(e, e->gidx->ix, G, *gp))) return rc;
+        if ((rc = gj_phase1(e, *gp, 0, G, &nC, &nCO))) return rc;
+    } else {
+        if ((rc = ensure_filter_index(e, algorithm, nullptr))) return rc;
+        if (probe_begin >= probe_end) return SSJ_OK;
+        if (!e->gen) e->gen = new GenState;
+        gp = e->gen;
+        if (gp->hbase.empty() && (rc = gen_bounds(e, *gp))) return rc;
+        if ((rc = gen_block(e, *gp, probe_begin, probe_end, &nC, &nCO))) return rc;
+    }
+    GenState& g = *gp;
     *nC_out = nC;
     *nCO_out = nCO;
     if (nC > C_cap || nCO > C_O_cap) return fail(SSJ_ERR_RUNTIME, "output capacity too small");
@@ -1309,7 +1473,12 @@ int ssj_gpu_join_shard(ssj_engine* e, int32_t algorithm, uint32_t shard, uint32_
     const auto t_start = std::chrono::steady_clock::now();
     ssj_gpu_join_report rep{};
     int rc;
-    if ((rc = ensure_filter_index(e, algorithm, &rep.index_ms))) return rc;
+    const bool groupjoin = algorithm == SSJ_ALG_GROUPJOIN;
+    if (groupjoin && n_shards != 1)
+        return fail(SSJ_ERR_INVALID_ARGUMENT, "GroupJoin on the GPU runs as one shard");
+    if ((rc = groupjoin ? ensure_group_index(e, &rep.index_ms)
+                        : ensure_filter_index(e, algorithm, &rep.index_ms)))
+        return rc;
     const bool want_pairs = pairs_out != nullptr;
     if (want_pairs && !e->d_oid && (rc = ssj_engine_set_original_ids(e, nullptr))) return rc;
     cudaStream_t st = e->s_comp;
@@ -1322,10 +1491,14 @@ int ssj_gpu_join_shard(ssj_engine* e, int32_t algorithm, uint32_t shard, uint32_
         }
     } evg{ev};
     const uint64_t cap = max_chunk_candidates ? max_chunk_candidates : (256ull << 20);
-    if (!e->gen) e->gen = new GenState;
-    GenState& g = *e->gen;
+    GenState*& gslot = groupjoin ? e->gen_g : e->gen;
+    if (!gslot) gslot = new GenState;
+    GenState& g = *gslot;
+    // units: probes (AllPairs / PPJoin) or groups (GroupJoin), filtered through `ix`
+    const ssjb::FilterIndex& ix = groupjoin ? e->gidx->ix : *e->fidx;
+    const uint32_t n_units = groupjoin ? e->gidx->n_groups : e->n_sets;
     SSJ_CK(cudaEventRecord(ev[0], st));
-    if (g.hbase.empty() && (rc = gen_bounds(e, g))) return rc;  // per engine: fixed collection
+    if (g.hbase.empty() && (rc = gen_bounds_ix(e, ix, n_units, g))) return rc;  // cached
     SSJ_CK(cudaEventRecord(ev[1], st));
     SSJ_CK(cudaEventSynchronize(ev[1]));
     float ms = 0;
@@ -1334,68 +1507,82 @@ int ssj_gpu_join_shard(ssj_engine* e, int32_t algorithm, uint32_t shard, uint32_
     DevBuf acc, keys_all;
     if ((rc = acc.alloc(SSJ_RESULT_WORDS * 8))) return rc;
     uint64_t keys_n = 0, keys_cap = 0;
-    // this shard's probes: equal shares of the total candidate upper bound
-    const uint64_t total = g.hbase[e->n_sets];
+    // verification of one device-resident chunk (g.C / g.CO), results appended
+    auto consume = [&](uint64_t nC, uint64_t nCO) -> int {
+        if (!nC) return SSJ_OK;
+        int r;
+        const int out = want_pairs ? ssjb::kOutResults : ssjb::kOutCount;
+        if ((r = verify_device(e, g.C.as<uint32_t>(), nC, g.CO.as<uint32_t>(), nCO, out, nullptr,
+                               acc.as<unsigned long long>(), st)))
+            return r;
+        unsigned long long words[SSJ_RESULT_WORDS];
+        SSJ_CK(cudaMemcpyAsync(words, acc.p, sizeof(words), cudaMemcpyDeviceToHost, st));
+        unsigned long long nres = 0;
+        if (want_pairs) SSJ_CK(cudaMemcpyAsync(&nres, e->d_res_n, 8, cudaMemcpyDeviceToHost, st));
+        SSJ_CK(cudaStreamSynchronize(st));
+        if ((r = decode_error(words[SSJ_RESULT_ERROR]))) return r;
+        rep.count += words[SSJ_RESULT_COUNT];
+        if (want_pairs && nres) {
+            if (keys_n + nres > keys_cap) {
+                DevBuf grown;
+                const uint64_t nc = std::max<uint64_t>(2 * keys_cap, keys_n + nres);
+                if ((r = grown.alloc(nc * 8))) return r;
+                if (keys_n)
+                    SSJ_CK(cudaMemcpyAsync(grown.p, keys_all.p, keys_n * 8, cudaMemcpyDeviceToDevice, st));
+                std::swap(grown.p, keys_all.p);
+                keys_cap = nc;
+            }
+            KParams p = base_params(*e);
+            p.C = g.C.as<uint32_t>();
+            p.nC = nC;
+            p.C_O = g.CO.as<uint32_t>();
+            p.n_slices = (uint32_t)(nCO / 2);
+            p.res_slots = e->d_res_slots;
+            SSJ_CK(ssjb::launch_pairs(p, e->d_oid, nres, keys_all.as<unsigned long long>() + keys_n, st));
+            keys_n += nres;
+        }
+        return SSJ_OK;
+    };
+    // this shard's units: equal shares of the total candidate upper bound
+    const uint64_t total = g.hbase[n_units];
     auto cut = [&](uint32_t k) -> uint32_t {
         if (k == 0) return 0;
-        if (k >= n_shards) return e->n_sets;
+        if (k >= n_shards) return n_units;
         const unsigned long long target = (unsigned long long)((u128_host)total * k / n_shards);
         return (uint32_t)(std::lower_bound(g.hbase.begin(), g.hbase.end(), target) - g.hbase.begin());
     };
-    const uint32_t p_begin = std::min(cut(shard), e->n_sets);
-    const uint32_t n = std::max(p_begin, std::min(cut(shard + 1), e->n_sets));
-    for (uint32_t a = p_begin; a < n;) {
-        // the longest probe block whose candidate upper bound fits the budget (>= 1 probe)
-        uint32_t b = (uint32_t)(std::upper_bound(g.hbase.begin() + a + 1, g.hbase.end(),
-                                                 g.hbase[a] + cap) - g.hbase.begin()) - 1;
-        if (b <= a) b = a + 1;
-        b = std::min(b, n);
-        uint64_t nC = 0, nCO = 0;
-        SSJ_CK(cudaEventRecord(ev[0], st));
-        if ((rc = gen_block(e, g, a, b, &nC, &nCO))) return rc;
-        SSJ_CK(cudaEventRecord(ev[1], st));
-        if (nC) {
-            const int out = want_pairs ? ssjb::kOutResults : ssjb::kOutCount;
-            if ((rc = verify_device(e, g.C.as<uint32_t>(), nC, g.CO.as<uint32_t>(), nCO, out,
-                                    nullptr, acc.as<unsigned long long>(), st)))
-                return rc;
-            unsigned long long words[SSJ_RESULT_WORDS];
-            SSJ_CK(cudaMemcpyAsync(words, acc.p, sizeof(words), cudaMemcpyDeviceToHost, st));
-            unsigned long long nres = 0;
-            if (want_pairs)
-                SSJ_CK(cudaMemcpyAsync(&nres, e->d_res_n, 8, cudaMemcpyDeviceToHost, st));
-            SSJ_CK(cudaStreamSynchronize(st));
-            if ((rc = decode_error(words[SSJ_RESULT_ERROR]))) return rc;
-            rep.count += words[SSJ_RESULT_COUNT];
-            if (want_pairs && nres) {
-                if (keys_n + nres > keys_cap) {
-                    DevBuf grown;
-                    const uint64_t nc = std::max<uint64_t>(2 * keys_cap, keys_n + nres);
-                    if ((rc = grown.alloc(nc * 8))) return rc;
-                    if (keys_n) SSJ_CK(cudaMemcpyAsync(grown.p, keys_all.p, keys_n * 8, cudaMemcpyDeviceToDevice, st));
-                    std::swap(grown.p, keys_all.p);
-                    keys_cap = nc;
-                }
-                KParams p = base_params(*e);
-                p.C = g.C.as<uint32_t>();
-                p.nC = nC;
-                p.C_O = g.CO.as<uint32_t>();
-                p.n_slices = (uint32_t)(nCO / 2);
-                p.res_slots = e->d_res_slots;
-                SSJ_CK(ssjb::launch_pairs(p, e->d_oid, nres,
-                                          keys_all.as<unsigned long long>() + keys_n, st));
-                keys_n += nres;
+    const uint32_t p_begin = std::min(cut(shard), n_units);
+    const uint32_t n = std::max(p_begin, std::min(cut(shard + 1), n_units));
+    for (int phase = 0; phase < (groupjoin ? 2 : 1); ++phase) {
+        for (uint32_t a = p_begin; a < n;) {
+            // the longest block whose candidate upper bound fits the budget (>= 1 unit); the
+            // intra-group phase takes all groups at once
+            uint32_t b = n;
+            if (phase == 0) {
+                b = (uint32_t)(std::upper_bound(g.hbase.begin() + a + 1, g.hbase.end(),
+                                                g.hbase[a] + cap) - g.hbase.begin()) - 1;
+                if (b <= a) b = a + 1;
+                b = std::min(b, n);
             }
+            uint64_t nC = 0, nCO = 0;
+            SSJ_CK(cudaEventRecord(ev[0], st));
+            if (!groupjoin) rc = gen_block(e, g, a, b, &nC, &nCO);
+            else if (phase == 0) rc = gj_phase1(e, g, a, b, &nC, &nCO);
+            else rc = gj_phase2(e, g, a, b, &nC, &nCO);
+            if (rc) return rc;
+            SSJ_CK(cudaEventRecord(ev[1], st));
+            if ((rc = consume(nC, nCO))) return rc;
+            SSJ_CK(cudaEventRecord(ev[2], st));
+            SSJ_CK(cudaEventSynchronize(ev[2]));
+            SSJ_CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+            rep.filtering_ms += ms;
+            SSJ_CK(cudaEventElapsedTime(&ms, ev[1], ev[2]));
+            rep.verification_ms += ms;
+            if (phase == 0) rep.candidate_count += nC;
+            else rep.intra_group_pairs += nC;  // GroupJoin phase 2 (joiners.hpp:175-179)
+            rep.chunk_count += nC ? 1 : 0;
+            a = b;
         }
-        SSJ_CK(cudaEventRecord(ev[2], st));
-        SSJ_CK(cudaEventSynchronize(ev[2]));
-        SSJ_CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
-        rep.filtering_ms += ms;
-        SSJ_CK(cudaEventElapsedTime(&ms, ev[1], ev[2]));
-        rep.verification_ms += ms;
-        rep.candidate_count += nC;
-        rep.chunk_count += nC ? 1 : 0;
-        a = b;
     }
     if (want_pairs) {
         *n_pairs = keys_n;

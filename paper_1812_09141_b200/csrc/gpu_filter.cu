@@ -425,3 +425,232 @@ cudaError_t filter_compact(uint32_t a, uint32_t b, const unsigned long long* d_b
 }
 
 }  // namespace ssjb
+
+// ---- GroupJoin -------------------------------------------------------------------------------
+namespace ssjb {
+
+namespace {
+
+__global__ void group_flags_kernel(const uint32_t* __restrict__ tokens, const uint2* __restrict__ sets,
+                                   uint32_t n, const PredDev pred, uint32_t* flag) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t f = 1;
+    if (i) {
+        const uint2 a = sets[i], b = sets[i - 1];
+        if (a.y == b.y) {
+            // equal sizes -> equal probe-prefix lengths; compare the prefixes (joiners.hpp:125-129)
+            const uint32_t P = a.y ? dev_prefix_lengths(pred, a.y).x : 0u;
+            const uint32_t* ta = tokens + (size_t)a.x * 8;
+            const uint32_t* tb = tokens + (size_t)b.x * 8;
+            uint32_t q = 0;
+            while (q < P && ta[q] == tb[q]) ++q;
+            f = q < P;
+        }
+    }
+    flag[i] = f;
+}
+
+__global__ void group_fill_kernel(const uint2* __restrict__ sets, uint32_t n, const uint32_t* flag,
+                                  const uint32_t* gid_incl, uint32_t* first, uint2* rep) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !flag[i]) return;
+    const uint32_t g = gid_incl[i] - 1;
+    first[g] = i;
+    rep[g] = sets[i];
+}
+
+__global__ void group_count_kernel(const uint32_t* first, uint32_t G, uint32_t n, uint32_t* count) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < G) count[g] = (g + 1 < G ? first[g + 1] : n) - first[g];
+}
+
+__global__ void group_sizes_kernel(const GroupIndex gi, uint32_t a, uint32_t b,
+                                   const unsigned long long* base, unsigned long long base0,
+                                   const uint32_t* M, const unsigned long long* mcnt,
+                                   unsigned long long* per, unsigned long long* cand,
+                                   uint32_t* nbat) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t k = w; k < (uint64_t)(b - a); k += nw) {
+        const uint32_t* m = M + (base[k] - base0);
+        const uint32_t nm = (uint32_t)mcnt[k];
+        unsigned long long S = 0;
+        for (uint32_t q = lane; q < nm; q += 32) S += gi.count[m[q]];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+        if (lane == 0) {
+            const uint32_t c = gi.count[a + k];
+            per[k] = S;
+            cand[k] = nm ? (unsigned long long)c * S : 0ull;
+            nbat[k] = nm ? c : 0u;
+        }
+    }
+}
+
+__global__ void group_expand_kernel(const GroupIndex gi, uint32_t a, uint32_t b,
+                                    const unsigned long long* base, unsigned long long base0,
+                                    const uint32_t* M, const unsigned long long* mcnt,
+                                    const unsigned long long* per, const unsigned long long* coff,
+                                    const uint32_t* soff, uint32_t* C, uint32_t* CO) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t k = w; k < (uint64_t)(b - a); k += nw) {
+        const uint32_t nm = (uint32_t)mcnt[k];
+        if (!nm) continue;
+        const uint32_t g = a + (uint32_t)k;
+        const uint32_t* m = M + (base[k] - base0);
+        const uint32_t c = gi.count[g], f = gi.first[g];
+        const unsigned long long S = per[k];
+        for (uint32_t mm = 0; mm < c; ++mm) {
+            const unsigned long long out0 = coff[k] + (unsigned long long)mm * S;
+            unsigned long long run = 0;
+            for (uint32_t q0 = 0; q0 < nm; q0 += 32) {
+                const uint32_t q = q0 + lane;
+                const uint32_t h = q < nm ? m[q] : 0u;
+                const uint32_t ch = q < nm ? gi.count[h] : 0u;
+                uint32_t incl = ch;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+                    if (lane >= (uint32_t)off) incl += v;
+                }
+                const uint32_t fh = q < nm ? gi.first[h] : 0u;
+                for (uint32_t j = 0; j < ch; ++j) C[out0 + run + incl - ch + j] = fh + j;
+                run += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            if (lane == 0) {
+                const size_t sl = (size_t)soff[k] + mm;
+                CO[2 * sl] = f + mm;
+                CO[2 * sl + 1] = (uint32_t)(out0 + S);
+            }
+        }
+    }
+}
+
+__global__ void group_intra_sizes_kernel(const GroupIndex gi, uint32_t a, uint32_t b,
+                                         unsigned long long* icand, uint32_t* islc) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= b - a) return;
+    const unsigned long long c = gi.count[a + k];
+    icand[k] = c * (c - 1) / 2;
+    islc[k] = c ? (uint32_t)(c - 1) : 0u;
+}
+
+__global__ void group_intra_kernel(const GroupIndex gi, uint32_t a, uint32_t b,
+                                   const unsigned long long* coff, const uint32_t* soff,
+                                   uint32_t* C, uint32_t* CO) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t k = w; k < (uint64_t)(b - a); k += nw) {
+        const uint32_t c = gi.count[a + k], f = gi.first[a + k];
+        for (uint32_t i = 1; i < c; ++i) {
+            const unsigned long long o = coff[k] + (unsigned long long)i * (i - 1) / 2;
+            for (uint32_t j = lane; j < i; j += 32) C[o + j] = f + j;
+            if (lane == 0) {
+                const size_t sl = (size_t)soff[k] + (i - 1);
+                CO[2 * sl] = f + i;
+                CO[2 * sl + 1] = (uint32_t)(o + i);
+            }
+        }
+    }
+}
+
+uint32_t warps_grid2(uint64_t items) {
+    const uint64_t warps = items < 148ull * 64 ? (items ? items : 1) : 148ull * 64;
+    return (uint32_t)((warps * 32 + 255) / 256);
+}
+
+}  // namespace
+
+cudaError_t group_index_build(GroupIndex* gi, const uint32_t* d_tokens, const uint2* d_sets,
+                              uint32_t n, const PredDev& pred, cudaStream_t st) {
+    group_index_free(gi);
+    if (!n) return cudaSuccess;
+    uint32_t *flag = nullptr, *incl = nullptr;
+    void* tmp = nullptr;
+    cudaError_t err = cudaSuccess;
+    auto ck = [&](cudaError_t e) {
+        if (err == cudaSuccess && e != cudaSuccess) err = e;
+        return err == cudaSuccess;
+    };
+    size_t tb = 0;
+    uint32_t G = 0;
+    const uint32_t g256 = (n + 255) / 256;
+    if (!ck(cudaMalloc(&flag, (size_t)n * 4)) || !ck(cudaMalloc(&incl, (size_t)n * 4))) goto done;
+    group_flags_kernel<<<g256, 256, 0, st>>>(d_tokens, d_sets, n, pred, flag);
+    if (!ck(cudaGetLastError())) goto done;
+    if (!ck(cub::DeviceScan::InclusiveSum(nullptr, tb, flag, incl, (int)n, st)) ||
+        !ck(cudaMalloc(&tmp, tb)) || !ck(cub::DeviceScan::InclusiveSum(tmp, tb, flag, incl, (int)n, st)) ||
+        !ck(cudaMemcpyAsync(&G, incl + n - 1, 4, cudaMemcpyDeviceToHost, st)) ||
+        !ck(cudaStreamSynchronize(st)))
+        goto done;
+    gi->n_groups = G;
+    if (!ck(cudaMalloc(&gi->first, (size_t)G * 4)) || !ck(cudaMalloc(&gi->count, (size_t)G * 4)) ||
+        !ck(cudaMalloc(&gi->rep, (size_t)G * sizeof(uint2))))
+        goto done;
+    group_fill_kernel<<<g256, 256, 0, st>>>(d_sets, n, flag, incl, gi->first, gi->rep);
+    group_count_kernel<<<(G + 255) / 256, 256, 0, st>>>(gi->first, G, n, gi->count);
+    if (!ck(cudaGetLastError())) goto done;
+    // PPJoin over the representatives (joiners.hpp:144-160)
+    if (!ck(filter_index_build(&gi->ix, d_tokens, gi->rep, G, pred, 1, st))) goto done;
+    gi->ix.heads = nullptr;  // head records are indexed by set, not by group
+done:
+    cudaFree(flag);
+    cudaFree(incl);
+    cudaFree(tmp);
+    if (err != cudaSuccess) group_index_free(gi);
+    return err;
+}
+
+void group_index_free(GroupIndex* gi) {
+    cudaFree(gi->first);
+    cudaFree(gi->count);
+    cudaFree(gi->rep);
+    gi->first = gi->count = nullptr;
+    gi->rep = nullptr;
+    gi->n_groups = 0;
+    filter_index_free(&gi->ix);
+}
+
+cudaError_t group_sizes(const GroupIndex& gi, uint32_t a, uint32_t b,
+                        const unsigned long long* d_base, unsigned long long base0,
+                        const uint32_t* d_M, const unsigned long long* d_mcnt,
+                        unsigned long long* d_per, unsigned long long* d_cand, uint32_t* d_nbat,
+                        cudaStream_t st) {
+    if (b <= a) return cudaSuccess;
+    group_sizes_kernel<<<warps_grid2(b - a), 256, 0, st>>>(gi, a, b, d_base, base0, d_M, d_mcnt,
+                                                            d_per, d_cand, d_nbat);
+    return cudaGetLastError();
+}
+
+cudaError_t group_expand(const GroupIndex& gi, uint32_t a, uint32_t b,
+                         const unsigned long long* d_base, unsigned long long base0,
+                         const uint32_t* d_M, const unsigned long long* d_mcnt,
+                         const unsigned long long* d_per, const unsigned long long* d_coff,
+                         const uint32_t* d_soff, uint32_t* d_C, uint32_t* d_CO, cudaStream_t st) {
+    if (b <= a) return cudaSuccess;
+    group_expand_kernel<<<warps_grid2(b - a), 256, 0, st>>>(gi, a, b, d_base, base0, d_M, d_mcnt,
+                                                             d_per, d_coff, d_soff, d_C, d_CO);
+    return cudaGetLastError();
+}
+
+cudaError_t group_intra_sizes(const GroupIndex& gi, uint32_t a, uint32_t b,
+                              unsigned long long* d_icand, uint32_t* d_islc, cudaStream_t st) {
+    if (b <= a) return cudaSuccess;
+    group_intra_sizes_kernel<<<(b - a + 255) / 256, 256, 0, st>>>(gi, a, b, d_icand, d_islc);
+    return cudaGetLastError();
+}
+
+cudaError_t group_intra(const GroupIndex& gi, uint32_t a, uint32_t b,
+                        const unsigned long long* d_coff, const uint32_t* d_soff,
+                        uint32_t* d_C, uint32_t* d_CO, cudaStream_t st) {
+    if (b <= a) return cudaSuccess;
+    group_intra_kernel<<<warps_grid2(b - a), 256, 0, st>>>(gi, a, b, d_coff, d_soff, d_C, d_CO);
+    return cudaGetLastError();
+}
+
+}  // namespace ssjb

@@ -67,3 +67,51 @@ cudaError_t filter_compact(uint32_t a, uint32_t b, const unsigned long long* d_b
                            uint32_t* d_outC, uint32_t* d_outCO, cudaStream_t st);
 
 }  // namespace ssjb
+
+namespace ssjb {
+
+// ---- GroupJoin (joiners.hpp:111-183) ---------------------------------------------------------
+// Groups: maximal runs of consecutive sets with equal size, equal probe-prefix length and
+// equal probe prefix (the collection order puts them next to each other). The reference
+// filters the groups' representatives like PPJoin and expands matched group pairs to member
+// pairs (phase 1); pairs inside a group (phase 2) are verified separately.
+struct GroupIndex {
+    uint32_t n_groups = 0;
+    uint32_t* first = nullptr;   // [n_groups] first member (the representative)
+    uint32_t* count = nullptr;   // [n_groups] members
+    uint2* rep = nullptr;        // [n_groups] the representative's {pos8, size}
+    FilterIndex ix;              // PPJoin index over the representatives
+};
+
+cudaError_t group_index_build(GroupIndex* gi, const uint32_t* d_tokens, const uint2* d_sets,
+                              uint32_t n_sets, const PredDev& pred, cudaStream_t st);
+void group_index_free(GroupIndex* gi);
+
+// Phase-1 sizes of groups [a, b) from their matched lists (d_M at d_base[k] - base0, d_mcnt[k]
+// groups each): d_per[k] = candidates per member (sum of the matched groups' sizes),
+// d_cand[k] = members * per (0 when nothing matched), d_nbat[k] = batches (members or 0).
+cudaError_t group_sizes(const GroupIndex& gi, uint32_t a, uint32_t b,
+                        const unsigned long long* d_base, unsigned long long base0,
+                        const uint32_t* d_M, const unsigned long long* d_mcnt,
+                        unsigned long long* d_per, unsigned long long* d_cand, uint32_t* d_nbat,
+                        cudaStream_t st);
+
+// Phase-1 stream of groups [a, b): every member of group g is a probe whose candidates are
+// the members of g's matched groups in matched order (joiners.hpp:160-170). d_coff / d_soff:
+// exclusive scans of d_cand / d_nbat.
+cudaError_t group_expand(const GroupIndex& gi, uint32_t a, uint32_t b,
+                         const unsigned long long* d_base, unsigned long long base0,
+                         const uint32_t* d_M, const unsigned long long* d_mcnt,
+                         const unsigned long long* d_per, const unsigned long long* d_coff,
+                         const uint32_t* d_soff, uint32_t* d_C, uint32_t* d_CO, cudaStream_t st);
+
+// Phase-2 chunk of groups [a, b) (joiners.hpp:175-179): probe first+i (i >= 1) with candidates
+// first..first+i-1. d_coff / d_soff: exclusive scans of c(c-1)/2 and c-1 per group.
+cudaError_t group_intra(const GroupIndex& gi, uint32_t a, uint32_t b,
+                        const unsigned long long* d_coff, const uint32_t* d_soff,
+                        uint32_t* d_C, uint32_t* d_CO, cudaStream_t st);
+// per group of [a, b): d_icand[k] = c(c-1)/2, d_islc[k] = c - 1 (c = members)
+cudaError_t group_intra_sizes(const GroupIndex& gi, uint32_t a, uint32_t b,
+                              unsigned long long* d_icand, uint32_t* d_islc, cudaStream_t st);
+
+}  // namespace ssjb

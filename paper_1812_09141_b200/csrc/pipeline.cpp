@@ -224,9 +224,6 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
 
     if (cfg->filter_threads == SSJ_FILTER_ON_GPU) {
         // H0 on the device: candidates are generated, verified and decoded there
-        if (cfg->algorithm == SSJ_ALG_GROUPJOIN)
-            return ssjh::set_error(SSJ_ERR_INVALID_ARGUMENT,
-                                   "GPU filtering supports allpairs and ppjoin");
         if (cfg->observer)
             return ssjh::set_error(SSJ_ERR_INVALID_ARGUMENT,
                                    "chunk_observer needs host chunks (GPU filtering keeps them on "
@@ -252,6 +249,7 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
         }
         report.count = gr.count;
         report.candidate_count = gr.candidate_count;
+        report.host_verified_pairs = gr.intra_group_pairs;
         report.chunk_count = gr.chunk_count;
         report.filtering_ms = gr.index_ms + gr.filtering_ms;
         report.verification_ms = gr.verification_ms;

@@ -32,13 +32,13 @@ def test_gpu_streams_match_reference(ssj, gpu, name):
         key = k[2:]
         fn, num, den = (int(x) for x in key.split("_")[:3])
         alg = int(key.split("_a")[1])
-        if alg == 2:  # GroupJoin stays on the host
-            continue
         pred = ssj.SimilarityPredicate(ssj.SimilarityFunction(fn), ssj.Threshold(num, den))
         with engine(ssj, coll, pred) as eng:
             chunk = eng.gpu_generate_candidates(alg)
             assert np.array_equal(chunk.C, g["C_" + key]), key
             assert np.array_equal(chunk.C_O, g["CO_" + key]), key
+            if alg == 2:  # GroupJoin: the stream is per group (no probe windows)
+                continue
             # any probe window is the matching piece of the stream
             n = coll.size()
             lo, hi = n // 3, 2 * n // 3
@@ -58,7 +58,7 @@ def test_gpu_join_matches_brute_force(ssj, gpu, oracle, name):
         fn, num, den = (int(x) for x in k[3:].split("_"))
         pred = ssj.SimilarityPredicate(ssj.SimilarityFunction(fn), ssj.Threshold(num, den))
         want = oracle.oracle_pairs(g["original_id"], np.asarray(g[k]).reshape(-1, 3))
-        for alg in (0, 1):
+        for alg in (0, 1, 2):
             with engine(ssj, coll, pred) as eng:
                 eng.set_original_ids(coll.original_id)
                 pairs, rep = eng.gpu_join(alg, max_chunk_candidates=1000)
@@ -86,14 +86,15 @@ def test_gpu_join_matches_host_join(ssj, gpu, shape, thr):
     several probe blocks) returns the host run_join's pairs."""
     coll = ssj.synth_collection(2024, ssj.SynthConfig(**shape))
     pred = ssj.jaccard(*thr)
-    for alg in (ssj.Algorithm.AllPairs, ssj.Algorithm.PPJoin):
-        host, _ = ssj.generate_candidates(coll, pred, alg)
+    for alg in (ssj.Algorithm.AllPairs, ssj.Algorithm.PPJoin, ssj.Algorithm.GroupJoin):
+        host, host_pairs = ssj.generate_candidates(coll, pred, alg)
         with engine(ssj, coll, pred) as eng:
             dev = eng.gpu_generate_candidates(int(alg))
             assert np.array_equal(dev.C, host.C) and np.array_equal(dev.C_O, host.C_O), alg
             eng.set_original_ids(coll.original_id)
             pairs, rep = eng.gpu_join(int(alg), max_chunk_candidates=max(host.C.size // 5, 1))
             assert rep["candidate_count"] == host.C.size
+            assert rep["intra_group_pairs"] == len(host_pairs.reshape(-1, 2))
             assert rep["chunk_count"] >= 2 or host.C.size < 10
             # count mode (no pair decoding) agrees
             _, rep_c = eng.gpu_join(int(alg), pairs=False)
@@ -119,6 +120,8 @@ def test_gpu_join_shards_partition_the_join(ssj, gpu):
         assert cands == rep["candidate_count"]
         got = ssj.sorted_pairs(np.concatenate(parts))
         assert np.array_equal(got, full)
+        with pytest.raises(ValueError):  # GroupJoin runs as one shard
+            eng.gpu_join(2, shard=0, n_shards=2)
 
 
 def test_gpu_generation_edge_cases(ssj, gpu):
@@ -167,13 +170,11 @@ def test_run_join_with_gpu_filtering(ssj, gpu):
     the same report counts and pairs as with host filtering."""
     coll = ssj.synth_collection(11, ssj.SynthConfig(**SHAPES[0][0]))
     pred = ssj.jaccard(4, 5)
-    for alg in (ssj.Algorithm.AllPairs, ssj.Algorithm.PPJoin):
+    for alg in (ssj.Algorithm.AllPairs, ssj.Algorithm.PPJoin, ssj.Algorithm.GroupJoin):
         for mode in (ssj.OutputMode.Pairs, ssj.OutputMode.Count):
             host = ssj.run_join(coll, pred, ssj.PipelineConfig(algorithm=alg, mode=mode))
             dev = ssj.run_join(coll, pred, ssj.PipelineConfig(algorithm=alg, mode=mode,
                                                               filter_threads=ssj.FILTER_ON_GPU))
             assert dev.count == host.count and dev.candidate_count == host.candidate_count
+            assert dev.host_verified_pairs == host.host_verified_pairs
             assert np.array_equal(ssj.sorted_pairs(dev.pairs), ssj.sorted_pairs(host.pairs))
-    with pytest.raises(ValueError):
-        ssj.run_join(coll, pred, ssj.PipelineConfig(algorithm=ssj.Algorithm.GroupJoin,
-                                                    filter_threads=ssj.FILTER_ON_GPU))
