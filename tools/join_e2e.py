@@ -31,12 +31,16 @@ def main():
     ap.add_argument("--budget", type=int, default=64 << 20)
     ap.add_argument("--seed", type=int, default=1812)
     ap.add_argument("--skip-reference", action="store_true")
+    ap.add_argument("--algorithm", default=None, choices=["allpairs", "ppjoin", "groupjoin"],
+                    help="override the workload's generator")
     args = ap.parse_args()
 
     synth_kw, pred_t, algorithm, desc = bench.WORKLOADS[args.workload]
+    algorithm = args.algorithm or algorithm
     coll = ssj.synth_collection(args.seed, ssj.SynthConfig(**synth_kw))
     pred = ssj.jaccard(*pred_t)
-    alg = ssj.Algorithm.AllPairs if algorithm == "allpairs" else ssj.Algorithm.PPJoin
+    alg = {"allpairs": ssj.Algorithm.AllPairs, "ppjoin": ssj.Algorithm.PPJoin,
+           "groupjoin": ssj.Algorithm.GroupJoin}[algorithm]
     mode = ssj.OutputMode.Pairs if args.mode == "pairs" else ssj.OutputMode.Count
     out = {"workload": desc, "n_sets": coll.size(), "threshold": f"{pred_t[0]}/{pred_t[1]}",
            "algorithm": algorithm, "mode": args.mode, "chunk_budget": args.budget}
@@ -92,7 +96,7 @@ def main():
             workers = R.L.ref_hardware_concurrency()
             t0 = time.perf_counter()
             rep, pairs, _ = R.run_join(h, 0, pred_t[0], pred_t[1], 1,
-                                       algorithm=0 if algorithm == "allpairs" else 1,
+                                       algorithm=int(alg),
                                        budget=args.budget, kind=0, group=1,
                                        pairs_mode=args.mode == "pairs", workers=workers)
             out["cpu_reference_join"] = {
