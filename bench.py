@@ -534,7 +534,7 @@ def main():
             "roofline": {
                 "bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                 "frac": achieved_gbs / peak, "traffic": ncu_traffic(args.workload),
-                "kernel": "strategy-A verification pass (runs_gen + run_kernel + warp_tile_kernel + long_kernel; run_kernel dominant)" if resolved.kind.name == "A" else
+                "kernel": "strategy-A verification pass (runs_gen + run_kernel + warp_tile_kernel + long_slice_kernel; run_kernel dominant)" if resolved.kind.name == "A" else
                           f"strategy {resolved.kind.name} kernel",
                 "algorithmic_bytes_per_launch": algo_bytes,
                 "kernel_ms_avg": kernel_avg_ms, "peak_source": peak_src,

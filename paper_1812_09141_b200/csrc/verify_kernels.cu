@@ -3,10 +3,15 @@
 // The reference verifies a chunk on a CPU worker pool under one of three work
 // assignments (verify.hpp:232-345, the paper's thread-allocation alternatives A/B/C,
 // PAPER.md:605-644). Here each becomes a grid:
-//   A  tile_kernel  : load-balanced thread-per-pair. The chunk's slot range is cut into
-//                     fixed tiles of kTile candidates (independent of slice lengths); a CTA
-//                     maps its slots to slices with a shared-memory search over the
-//                     tile's C_O entries and stages the tile's probe sets in shared memory.
+//   A  (= Auto) thread per pair, load-balanced independently of slice lengths:
+//      prep_kernel / bitmap_kernel : slice descriptors, tile index, probe bitmaps
+//      runs_gen_kernel   : slices with >= kRunMinSlice candidates -> runs, the rest -> tiles
+//      run_kernel        : runs; candidate head records by 256-bit loads, the probe as a
+//                          byte map in shared memory, first 8 tokens per thread and a
+//                          per-warp continuation queue (the headline kernel)
+//      warp_tile_kernel  : 64-slot warp tiles of short slices (shuffle slot -> slice search)
+//      long_slice_kernel : pairs longer than kLongPair, CTA per slice with the probe bitmap
+//                          and rank in shared memory, 128 tokens per warp step
 //   B  block_kernel : one CTA per probe slice (paper Alt B): the probe set is staged in
 //                     shared memory and the CTA's threads stride over the slice's
 //                     candidates, each running the sequential early-exit merge.
@@ -279,8 +284,8 @@ __device__ __forceinline__ bool verify_bitmap(const uint32_t* __restrict__ bits,
 // (C ids in one vector load, flags in one vector store). The slices of the warp tile (first
 // one from the prep kernel's index) are read one per lane; a slot's slice is found by a
 // 5-step shuffle binary search over those ends. Slice descriptors, probe bitmaps and probe
-// tokens are read through L1 (lanes of a tile share them). Long candidates are deferred to
-// long_kernel exactly as in tile_kernel.
+// tokens are read through L1 (lanes of a tile share them). Long candidates are left to
+// long_slice_kernel (their slice is marked).
 // The tile's loads that do not depend on other loads: the lane's C ids and the tile's first
 // and last slice (prefetched one tile ahead by warp_tile_kernel).
 struct TilePre {
@@ -420,7 +425,7 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
                         written = false;  // long_slice_kernel writes it
                     }
                     if (deferred) {
-                        // verdict, flag and stats come from long_kernel
+                        // verdict, flag and stats come from long_slice_kernel
                     } else if (req == 0) {
                         met = true;  // verify.hpp:57: no comparison, met = (0 >= 0)
                         if (kOut == kOutResults)
@@ -473,8 +478,8 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
 // (C ids in one vector load, flags in one vector store). The slices of the warp tile (first
 // one from the prep kernel's index) are read one per lane; a slot's slice is found by a
 // 5-step shuffle binary search over those ends. Slice descriptors, probe bitmaps and probe
-// tokens are read through L1 (lanes of a tile share them). Long candidates are deferred to
-// long_kernel. Persistent over the segment's short-tile list; slots of slices with
+// tokens are read through L1 (lanes of a tile share them). Long candidates are left to
+// long_slice_kernel. Persistent over the segment's short-tile list; slots of slices with
 // >= kRunMinSlice candidates are left to run_kernel.
 template <int kOut, bool kStats, bool kPacked>
 __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) warp_tile_kernel(const KParams p) {

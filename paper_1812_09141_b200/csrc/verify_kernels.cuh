@@ -25,7 +25,7 @@ constexpr int kTileMinBlocks = SSJB_TILE_MIN_BLOCKS;         // CTAs per SM (reg
 constexpr uint32_t kSliceBitmapMinCands = 64;  // slices this long get a probe bitmap per chunk
 constexpr uint32_t kMaxBitmapWords = 8192;     // probe token range cap (256K tokens)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
-constexpr uint32_t kLongPair = 256;            // candidates longer than this go to long_kernel
+constexpr uint32_t kLongPair = 256;            // candidates longer than this: long_slice_kernel
 
 // Strategy A, long slices ("runs"): a run is a piece of <= kRun consecutive slots of one
 // slice with >= kRunMinSlice candidates (slices are cut at the chunk-segment boundaries
@@ -146,7 +146,8 @@ cudaError_t launch_build_heads(const uint32_t* tokens, const uint2* sets, uint32
 // prep_kernel (+ bitmap_kernel when p.slices && p.bm_cap): validation, tile index, slice
 // descriptors and probe bitmaps. Returns the number of kernels launched through *launches.
 cudaError_t launch_prep(const KParams& p, cudaStream_t st, int* launches = nullptr);
-// Strategy A: tiles [tile_begin, tile_end)
+// Strategy A, first pass over tiles [tile_begin, tile_end) of the chunk: runs_gen_kernel,
+// run_kernel (long slices), warp_tile_kernel (short slices)
 cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_begin,
                          uint32_t tile_end, cudaStream_t st);
 // Strategy A, second pass: slices the first pass marked for long pairs, slots of tiles
