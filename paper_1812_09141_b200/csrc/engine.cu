@@ -385,8 +385,8 @@ int check_chunk_args(const ssj_engine* e, const uint32_t* C, uint64_t nC, const 
     if (nC && !C) return fail(SSJ_ERR_INVALID_ARGUMENT, "null C with nC > 0");
     if (nCO >= 2 && !C_O) return fail(SSJ_ERR_INVALID_ARGUMENT, "null C_O with nCO > 0");
     if (nCO / 2 > 0xFFFFFFFFull) return fail(SSJ_ERR_INVALID_ARGUMENT, "too many slices");
-    if (nC > (0xFFFFFFFFull * (uint64_t)ssjb::kTile))
-        return fail(SSJ_ERR_INVALID_ARGUMENT, "chunk too large");
+    if (nC > 0xFFFFFFFFull)  // C_O end offsets are u32 (chunk.hpp:20-28)
+        return fail(SSJ_ERR_INVALID_ARGUMENT, "chunk too large: C_O offsets are 32-bit");
     return SSJ_OK;
 }
 
