@@ -1209,8 +1209,8 @@ int ensure_group_index(ssj_engine* e, double* build_ms) {
     if ((rc = ensure_filter_index(e, SSJ_ALG_PPJOIN, nullptr))) return rc;  // also checks the order
     auto t0 = std::chrono::steady_clock::now();
     e->gidx = new ssjb::GroupIndex;
-    cudaError_t err = ssjb::group_index_build(e->gidx, e->d_tokens, e->d_sets, e->n_sets, e->pred,
-                                              e->s_comp);
+    cudaError_t err = ssjb::group_index_build(e->gidx, e->d_tokens, e->d_sets, e->d_heads, e->n_sets,
+                                              e->pred, e->s_comp);
     if (err != cudaSuccess) {
         delete e->gidx;
         e->gidx = nullptr;

@@ -37,15 +37,6 @@ __device__ __forceinline__ uint2 dev_prefix_lengths(const PredDev& p, uint32_t s
     return make_uint2(probe, index);
 }
 
-// filters.hpp:174-181 positional_filter with current_overlap = 1 (joiners.hpp:94).
-__device__ __forceinline__ bool dev_positional_keep(const PredDev& p, uint32_t size_r,
-                                                    uint32_t size_s, uint32_t pos_r,
-                                                    uint32_t pos_s) {
-    const uint64_t required = dev_required(p, size_r, size_s);
-    const uint64_t a = size_r - pos_r - 1, b = size_s - pos_s - 1;
-    return 1 + (a < b ? a : b) >= required;
-}
-
 __device__ __forceinline__ uint32_t set_size(const FilterIndex& ix, uint32_t s) {
     return __ldg(&ix.sets[s].y);
 }
@@ -143,6 +134,23 @@ __global__ void bounds_kernel(const FilterIndex ix, uint32_t a, uint32_t b,
 // searches, and s's first 8 tokens come from its packed head record in one 256-bit load.
 constexpr uint32_t kGenThreads = 256;
 constexpr uint32_t kGenRStage = 256;
+// Per-warp Bloom bitmap over the probe prefix r[0..P): a token of s below r[p] is in r[0..p)
+// iff it is in r at all (r is sorted), so one membership filter per probe serves every p and
+// the exact binary search only runs on a Bloom hit.
+constexpr uint32_t kGenBloomBits = 12;
+constexpr uint32_t kGenBloomWords = (1u << kGenBloomBits) / 32;
+
+__device__ __forceinline__ uint32_t bloom_hash(uint32_t v) {
+    return (v * 0x9E3779B1u) >> (32 - kGenBloomBits);
+}
+#ifndef SSJB_GEN_BLOOM
+#define SSJB_GEN_BLOOM 1
+#endif
+__device__ __forceinline__ bool bloom_hit(const uint32_t* __restrict__ bm, uint32_t v) {
+    if (!SSJB_GEN_BLOOM) return true;
+    const uint32_t h = bloom_hash(v);
+    return (bm[h >> 5] >> (h & 31)) & 1u;
+}
 
 __device__ __forceinline__ void ld8(const uint32_t* __restrict__ s, uint32_t t[8]) {
     asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -167,13 +175,71 @@ __device__ __forceinline__ bool in_r(const uint32_t* __restrict__ rs,
     return l < p && (l < kGenRStage ? rs[l] : __ldg(r + l)) == v;
 }
 
-__global__ void __launch_bounds__(kGenThreads, 4)
+// Keep posting q of probe r (size m) at prefix position p? *s_out = the posting's set.
+// Duplicate iff an index-prefix token of s below r[p] is in r (then it is in r[0..p), where s
+// was already emitted); PPJoin also applies the positional filter at this first match.
+__device__ __forceinline__ bool candidate_keep(const FilterIndex& ix, const uint32_t* __restrict__ rs,
+                                               const uint32_t* __restrict__ r,
+                                               const uint32_t* __restrict__ bm, uint32_t m,
+                                               uint32_t p, uint32_t q, bool positional,
+                                               uint32_t* s_out) {
+    const uint2 pe = __ldg(&ix.post[q]);
+    const uint32_t s = pe.x;
+    *s_out = s;
+    bool keep = true;
+    if (p && pe.y) {  // pe.y = position of r[p] in s: the tokens before it are < r[p]
+        uint32_t pos;
+        if (ix.heads) {
+            uint32_t hv[8];
+            ld8(reinterpret_cast<const uint32_t*>(ix.heads + 2 * (size_t)s), hv);
+            const uint32_t lim = min(pe.y, 8u);
+#pragma unroll
+            for (uint32_t u = 0; u < 8; ++u) {
+                const uint32_t v = hv[u] & kHeadTokenMask;
+                if (u < lim && keep && bloom_hit(bm, v) && in_r(rs, r, 0, p, v, &pos)) keep = false;
+            }
+            if (keep && pe.y > 8) {
+                const uint32_t* st = set_tokens(ix, s);
+                for (uint32_t u = 8; u < pe.y; ++u) {
+                    const uint32_t v = __ldg(st + u);
+                    if (bloom_hit(bm, v) && in_r(rs, r, 0, p, v, &pos)) {
+                        keep = false;
+                        break;
+                    }
+                }
+            }
+        } else {
+            const uint32_t* st = set_tokens(ix, s);
+            for (uint32_t u = 0; u < pe.y; ++u) {
+                const uint32_t v = __ldg(st + u);
+                if (bloom_hit(bm, v) && in_r(rs, r, 0, p, v, &pos)) {
+                    keep = false;
+                    break;
+                }
+            }
+        }
+    }
+    if (keep && positional) {
+        // filters.hpp:174-181 positional_filter with current_overlap = 1 (joiners.hpp:94)
+        const uint32_t ns = set_size(ix, s);
+        const uint64_t a = m - p - 1, b = ns - pe.y - 1;
+        keep = 1 + (a < b ? a : b) >= dev_required_fast(ix.pred, m, ns);
+    }
+    return keep;
+}
+
+#ifndef SSJB_GEN_MINB
+#define SSJB_GEN_MINB 4
+#endif
+__global__ void __launch_bounds__(kGenThreads, SSJB_GEN_MINB)
     generate_kernel(const FilterIndex ix, uint32_t a, uint32_t b, const unsigned long long* base,
                     unsigned long long base0, uint32_t* C, unsigned long long* count,
                     uint32_t* flag) {
     __shared__ uint32_t rstage[kGenThreads / 32][kGenRStage];
+    __shared__ uint32_t bloom[kGenThreads / 32][kGenBloomWords];
     const uint32_t lane = threadIdx.x & 31;
     uint32_t* const rs = rstage[threadIdx.x >> 5];
+    uint32_t* const bm = bloom[threadIdx.x >> 5];
     const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const bool positional = ix.algorithm == 1;
@@ -186,72 +252,36 @@ __global__ void __launch_bounds__(kGenThreads, 4)
             const uint32_t smin = first_set_of_size(ix, dev_size_lower_bound(ix.pred, m));
             const uint32_t* r = set_tokens(ix, i);
             __syncwarp();
-            for (uint32_t u = lane; u < min(P, kGenRStage); u += 32) rs[u] = __ldg(r + u);
+            for (uint32_t u = lane; u < kGenBloomWords; u += 32) bm[u] = 0;
+            __syncwarp();
+            for (uint32_t u = lane; u < P; u += 32) {
+                const uint32_t v = __ldg(r + u);
+                if (u < kGenRStage) rs[u] = v;
+                const uint32_t h = bloom_hash(v);
+                atomicOr(&bm[h >> 5], 1u << (h & 31));
+            }
             __syncwarp();
             uint32_t* out = C + (base[k] - base0);
             for (uint32_t p0 = 0; p0 < P; p0 += 32) {
                 // ranges of prefix positions p0 + lane
-                uint32_t my_lo = 0, my_hi = 0, my_t = 0;
+                uint32_t my_lo = 0, my_hi = 0;
                 if (p0 + lane < P) {
-                    my_t = __ldg(r + p0 + lane);
-                    if (my_t < ix.universe) {
-                        const uint32_t h0 = __ldg(ix.head + my_t), h1 = __ldg(ix.head + my_t + 1);
+                    const uint32_t t = __ldg(r + p0 + lane);
+                    if (t < ix.universe) {
+                        const uint32_t h0 = __ldg(ix.head + t), h1 = __ldg(ix.head + t + 1);
                         my_lo = posting_lower_bound(ix, h0, h1, smin);
                         my_hi = posting_lower_bound(ix, my_lo, h1, i);
                     }
                 }
                 const uint32_t pend = min(32u, P - p0);
                 for (uint32_t pl = 0; pl < pend; ++pl) {
-                    const uint32_t p = p0 + pl;
                     const uint32_t lo = __shfl_sync(0xffffffffu, my_lo, pl);
                     const uint32_t hi = __shfl_sync(0xffffffffu, my_hi, pl);
-                    const uint32_t t = __shfl_sync(0xffffffffu, my_t, pl);
                     for (uint32_t q0 = lo; q0 < hi; q0 += 32) {
                         const uint32_t q = q0 + lane;
                         bool keep = false;
                         uint32_t s = 0;
-                        if (q < hi) {
-                            const uint2 pe = __ldg(&ix.post[q]);
-                            s = pe.x;
-                            keep = true;
-                            // duplicate iff an index-prefix token v < t of s is in r[0..p)
-                            if (p && pe.y) {  // pe.y = position of t in s: tokens before it are < t
-                                uint32_t lo_r = 0, pos;
-                                if (ix.heads) {
-                                    uint32_t hv[8];
-                                    ld8(reinterpret_cast<const uint32_t*>(ix.heads + 2 * (size_t)s), hv);
-                                    const uint32_t lim = min(pe.y, 8u);
-#pragma unroll
-                                    for (uint32_t u = 0; u < 8; ++u) {
-                                        if (u < lim && keep) {
-                                            if (in_r(rs, r, lo_r, p, hv[u] & kHeadTokenMask, &pos)) keep = false;
-                                            lo_r = pos;
-                                        }
-                                    }
-                                    if (keep && pe.y > 8) {
-                                        const uint32_t* st = set_tokens(ix, s);
-                                        for (uint32_t u = 8; u < pe.y; ++u) {
-                                            if (in_r(rs, r, lo_r, p, __ldg(st + u), &pos)) {
-                                                keep = false;
-                                                break;
-                                            }
-                                            lo_r = pos;
-                                        }
-                                    }
-                                } else {
-                                    const uint32_t* st = set_tokens(ix, s);
-                                    for (uint32_t u = 0; u < pe.y; ++u) {
-                                        if (in_r(rs, r, lo_r, p, __ldg(st + u), &pos)) {
-                                            keep = false;
-                                            break;
-                                        }
-                                        lo_r = pos;
-                                    }
-                                }
-                            }
-                            if (keep && positional)
-                                keep = dev_positional_keep(ix.pred, m, set_size(ix, s), p, pe.y);
-                        }
+                        if (q < hi) keep = candidate_keep(ix, rs, r, bm, m, p0 + pl, q, positional, &s);
                         const unsigned km = __ballot_sync(0xffffffffu, keep);
                         if (keep) out[n_out + __popc(km & ((1u << lane) - 1u))] = s;
                         n_out += __popc(km);
@@ -460,6 +490,14 @@ __global__ void group_fill_kernel(const uint2* __restrict__ sets, uint32_t n, co
     rep[g] = sets[i];
 }
 
+__global__ void group_heads_kernel(const uint4* __restrict__ heads, const uint32_t* first,
+                                   uint32_t G, uint4* rep_heads) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
+    rep_heads[2 * (size_t)g] = heads[2 * (size_t)first[g]];
+    rep_heads[2 * (size_t)g + 1] = heads[2 * (size_t)first[g] + 1];
+}
+
 __global__ void group_count_kernel(const uint32_t* first, uint32_t G, uint32_t n, uint32_t* count) {
     const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g < G) count[g] = (g + 1 < G ? first[g + 1] : n) - first[g];
@@ -567,7 +605,8 @@ uint32_t warps_grid2(uint64_t items) {
 }  // namespace
 
 cudaError_t group_index_build(GroupIndex* gi, const uint32_t* d_tokens, const uint2* d_sets,
-                              uint32_t n, const PredDev& pred, cudaStream_t st) {
+                              const uint4* d_heads, uint32_t n, const PredDev& pred,
+                              cudaStream_t st) {
     group_index_free(gi);
     if (!n) return cudaSuccess;
     uint32_t *flag = nullptr, *incl = nullptr;
@@ -597,7 +636,13 @@ cudaError_t group_index_build(GroupIndex* gi, const uint32_t* d_tokens, const ui
     if (!ck(cudaGetLastError())) goto done;
     // PPJoin over the representatives (joiners.hpp:144-160)
     if (!ck(filter_index_build(&gi->ix, d_tokens, gi->rep, G, pred, 1, st))) goto done;
-    gi->ix.heads = nullptr;  // head records are indexed by set, not by group
+    gi->ix.heads = nullptr;
+    if (d_heads) {  // the representatives' head records, indexed by group like the index
+        if (!ck(cudaMalloc(&gi->rep_heads, (size_t)G * 2 * sizeof(uint4)))) goto done;
+        group_heads_kernel<<<(G + 255) / 256, 256, 0, st>>>(d_heads, gi->first, G, gi->rep_heads);
+        if (!ck(cudaGetLastError())) goto done;
+        gi->ix.heads = gi->rep_heads;
+    }
 done:
     cudaFree(flag);
     cudaFree(incl);
@@ -607,6 +652,8 @@ done:
 }
 
 void group_index_free(GroupIndex* gi) {
+    cudaFree(gi->rep_heads);
+    gi->rep_heads = nullptr;
     cudaFree(gi->first);
     cudaFree(gi->count);
     cudaFree(gi->rep);

@@ -80,11 +80,13 @@ struct GroupIndex {
     uint32_t* first = nullptr;   // [n_groups] first member (the representative)
     uint32_t* count = nullptr;   // [n_groups] members
     uint2* rep = nullptr;        // [n_groups] the representative's {pos8, size}
+    uint4* rep_heads = nullptr;  // [2 n_groups] the representative's head record (nullable)
     FilterIndex ix;              // PPJoin index over the representatives
 };
 
 cudaError_t group_index_build(GroupIndex* gi, const uint32_t* d_tokens, const uint2* d_sets,
-                              uint32_t n_sets, const PredDev& pred, cudaStream_t st);
+                              const uint4* d_heads, uint32_t n_sets, const PredDev& pred,
+                              cudaStream_t st);
 void group_index_free(GroupIndex* gi);
 
 // Phase-1 sizes of groups [a, b) from their matched lists (d_M at d_base[k] - base0, d_mcnt[k]
