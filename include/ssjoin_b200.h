@@ -99,9 +99,15 @@ int ssj_engine_create(ssj_engine** out, int device, const uint32_t* tokens,
                       const uint32_t* offsets, uint32_t n_sets, const ssj_predicate* pred,
                       int32_t mode, const ssj_strategy* strategy);
 
+/* The engine's padded layout: set i's tokens start at token 8 * pos8[i] (32-byte aligned),
+ * each set padded to a multiple of 8 tokens with 0xFFFFFFFF, and SSJ_TOKEN_TAIL_PAD
+ * 0xFFFFFFFF tokens after the last set (the kernels read whole steps past a set's end). */
+#define SSJ_TOKEN_TAIL_PAD 512
+
 /* Same, but the collection is already in this device's memory in the engine's padded
  * layout (produced by another engine: see ssj_engine_device_collection), e.g. after an
- * NCCL broadcast over NVLink. The engine does not take ownership. */
+ * NCCL broadcast over NVLink. The engine does not take ownership. n_padded_tokens must
+ * cover the last set plus SSJ_TOKEN_TAIL_PAD (checked). */
 int ssj_engine_create_from_device(ssj_engine** out, int device, const uint32_t* d_tokens,
                                   uint64_t n_padded_tokens, const uint32_t* d_sets /*2*n*/,
                                   uint32_t n_sets, uint64_t n_tokens_total,

@@ -729,8 +729,9 @@ int ssj_engine_create(ssj_engine** out, int device, const uint32_t* tokens, cons
     }
     e->strategy = resolve_strategy(*e, *strategy);
 
-    // Padded CSR: every set starts on a 32-byte boundary; 8 sentinel tokens at the end so
-    // that the kernels' speculative 32-byte read of any set position stays in bounds.
+    // Padded CSR: every set starts on a 32-byte boundary; SSJ_TOKEN_TAIL_PAD sentinel tokens
+    // at the end so that the kernels' speculative reads past a set's end (32-byte head reads,
+    // the long pass's next-step prefetch) stay in bounds.
     std::vector<uint2> sets(n_sets ? n_sets : 1);
     uint64_t pos = 0;
     for (uint32_t i = 0; i < n_sets; ++i) {
@@ -742,7 +743,7 @@ int ssj_engine_create(ssj_engine** out, int device, const uint32_t* tokens, cons
         delete e;
         return fail(SSJ_ERR_INVALID_ARGUMENT, "collection too large for u32 set positions");
     }
-    e->n_padded = pos + 8;
+    e->n_padded = pos + SSJ_TOKEN_TAIL_PAD;
     std::vector<uint32_t> padded(e->n_padded, 0xFFFFFFFFu);
     for (uint32_t i = 0; i < n_sets; ++i) {
         const uint32_t sz = offsets[i + 1] - offsets[i];
@@ -790,6 +791,17 @@ int ssj_engine_create_from_device(ssj_engine** out, int device, const uint32_t* 
     e->owns_collection = false;
     e->d_tokens = const_cast<uint32_t*>(d_tokens);
     e->d_sets = reinterpret_cast<uint2*>(const_cast<uint32_t*>(d_sets));
+    if (n_sets) {  // the last set (largest position) must be followed by the tail pad
+        uint2 last{};
+        if (cudaMemcpy(&last, e->d_sets + (n_sets - 1), sizeof(uint2), cudaMemcpyDeviceToHost) !=
+                cudaSuccess ||
+            (uint64_t)last.x * 8 + (((uint64_t)last.y + 7) & ~7ull) + SSJ_TOKEN_TAIL_PAD >
+                n_padded_tokens) {
+            delete e;
+            return fail(SSJ_ERR_INVALID_ARGUMENT,
+                        "device collection is not in the engine's padded layout (tail pad)");
+        }
+    }
     if ((rc = make_pred_dev(*pred, &e->pred))) {
         delete e;
         return rc;

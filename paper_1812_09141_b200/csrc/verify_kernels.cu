@@ -25,6 +25,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "verify_kernels.cuh"
+#include "../../include/ssjoin_b200.h"
 
 namespace ssjb {
 
@@ -1232,13 +1233,21 @@ constexpr uint32_t kLongThreads = SSJB_LONG_THREADS;
 #define SSJB_LONG_PER_LANE 4
 #endif
 constexpr uint32_t kLongPerLane = SSJB_LONG_PER_LANE;  // candidate tokens per lane per step
+#ifndef SSJB_LONG_V2
+#define SSJB_LONG_V2 1
+#endif
 
+__device__ __forceinline__ uint32_t ldg_nc_v(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
-constexpr size_t kLongSmemBytes = (size_t)(2 * kMaxBitmapWords + 4) * 4 + kLongThreads * 16 + 16;
+constexpr size_t kLongSmemBytes = (size_t)(2 * kMaxBitmapWords + 8) * 4 + kLongThreads * 16 + 16;
 
 template <int kOut, bool kStats>
 __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams p,
@@ -1246,8 +1255,8 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                                                                   const uint64_t seg_hi) {
     extern __shared__ __align__(16) uint32_t lsh[];
     uint32_t* const bits = lsh;                          // [kMaxBitmapWords + 1]
-    uint32_t* const rank = lsh + kMaxBitmapWords + 4;    // [kMaxBitmapWords]
-    uint4* const llist = reinterpret_cast<uint4*>(rank + kMaxBitmapWords);  // [kLongThreads]
+    uint32_t* const rank = lsh + kMaxBitmapWords + 4;    // [kMaxBitmapWords + 1]
+    uint4* const llist = reinterpret_cast<uint4*>(rank + kMaxBitmapWords + 4);  // [kLongThreads]
     uint32_t* const lcount = reinterpret_cast<uint32_t*>(llist + kLongThreads);
     const uint32_t bits_s = (uint32_t)__cvta_generic_to_shared(bits);
     const uint32_t rank_s = (uint32_t)__cvta_generic_to_shared(rank);
@@ -1288,6 +1297,7 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                 rank[w] = x;
                 x += __popc(bits[w]);
             }
+            if (tid == 0) rank[nw] = m;  // the guard word (tokens above the range): all of r
             __syncthreads();
         }
         // the slice's long pairs, kLongThreads slots at a time: compacted into a shared list,
@@ -1325,6 +1335,86 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                 bool met;
                 uint32_t ov = 0;
                 if (use_bm) {
+#if SSJB_LONG_V2
+                    // 32 * kLongPerLane candidate tokens per step (token j + u*32 + lane in
+                    // lane `lane`, coalesced); per-lane counts summed with one warp reduction.
+                    // Full steps run without per-token predicates: the next step's loads are
+                    // issued (volatile, so they are not sunk past the exits) before this
+                    // step's lookups, reading past |s| inside the padded CSR
+                    // (SSJ_TOKEN_TAIL_PAD); the last, partial step masks tokens past |s| to
+                    // 0xFFFFFFFF, which clamps onto the bitmap's zero guard word.
+                    constexpr uint32_t U = kLongPerLane;
+                    static_assert(2 * 32 * U <= SSJ_TOKEN_TAIL_PAD, "prefetch past the tail pad");
+                    const uint32_t slack_r = m - sreq, slack_s = sn - sreq;
+                    const uint32_t* sl = s + lane;
+                    uint32_t bs;  // bitmap base, opaque: kept in a register, not rematerialised
+                    asm volatile("mov.b32 %0, %1;" : "=r"(bs) : "r"(bits_s));
+                    const uint32_t rs = bs + (rank_s - bits_s);
+                    // one step at token j: lookups of cur, next step's loads into nxt, the
+                    // verdict checks; the r-side position after the step's last token (rank +
+                    // popc, verify.hpp:58) is computed by every lane for its own last token
+                    // from the word its lookup already read, and taken from lane 31
+                    uint32_t j = 0;
+                    auto step = [&](uint32_t (&cur)[U], uint32_t (&nxt)[U], bool last) -> bool {
+                        const uint32_t jn = j + 32 * U;
+                        if (!last) {
+#pragma unroll
+                            for (uint32_t u = 0; u < U; ++u) nxt[u] = ldg_nc_v(sl + jn + u * 32);
+                        }
+                        uint32_t c = 0, il = 0;
+#pragma unroll
+                        for (uint32_t u = 0; u < U; ++u) {
+                            const uint32_t e = min(cur[u] - lo, nbits);
+                            const uint32_t w = lds_u32(bs + ((e >> 5) << 2));
+                            c += (w >> (e & 31)) & 1u;
+                            if (u == U - 1 && !last)
+                                il = cur[u] < lo ? 0u
+                                                 : lds_u32(rs + ((e >> 5) << 2)) +
+                                                       __popc(w & ((2u << (e & 31)) - 1u));
+                        }
+                        ov += __reduce_add_sync(0xffffffffu, c);
+                        if (last || jn == sn) {
+                            met = ov >= sreq;
+                            return true;
+                        }
+                        if (kOut != kOutResults && ov >= sreq) {
+                            met = true;
+                            return true;
+                        }
+                        const uint32_t i = __shfl_sync(0xffffffffu, il, 31);
+                        if (ov < sreq && (i - ov > slack_r || jn - ov > slack_s)) return true;
+                        j = jn;
+                        return false;
+                    };
+                    uint32_t A[U], B[U];
+#pragma unroll
+                    for (uint32_t u = 0; u < U; ++u) A[u] = ldg_nc_v(sl + u * 32);
+                    met = false;
+                    bool done = false;
+                    for (;;) {  // full steps, ping-pong buffers
+                        if (j + 32 * U > sn) break;
+                        if (step(A, B, false)) {
+                            done = true;
+                            break;
+                        }
+                        if (j + 32 * U > sn) {
+#pragma unroll
+                            for (uint32_t u = 0; u < U; ++u) A[u] = B[u];
+                            break;
+                        }
+                        if (step(B, A, false)) {
+                            done = true;
+                            break;
+                        }
+                    }
+                    if (!done) {  // j < |s| < j + 32U: the last, partial step
+#pragma unroll
+                        for (uint32_t u = 0; u < U; ++u)
+                            if (j + u * 32 + lane >= sn) A[u] = 0xFFFFFFFFu;
+                        step(A, B, true);
+                    }
+                    if (!met) ov = 0;
+#else
                     // 32 * kLongPerLane candidate tokens per step (token j + u*32 + lane in
                     // lane `lane`, coalesced), the next step's in flight; tokens past |s| read
                     // as 0xFFFFFFFF and clamp onto the bitmap's zero word; per-lane counts are
@@ -1382,6 +1472,7 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                     }
                     if (!decided) met = ov >= sreq;
                     if (!met) ov = 0;
+#endif
                 } else {
                     met = path_pair<32, kOut == kOutResults>(r, m, s, sn, sreq, lane, 0xffffffffu, &ov);
                 }

@@ -11,9 +11,13 @@ from typing import List, Tuple
 import numpy as np
 
 
+TOKEN_TAIL_PAD = 512  # SSJ_TOKEN_TAIL_PAD (include/ssjoin_b200.h)
+
+
 def padded_layout(offsets: np.ndarray) -> Tuple[int, np.ndarray]:
     """The engine's device layout (engine.cu, ssj_engine_create): set i starts at token
-    8 * pos8[i] (32-byte aligned), padded to a multiple of 8 tokens, plus 8 sentinel tokens.
+    8 * pos8[i] (32-byte aligned), padded to a multiple of 8 tokens, plus TOKEN_TAIL_PAD
+    sentinel tokens.
     Returns (n_padded_tokens, sets) with sets = uint32[2n] of (pos8, size) pairs."""
     offsets = np.asarray(offsets, np.int64)
     sizes = np.diff(offsets)
@@ -22,7 +26,7 @@ def padded_layout(offsets: np.ndarray) -> Tuple[int, np.ndarray]:
     if sizes.size:
         pos[1:] = np.cumsum(padded)[:-1]
     sets = np.stack([pos // 8, sizes], 1).astype(np.uint32).reshape(-1)
-    return int(padded.sum()) + 8, sets
+    return int(padded.sum()) + TOKEN_TAIL_PAD, sets
 
 
 def padded_tokens(tokens: np.ndarray, offsets: np.ndarray) -> np.ndarray:

@@ -71,11 +71,11 @@ def test_two_rank_gloo_sharding_and_broadcast(tmp_path):
 
 
 def test_padded_layout_matches_definition(ssj):
-    from paper_1812_09141_b200.parallel import padded_layout, padded_tokens
+    from paper_1812_09141_b200.parallel import TOKEN_TAIL_PAD, padded_layout, padded_tokens
     coll = ssj.Collection.from_sets([[1, 2, 3], [], list(range(9)), [7]])
     n_pad, sets = padded_layout(coll.offsets)
     assert sets.tolist() == [0, 3, 1, 0, 1, 9, 3, 1]
-    assert n_pad == 8 + 0 + 16 + 8 + 8
+    assert n_pad == 8 + 0 + 16 + 8 + TOKEN_TAIL_PAD
     pt = padded_tokens(coll.tokens, coll.offsets)
     assert pt[:3].tolist() == [1, 2, 3] and pt[3] == 0xFFFFFFFF
     assert pt[8:17].tolist() == list(range(9)) and pt[24] == 7
