@@ -1237,9 +1237,20 @@ constexpr uint32_t kLongPerLane = SSJB_LONG_PER_LANE;  // candidate tokens per l
 #define SSJB_LONG_V2 1
 #endif
 
+// Next-step token loads of the long pass. ptxas sinks plain (.nc) loads below the step's exit
+// branches, next to their first use; a strong load keeps its place ahead of the lookups.
+#ifndef SSJB_LONG_LD
+#define SSJB_LONG_LD 2
+#endif
 __device__ __forceinline__ uint32_t ldg_nc_v(const uint32_t* p) {
     uint32_t v;
+#if SSJB_LONG_LD == 0
     asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+#elif SSJB_LONG_LD == 1
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+#else
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+#endif
     return v;
 }
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
