@@ -518,49 +518,72 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) warp_tile_kernel(co
 // >= kRunMinSlice candidates is cut into runs of kRun slots from its first slot inside the
 // segment (all emitted by the tile holding that slot); a tile holding any slot of a short
 // slice, or a slot past the last slice, goes to the short-tile list.
+#ifndef SSJB_RG_THREADS
+#define SSJB_RG_THREADS 256
+#endif
+constexpr uint32_t kRunsGenThreads = SSJB_RG_THREADS;  // a multiple of 32 (warp ballots)
+
 __global__ void runs_gen_kernel(const KParams p, const uint32_t tile_begin,
                                 const uint32_t tile_end) {
     const uint32_t t = tile_begin + blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= tile_end) return;
     const uint64_t slot0 = (uint64_t)t * kTile;
-    if (slot0 >= p.nC) return;
-    const uint64_t slot1 = min(slot0 + (uint64_t)kTile, p.nC);
-    const uint64_t seg0 = (uint64_t)tile_begin * kTile;
-    const uint64_t seg1 = min((uint64_t)tile_end * kTile, p.nC);
-    uint32_t e = __ldg(p.tile_first + t);
-    uint64_t b = e ? min((uint64_t)__ldg(p.C_O + 2 * (size_t)e - 1), p.nC) : 0;  // decode: begin = previous end
-    uint64_t covered = slot0;
     bool has_short = false;
-    for (; e < p.n_slices; ++e) {
-        if (b >= slot1) break;
-        const uint64_t end = min((uint64_t)__ldg(p.C_O + 2 * (size_t)e + 1), p.nC);
-        if (end > b && end > slot0) {
-            if (end - b >= kRunMinSlice) {
-                const uint64_t start = max(b, seg0);
-                if (start >= slot0 && start < slot1) {
-                    const uint64_t stop = min(end, seg1);
-                    const uint64_t nrun = (stop - start + kRun - 1) / kRun;
-                    const unsigned long long k = atomicAdd(p.runs_n, (unsigned long long)nrun);
-                    for (uint64_t i = 0; i < nrun && k + i < p.runs_cap; ++i) {
-                        RunDesc d;
-                        d.slice = e;
-                        d.begin = (uint32_t)(start + i * kRun);
-                        d.end = (uint32_t)min(start + (i + 1) * kRun, stop);
-                        d.pad = 0;
-                        p.runs[k + i] = d;
+    if (t < tile_end && slot0 < p.nC) {
+        const uint64_t slot1 = min(slot0 + (uint64_t)kTile, p.nC);
+        const uint64_t seg0 = (uint64_t)tile_begin * kTile;
+        const uint64_t seg1 = min((uint64_t)tile_end * kTile, p.nC);
+        // the tile's slices: tile_first[t] .. tile_first[t + 1] inclusive (the last one may
+        // start inside the tile); a known range, so the C_O loads are independent
+        const uint32_t e0 = __ldg(p.tile_first + t);
+        const uint32_t e1 = min(__ldg(p.tile_first + t + 1) + 1, p.n_slices);  // exclusive
+        uint64_t b = e0 ? min((uint64_t)__ldg(p.C_O + 2 * (size_t)e0 - 1), p.nC) : 0;  // decode: begin = previous end
+        uint64_t covered = slot0;
+        // the span's ends are loaded 8 at a time (independent loads), so a tile of many tiny
+        // slices costs a few memory round trips, not one per slice
+        for (uint32_t eb = e0; eb < e1; eb += 8) {
+            uint32_t en[8];
+#pragma unroll
+            for (uint32_t k = 0; k < 8; ++k)
+                en[k] = eb + k < e1 ? __ldg(p.C_O + 2 * (size_t)(eb + k) + 1) : 0u;
+#pragma unroll
+            for (uint32_t k = 0; k < 8; ++k) {
+                if (eb + k >= e1) break;
+                const uint32_t e = eb + k;
+                const uint64_t end = min((uint64_t)en[k], p.nC);
+                if (b < slot1 && end > b && end > slot0) {
+                    if (end - b >= kRunMinSlice) {
+                        const uint64_t start = max(b, seg0);
+                        if (start >= slot0 && start < slot1) {
+                            const uint64_t stop = min(end, seg1);
+                            const uint64_t nrun = (stop - start + kRun - 1) / kRun;
+                            const unsigned long long kk = atomicAdd(p.runs_n, (unsigned long long)nrun);
+                            for (uint64_t i = 0; i < nrun && kk + i < p.runs_cap; ++i) {
+                                RunDesc d;
+                                d.slice = e;
+                                d.begin = (uint32_t)(start + i * kRun);
+                                d.end = (uint32_t)min(start + (i + 1) * kRun, stop);
+                                d.pad = 0;
+                                p.runs[kk + i] = d;
+                            }
+                        }
+                    } else {
+                        has_short = true;
                     }
+                    covered = max(covered, end);
                 }
-            } else {
-                has_short = true;
+                b = max(b, end);
             }
-            covered = max(covered, end);
         }
-        b = max(b, end);
+        if (covered < slot1) has_short = true;  // slots past the last slice (flag 0)
     }
-    if (covered < slot1) has_short = true;  // slots past the last slice (flag 0)
-    if (has_short) {
-        const unsigned long long k = atomicAdd(p.short_n, 1ull);
-        if (k < p.short_cap) p.short_tiles[k] = t;
+    // short tiles: one atomic per warp
+    const unsigned m = __ballot_sync(0xffffffffu, has_short);
+    if (m) {
+        const uint32_t lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+        unsigned long long k = 0;
+        if (lane == leader) k = atomicAdd(p.short_n, (unsigned long long)__popc(m));
+        k = __shfl_sync(0xffffffffu, k, leader) + __popc(m & ((1u << lane) - 1u));
+        if (has_short && k < p.short_cap) p.short_tiles[k] = t;
     }
 }
 
@@ -1663,7 +1686,8 @@ cudaError_t launch_tiles_t(const KParams& p, uint32_t tile_begin, uint32_t tile_
                            cudaStream_t st) {
     const int sms = sm_count();
     const uint32_t nt = tile_end - tile_begin;
-    runs_gen_kernel<<<(nt + 255) / 256, 256, 0, st>>>(p, tile_begin, tile_end);
+    runs_gen_kernel<<<(nt + kRunsGenThreads - 1) / kRunsGenThreads, kRunsGenThreads, 0, st>>>(
+        p, tile_begin, tile_end);
     auto rk = p.heads ? run_kernel<kOut, kStats, true> : run_kernel<kOut, kStats, false>;
     static bool attr[2] = {false, false};  // per instantiation; the attribute is per function
     if (!attr[p.heads ? 1 : 0]) {
