@@ -107,4 +107,9 @@ def test_gpu_export_and_engine_from_device(ssj, gpu, oracle):
     ref = oracle.verify_chunk(coll.tokens, coll.offsets, chunk.C, chunk.C_O, oracle.pred(0, 7, 10))
     assert np.array_equal(a.flags, ref["flags"]) and np.array_equal(b.flags, ref["flags"])
     eng2.close()
+    # a device collection without the tail pad (the kernels read past a set's end) is refused
+    with pytest.raises(Exception, match="tail pad"):
+        ssj.VerificationEngine.from_device(d_tok.data_ptr(), n_pad - 1, d_sets.data_ptr(),
+                                           coll.size(), coll.tokens.size, pred,
+                                           ssj.OutputMode.Pairs, ssj.Strategy())
     eng.close()
