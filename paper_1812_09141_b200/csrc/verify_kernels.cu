@@ -22,6 +22,8 @@
 //                     the reference it walks the path in rounds of G*kHops hops and stops
 //                     as soon as the verdict is decided.
 // All three produce the reference's flags bit for bit (see ssj_device.cuh).
+#include <atomic>
+
 #include <cub/block/block_scan.cuh>
 
 #include "verify_kernels.cuh"
@@ -1681,6 +1683,20 @@ int sm_count() {
     return cached[dev];
 }
 
+// cudaFuncSetAttribute applies on the current device: set the dynamic shared memory limit
+// once per (kernel, device); `done` holds one bit per device id.
+template <typename K>
+cudaError_t ensure_smem_attr(K kernel, int bytes, std::atomic<uint64_t>& done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
+
 template <int kOut, bool kStats>
 cudaError_t launch_tiles_t(const KParams& p, uint32_t tile_begin, uint32_t tile_end,
                            cudaStream_t st) {
@@ -1689,11 +1705,9 @@ cudaError_t launch_tiles_t(const KParams& p, uint32_t tile_begin, uint32_t tile_
     runs_gen_kernel<<<(nt + kRunsGenThreads - 1) / kRunsGenThreads, kRunsGenThreads, 0, st>>>(
         p, tile_begin, tile_end);
     auto rk = p.heads ? run_kernel<kOut, kStats, true> : run_kernel<kOut, kStats, false>;
-    static bool attr[2] = {false, false};  // per instantiation; the attribute is per function
-    if (!attr[p.heads ? 1 : 0]) {
-        cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRunSmemBytes);
-        attr[p.heads ? 1 : 0] = true;
-    }
+    static std::atomic<uint64_t> attr[2];  // per instantiation and device
+    cudaError_t err = ensure_smem_attr(rk, (int)kRunSmemBytes, attr[p.heads ? 1 : 0]);
+    if (err != cudaSuccess) return err;
     rk<<<sms * kRunMinBlocks, kRunThreads, kRunSmemBytes, st>>>(p);
     if (p.heads)
         warp_tile_kernel<kOut, kStats, true><<<sms * kTileMinBlocks, kThreadsA, 0, st>>>(p);
@@ -1718,11 +1732,9 @@ cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_be
 template <int kOut, bool kStats>
 cudaError_t launch_long_t(const KParams& p, uint64_t seg_lo, uint64_t seg_hi, cudaStream_t st) {
     auto k = long_slice_kernel<kOut, kStats>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLongSmemBytes);
-        attr = true;
-    }
+    static std::atomic<uint64_t> attr;  // per device
+    cudaError_t err = ensure_smem_attr(k, (int)kLongSmemBytes, attr);
+    if (err != cudaSuccess) return err;
     k<<<sm_count() * (1024 / kLongThreads) * 2, kLongThreads, kLongSmemBytes, st>>>(p, seg_lo, seg_hi);
     return cudaGetLastError();
 }
