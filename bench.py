@@ -158,6 +158,11 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
+        # a timed region shorter than NVML's start-up still gets one sample (taken at its end,
+        # while the clocks are still those of the region)
+        deadline = time.time() + 2.0
+        while not self.samples and self._t and self._t.is_alive() and time.time() < deadline:
+            time.sleep(0.002)
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
