@@ -11,7 +11,7 @@ for W in ${WORKLOADS:-cfg1 cfg2 cfg3 cfg4}; do
     set -- $S
     timeout 600 python bench.py --workload $W --strategy $1 --group $2 --steps 5 --warmup 3 \
         --e2e-steps 1 --cpu-sample 2e6 --join-workload none > $OUT/st_${TAG}.json 2> $OUT/st_${TAG}.err
-    python - $W $1 $2 $TAG <<'PY' | tee -a gpurun_out/strategies_$4.jsonl
+    python - $W $1 $2 $TAG <<'PY' | tee -a $OUT/strategies_$TAG.jsonl
 import json, sys
 w, s, g, t = sys.argv[1:]
 try:
