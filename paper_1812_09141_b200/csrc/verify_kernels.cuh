@@ -25,7 +25,10 @@ constexpr int kTileMinBlocks = SSJB_TILE_MIN_BLOCKS;         // CTAs per SM (reg
 constexpr uint32_t kSliceBitmapMinCands = 64;  // slices this long get a probe bitmap per chunk
 constexpr uint32_t kMaxBitmapWords = 8192;     // probe token range cap (256K tokens)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
-constexpr uint32_t kLongPair = 256;            // candidates longer than this: long_slice_kernel
+#ifndef SSJB_LONG_PAIR
+#define SSJB_LONG_PAIR 160
+#endif
+constexpr uint32_t kLongPair = SSJB_LONG_PAIR;  // candidates longer than this: long_slice_kernel
 
 // Strategy A, long slices ("runs"): a run is a piece of <= kRun consecutive slots of one
 // slice with >= kRunMinSlice candidates (slices are cut at the chunk-segment boundaries
