@@ -22,7 +22,10 @@ namespace ssjb {
 constexpr uint32_t kThreadsA = SSJB_TILE_THREADS;            // threads per CTA
 constexpr uint32_t kTile = 32 * SSJB_TILE_ITEMS;             // slots per warp tile
 constexpr int kTileMinBlocks = SSJB_TILE_MIN_BLOCKS;         // CTAs per SM (register cap)
-constexpr uint32_t kSliceBitmapMinCands = 64;  // slices this long get a probe bitmap per chunk
+#ifndef SSJB_BM_MIN_CANDS
+#define SSJB_BM_MIN_CANDS 64
+#endif
+constexpr uint32_t kSliceBitmapMinCands = SSJB_BM_MIN_CANDS;  // slices this long get a probe bitmap per chunk
 constexpr uint32_t kMaxBitmapWords = 8192;     // probe token range cap (256K tokens)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 #ifndef SSJB_LONG_PAIR
