@@ -134,21 +134,21 @@ __global__ void bounds_kernel(const FilterIndex ix, uint32_t a, uint32_t b,
 // searches, and s's first 8 tokens come from its packed head record in one 256-bit load.
 constexpr uint32_t kGenThreads = 256;
 constexpr uint32_t kGenRStage = 256;
-// Per-warp Bloom bitmap over the probe prefix r[0..P): a token of s below r[p] is in r[0..p)
-// iff it is in r at all (r is sorted), so one membership filter per probe serves every p and
-// the exact binary search only runs on a Bloom hit.
-constexpr uint32_t kGenBloomBits = 12;
-constexpr uint32_t kGenBloomWords = (1u << kGenBloomBits) / 32;
+// Per-warp membership filter over the probe prefix r[0..P): a token of s below r[p] is in
+// r[0..p) iff it is in r at all (r is sorted), so one filter per probe serves every p.
+// Exact mode (the prefix's token range fits kGenFilterWords - 1 words): bit v - lo, tokens
+// outside the range clamp onto a zero guard word -- a hit is a member. Otherwise a Bloom
+// filter (hashed bits) screens the exact binary search.
+constexpr uint32_t kGenFilterBits = 13;
+constexpr uint32_t kGenFilterWords = (1u << kGenFilterBits) / 32;
 
 __device__ __forceinline__ uint32_t bloom_hash(uint32_t v) {
-    return (v * 0x9E3779B1u) >> (32 - kGenBloomBits);
+    return (v * 0x9E3779B1u) >> (32 - kGenFilterBits);
 }
-#ifndef SSJB_GEN_BLOOM
-#define SSJB_GEN_BLOOM 1
-#endif
-__device__ __forceinline__ bool bloom_hit(const uint32_t* __restrict__ bm, uint32_t v) {
-    if (!SSJB_GEN_BLOOM) return true;
-    const uint32_t h = bloom_hash(v);
+template <bool kExact>
+__device__ __forceinline__ bool filter_hit(const uint32_t* __restrict__ bm, uint32_t v,
+                                           uint32_t lo, uint32_t nbits) {
+    const uint32_t h = kExact ? min(v - lo, nbits) : bloom_hash(v);
     return (bm[h >> 5] >> (h & 31)) & 1u;
 }
 
@@ -178,17 +178,22 @@ __device__ __forceinline__ bool in_r(const uint32_t* __restrict__ rs,
 // Keep posting q of probe r (size m) at prefix position p? *s_out = the posting's set.
 // Duplicate iff an index-prefix token of s below r[p] is in r (then it is in r[0..p), where s
 // was already emitted); PPJoin also applies the positional filter at this first match.
+template <bool kExact>
 __device__ __forceinline__ bool candidate_keep(const FilterIndex& ix, const uint32_t* __restrict__ rs,
                                                const uint32_t* __restrict__ r,
-                                               const uint32_t* __restrict__ bm, uint32_t m,
-                                               uint32_t p, uint32_t q, bool positional,
-                                               uint32_t* s_out) {
+                                               const uint32_t* __restrict__ bm, uint32_t flo,
+                                               uint32_t fbits, uint32_t m, uint32_t p,
+                                               uint32_t q, bool positional, uint32_t* s_out) {
     const uint2 pe = __ldg(&ix.post[q]);
     const uint32_t s = pe.x;
     *s_out = s;
     bool keep = true;
-    if (p && pe.y) {  // pe.y = position of r[p] in s: the tokens before it are < r[p]
+    // member of r: exact filter hit, or Bloom hit confirmed by the binary search
+    auto member = [&](uint32_t v) {
         uint32_t pos;
+        return filter_hit<kExact>(bm, v, flo, fbits) && (kExact || in_r(rs, r, 0, p, v, &pos));
+    };
+    if (p && pe.y) {  // pe.y = position of r[p] in s: the tokens before it are < r[p]
         if (ix.heads) {
             uint32_t hv[8];
             ld8(reinterpret_cast<const uint32_t*>(ix.heads + 2 * (size_t)s), hv);
@@ -196,13 +201,12 @@ __device__ __forceinline__ bool candidate_keep(const FilterIndex& ix, const uint
 #pragma unroll
             for (uint32_t u = 0; u < 8; ++u) {
                 const uint32_t v = hv[u] & kHeadTokenMask;
-                if (u < lim && keep && bloom_hit(bm, v) && in_r(rs, r, 0, p, v, &pos)) keep = false;
+                if (u < lim && keep && member(v)) keep = false;
             }
             if (keep && pe.y > 8) {
                 const uint32_t* st = set_tokens(ix, s);
                 for (uint32_t u = 8; u < pe.y; ++u) {
-                    const uint32_t v = __ldg(st + u);
-                    if (bloom_hit(bm, v) && in_r(rs, r, 0, p, v, &pos)) {
+                    if (member(__ldg(st + u))) {
                         keep = false;
                         break;
                     }
@@ -211,8 +215,7 @@ __device__ __forceinline__ bool candidate_keep(const FilterIndex& ix, const uint
         } else {
             const uint32_t* st = set_tokens(ix, s);
             for (uint32_t u = 0; u < pe.y; ++u) {
-                const uint32_t v = __ldg(st + u);
-                if (bloom_hit(bm, v) && in_r(rs, r, 0, p, v, &pos)) {
+                if (member(__ldg(st + u))) {
                     keep = false;
                     break;
                 }
@@ -228,6 +231,9 @@ __device__ __forceinline__ bool candidate_keep(const FilterIndex& ix, const uint
     return keep;
 }
 
+#ifndef SSJB_GEN_EXACT
+#define SSJB_GEN_EXACT 1
+#endif
 #ifndef SSJB_GEN_MINB
 #define SSJB_GEN_MINB 4
 #endif
@@ -236,7 +242,7 @@ __global__ void __launch_bounds__(kGenThreads, SSJB_GEN_MINB)
                     unsigned long long base0, uint32_t* C, unsigned long long* count,
                     uint32_t* flag) {
     __shared__ uint32_t rstage[kGenThreads / 32][kGenRStage];
-    __shared__ uint32_t bloom[kGenThreads / 32][kGenBloomWords];
+    __shared__ uint32_t bloom[kGenThreads / 32][kGenFilterWords];
     const uint32_t lane = threadIdx.x & 31;
     uint32_t* const rs = rstage[threadIdx.x >> 5];
     uint32_t* const bm = bloom[threadIdx.x >> 5];
@@ -251,13 +257,18 @@ __global__ void __launch_bounds__(kGenThreads, SSJB_GEN_MINB)
             const uint32_t P = dev_prefix_lengths(ix.pred, m).x;
             const uint32_t smin = first_set_of_size(ix, dev_size_lower_bound(ix.pred, m));
             const uint32_t* r = set_tokens(ix, i);
+            // the prefix's token range decides the filter mode (warp-uniform)
+            const uint32_t flo = __ldg(r) & ~31u, fhi = __ldg(r + P - 1);
+            const uint32_t fnw = ((fhi - flo) >> 5) + 1;
+            const bool exact = SSJB_GEN_EXACT && fnw < kGenFilterWords;
+            const uint32_t fbits = fnw * 32u;
             __syncwarp();
-            for (uint32_t u = lane; u < kGenBloomWords; u += 32) bm[u] = 0;
+            for (uint32_t u = lane; u < (exact ? fnw + 1 : kGenFilterWords); u += 32) bm[u] = 0;
             __syncwarp();
             for (uint32_t u = lane; u < P; u += 32) {
                 const uint32_t v = __ldg(r + u);
                 if (u < kGenRStage) rs[u] = v;
-                const uint32_t h = bloom_hash(v);
+                const uint32_t h = exact ? v - flo : bloom_hash(v);
                 atomicOr(&bm[h >> 5], 1u << (h & 31));
             }
             __syncwarp();
@@ -281,7 +292,9 @@ __global__ void __launch_bounds__(kGenThreads, SSJB_GEN_MINB)
                         const uint32_t q = q0 + lane;
                         bool keep = false;
                         uint32_t s = 0;
-                        if (q < hi) keep = candidate_keep(ix, rs, r, bm, m, p0 + pl, q, positional, &s);
+                        if (q < hi)
+                            keep = exact ? candidate_keep<true>(ix, rs, r, bm, flo, fbits, m, p0 + pl, q, positional, &s)
+                                         : candidate_keep<false>(ix, rs, r, bm, flo, fbits, m, p0 + pl, q, positional, &s);
                         const unsigned km = __ballot_sync(0xffffffffu, keep);
                         if (keep) out[n_out + __popc(km & ((1u << lane) - 1u))] = s;
                         n_out += __popc(km);
