@@ -193,10 +193,14 @@ __device__ __forceinline__ bool candidate_keep(const FilterIndex& ix, const uint
         uint32_t pos;
         return filter_hit<kExact>(bm, v, flo, fbits) && (kExact || in_r(rs, r, 0, p, v, &pos));
     };
+    uint32_t ns = 0;  // |s| when the head record was read
     if (p && pe.y) {  // pe.y = position of r[p] in s: the tokens before it are < r[p]
         if (ix.heads) {
             uint32_t hv[8];
             ld8(reinterpret_cast<const uint32_t*>(ix.heads + 2 * (size_t)s), hv);
+            // pos8 / |s| from the record's top bytes (build_heads_kernel): no descriptor load
+            const uint32_t pos8 = __byte_perm(__byte_perm(hv[0], hv[1], 0x0073), __byte_perm(hv[2], hv[3], 0x0073), 0x5410);
+            ns = __byte_perm(__byte_perm(hv[4], hv[5], 0x0073), __byte_perm(hv[6], hv[7], 0x0073), 0x5410);
             const uint32_t lim = min(pe.y, 8u);
 #pragma unroll
             for (uint32_t u = 0; u < 8; ++u) {
@@ -204,7 +208,7 @@ __device__ __forceinline__ bool candidate_keep(const FilterIndex& ix, const uint
                 if (u < lim && keep && member(v)) keep = false;
             }
             if (keep && pe.y > 8) {
-                const uint32_t* st = set_tokens(ix, s);
+                const uint32_t* st = ix.tokens + (size_t)pos8 * 8;
                 for (uint32_t u = 8; u < pe.y; ++u) {
                     if (member(__ldg(st + u))) {
                         keep = false;
@@ -224,7 +228,7 @@ __device__ __forceinline__ bool candidate_keep(const FilterIndex& ix, const uint
     }
     if (keep && positional) {
         // filters.hpp:174-181 positional_filter with current_overlap = 1 (joiners.hpp:94)
-        const uint32_t ns = set_size(ix, s);
+        if (!ns) ns = set_size(ix, s);  // sets in an index are never empty
         const uint64_t a = m - p - 1, b = ns - pe.y - 1;
         keep = 1 + (a < b ? a : b) >= dev_required_fast(ix.pred, m, ns);
     }
