@@ -515,9 +515,13 @@ __global__ void group_heads_kernel(const uint4* __restrict__ heads, const uint32
     rep_heads[2 * (size_t)g + 1] = heads[2 * (size_t)first[g] + 1];
 }
 
-__global__ void group_count_kernel(const uint32_t* first, uint32_t G, uint32_t n, uint32_t* count) {
+__global__ void group_count_kernel(const uint32_t* first, uint32_t G, uint32_t n, uint32_t* count,
+                                   uint2* fc) {
     const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g < G) count[g] = (g + 1 < G ? first[g + 1] : n) - first[g];
+    if (g >= G) return;
+    const uint32_t c = (g + 1 < G ? first[g + 1] : n) - first[g];
+    count[g] = c;
+    fc[g] = make_uint2(first[g], c);
 }
 
 __global__ void group_sizes_kernel(const GroupIndex gi, uint32_t a, uint32_t b,
@@ -559,28 +563,28 @@ __global__ void group_expand_kernel(const GroupIndex gi, uint32_t a, uint32_t b,
         const uint32_t* m = M + (base[k] - base0);
         const uint32_t c = gi.count[g], f = gi.first[g];
         const unsigned long long S = per[k];
-        for (uint32_t mm = 0; mm < c; ++mm) {
-            const unsigned long long out0 = coff[k] + (unsigned long long)mm * S;
-            unsigned long long run = 0;
-            for (uint32_t q0 = 0; q0 < nm; q0 += 32) {
-                const uint32_t q = q0 + lane;
-                const uint32_t h = q < nm ? m[q] : 0u;
-                const uint32_t ch = q < nm ? gi.count[h] : 0u;
-                uint32_t incl = ch;
+        // the matched groups' members, 32 matched groups at a time: one {first, count}
+        // gather per matched group, written once per member of g (joiners.hpp:160-170)
+        unsigned long long run = 0;
+        for (uint32_t q0 = 0; q0 < nm; q0 += 32) {
+            const uint32_t q = q0 + lane;
+            const uint2 fh = q < nm ? gi.fc[m[q]] : make_uint2(0u, 0u);
+            uint32_t incl = fh.y;
 #pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
-                    if (lane >= (uint32_t)off) incl += v;
-                }
-                const uint32_t fh = q < nm ? gi.first[h] : 0u;
-                for (uint32_t j = 0; j < ch; ++j) C[out0 + run + incl - ch + j] = fh + j;
-                run += __shfl_sync(0xffffffffu, incl, 31);
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= (uint32_t)off) incl += v;
             }
-            if (lane == 0) {
-                const size_t sl = (size_t)soff[k] + mm;
-                CO[2 * sl] = f + mm;
-                CO[2 * sl + 1] = (uint32_t)(out0 + S);
+            for (uint32_t mm = 0; mm < c; ++mm) {
+                uint32_t* dst = C + coff[k] + (unsigned long long)mm * S + run + (incl - fh.y);
+                for (uint32_t j = 0; j < fh.y; ++j) dst[j] = fh.x + j;
             }
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        for (uint32_t mm = lane; mm < c; mm += 32) {
+            const size_t sl = (size_t)soff[k] + mm;
+            CO[2 * sl] = f + mm;
+            CO[2 * sl + 1] = (uint32_t)(coff[k] + (unsigned long long)mm * S + S);
         }
     }
 }
@@ -646,10 +650,11 @@ cudaError_t group_index_build(GroupIndex* gi, const uint32_t* d_tokens, const ui
         goto done;
     gi->n_groups = G;
     if (!ck(cudaMalloc(&gi->first, (size_t)G * 4)) || !ck(cudaMalloc(&gi->count, (size_t)G * 4)) ||
+        !ck(cudaMalloc(&gi->fc, (size_t)G * sizeof(uint2))) ||
         !ck(cudaMalloc(&gi->rep, (size_t)G * sizeof(uint2))))
         goto done;
     group_fill_kernel<<<g256, 256, 0, st>>>(d_sets, n, flag, incl, gi->first, gi->rep);
-    group_count_kernel<<<(G + 255) / 256, 256, 0, st>>>(gi->first, G, n, gi->count);
+    group_count_kernel<<<(G + 255) / 256, 256, 0, st>>>(gi->first, G, n, gi->count, gi->fc);
     if (!ck(cudaGetLastError())) goto done;
     // PPJoin over the representatives (joiners.hpp:144-160)
     if (!ck(filter_index_build(&gi->ix, d_tokens, gi->rep, G, pred, 1, st))) goto done;
@@ -673,6 +678,8 @@ void group_index_free(GroupIndex* gi) {
     gi->rep_heads = nullptr;
     cudaFree(gi->first);
     cudaFree(gi->count);
+    cudaFree(gi->fc);
+    gi->fc = nullptr;
     cudaFree(gi->rep);
     gi->first = gi->count = nullptr;
     gi->rep = nullptr;

@@ -79,6 +79,7 @@ struct GroupIndex {
     uint32_t n_groups = 0;
     uint32_t* first = nullptr;   // [n_groups] first member (the representative)
     uint32_t* count = nullptr;   // [n_groups] members
+    uint2* fc = nullptr;         // [n_groups] {first, count}: one gather per matched group
     uint2* rep = nullptr;        // [n_groups] the representative's {pos8, size}
     uint4* rep_heads = nullptr;  // [2 n_groups] the representative's head record (nullable)
     FilterIndex ix;              // PPJoin index over the representatives
