@@ -202,10 +202,18 @@ __device__ __forceinline__ bool candidate_keep(const FilterIndex& ix, const uint
             const uint32_t pos8 = __byte_perm(__byte_perm(hv[0], hv[1], 0x0073), __byte_perm(hv[2], hv[3], 0x0073), 0x5410);
             ns = __byte_perm(__byte_perm(hv[4], hv[5], 0x0073), __byte_perm(hv[6], hv[7], 0x0073), 0x5410);
             const uint32_t lim = min(pe.y, 8u);
+            if (kExact) {  // branch-free: all 8 lookups, hits below lim decide
+                uint32_t hit = 0;
 #pragma unroll
-            for (uint32_t u = 0; u < 8; ++u) {
-                const uint32_t v = hv[u] & kHeadTokenMask;
-                if (u < lim && keep && member(v)) keep = false;
+                for (uint32_t u = 0; u < 8; ++u)
+                    hit |= (uint32_t)filter_hit<true>(bm, hv[u] & kHeadTokenMask, flo, fbits) << u;
+                keep = (hit & ((1u << lim) - 1u)) == 0;
+            } else {
+#pragma unroll
+                for (uint32_t u = 0; u < 8; ++u) {
+                    const uint32_t v = hv[u] & kHeadTokenMask;
+                    if (u < lim && keep && member(v)) keep = false;
+                }
             }
             if (keep && pe.y > 8) {
                 const uint32_t* st = ix.tokens + (size_t)pos8 * 8;
