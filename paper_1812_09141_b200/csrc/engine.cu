@@ -164,8 +164,11 @@ struct DevBuf {
 // Per-join scratch: per-probe bounds (scanned), block buffers.
 struct GenState {
     DevBuf bound, base, G, count, flag, obase, slot, C, CO, tmp;
-    DevBuf per, cand, coff;  // GroupJoin expansion
-    size_t gj_cap = 0, gjC_cap = 0, gjCO_cap = 0;
+    DevBuf per, cand, coff, iflag, islot;  // GroupJoin expansion / intra-group chunk
+    DevBuf acc, keys, sorted;              // join result words; pair keys (pairs mode)
+    size_t keys_cap = 0, sorted_cap = 0;
+    size_t gj_cap = 0, gjC_cap = 0, gjCO_cap = 0, cand_cap = 0, coff_cap = 0, iflag_cap = 0,
+           islot_cap = 0;
     size_t tmp_bytes = 0, G_cap = 0, C_cap = 0, blk_cap = 0;
     std::vector<unsigned long long> hbase;  // exclusive scan of the bounds, n + 1 entries
 };
@@ -1344,8 +1347,10 @@ int gj_phase1(ssj_engine* e, GenState& g, uint32_t a, uint32_t b, uint64_t* nC, 
     uint64_t unused = 0;
     if ((rc = gen_block_ix(e, gi.ix, g, a, b, &unused, &unused, false))) return rc;
     const uint32_t np = b - a;
-    if ((rc = ensure_buf<unsigned long long>(g.per, g.gj_cap, np))) return rc;
-    if ((rc = g.cand.alloc((size_t)np * 8)) || (rc = g.coff.alloc((size_t)np * 8))) return rc;
+    if ((rc = ensure_buf<unsigned long long>(g.per, g.gj_cap, np)) ||
+        (rc = ensure_buf<unsigned long long>(g.cand, g.cand_cap, np)) ||
+        (rc = ensure_buf<unsigned long long>(g.coff, g.coff_cap, np)))
+        return rc;
     const auto* base = g.base.as<unsigned long long>() + a;
     const unsigned long long base0 = g.hbase[a];
     auto* per = g.per.as<unsigned long long>();
@@ -1390,14 +1395,16 @@ int gj_phase2(ssj_engine* e, GenState& g, uint32_t a, uint32_t b, uint64_t* nC, 
     cudaStream_t st = e->s_comp;
     int rc;
     const uint32_t np = b - a;
-    if ((rc = g.cand.alloc((size_t)np * 8)) || (rc = g.coff.alloc((size_t)np * 8)) ||
-        (rc = g.flag.alloc((size_t)np * 4)) || (rc = g.slot.alloc((size_t)np * 4)))
+    // scratch cached across calls (no cudaMalloc / cudaFree inside a warm join)
+    if ((rc = ensure_buf<unsigned long long>(g.cand, g.cand_cap, np)) ||
+        (rc = ensure_buf<unsigned long long>(g.coff, g.coff_cap, np)) ||
+        (rc = ensure_buf<uint32_t>(g.iflag, g.iflag_cap, np)) ||
+        (rc = ensure_buf<uint32_t>(g.islot, g.islot_cap, np)))
         return rc;
-    g.blk_cap = 0;  // flag / slot were re-sized here
     auto* cand = g.cand.as<unsigned long long>();
     auto* coff = g.coff.as<unsigned long long>();
-    auto* islc = g.flag.as<uint32_t>();
-    auto* soff = g.slot.as<uint32_t>();
+    auto* islc = g.iflag.as<uint32_t>();
+    auto* soff = g.islot.as<uint32_t>();
     SSJ_CK(ssjb::group_intra_sizes(gi, a, b, cand, islc, st));
     if ((rc = cub_run(g, [&](void* t, size_t& bb) {
              return cub::DeviceScan::ExclusiveSum(t, bb, cand, coff, (int)np, st);
@@ -1516,9 +1523,12 @@ int ssj_gpu_join_shard(ssj_engine* e, int32_t algorithm, uint32_t shard, uint32_
     float ms = 0;
     SSJ_CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
     rep.filtering_ms += ms;
-    DevBuf acc, keys_all;
-    if ((rc = acc.alloc(SSJ_RESULT_WORDS * 8))) return rc;
-    uint64_t keys_n = 0, keys_cap = 0;
+    // scratch cached on the engine: a warm join allocates nothing
+    if (!g.acc.p && (rc = g.acc.alloc(SSJ_RESULT_WORDS * 8))) return rc;
+    DevBuf& acc = g.acc;
+    DevBuf& keys_all = g.keys;
+    size_t& keys_cap = g.keys_cap;
+    uint64_t keys_n = 0;
     // verification of one device-resident chunk (g.C / g.CO), results appended
     auto consume = [&](uint64_t nC, uint64_t nCO) -> int {
         if (!nC) return SSJ_OK;
@@ -1600,8 +1610,8 @@ int ssj_gpu_join_shard(ssj_engine* e, int32_t algorithm, uint32_t shard, uint32_
         *n_pairs = keys_n;
         if (keys_n) {
             // write_pairs order (report.hpp:39-42): radix sort of the (r_id << 32 | s_id) keys
-            DevBuf sorted;
-            if ((rc = sorted.alloc(keys_n * 8))) return rc;
+            DevBuf& sorted = g.sorted;
+            if ((rc = ensure_buf<unsigned long long>(sorted, g.sorted_cap, keys_n))) return rc;
             auto* kin = keys_all.as<unsigned long long>();
             auto* kout = sorted.as<unsigned long long>();
             if ((rc = cub_run(g, [&](void* t, size_t& bb) {

@@ -208,11 +208,19 @@ __device__ __forceinline__ bool candidate_keep(const FilterIndex& ix, const uint
                 for (uint32_t u = 0; u < 8; ++u)
                     hit |= (uint32_t)filter_hit<true>(bm, hv[u] & kHeadTokenMask, flo, fbits) << u;
                 keep = (hit & ((1u << lim) - 1u)) == 0;
-            } else {
+            } else {  // Bloom: branch-free screen, then the exact search for the hits only
+                uint32_t hit = 0;
 #pragma unroll
-                for (uint32_t u = 0; u < 8; ++u) {
-                    const uint32_t v = hv[u] & kHeadTokenMask;
-                    if (u < lim && keep && member(v)) keep = false;
+                for (uint32_t u = 0; u < 8; ++u)
+                    hit |= (uint32_t)filter_hit<false>(bm, hv[u] & kHeadTokenMask, flo, fbits) << u;
+                hit &= (1u << lim) - 1u;
+                if (hit) {
+#pragma unroll
+                    for (uint32_t u = 0; u < 8; ++u) {
+                        uint32_t pos;
+                        if ((hit >> u & 1u) && keep && in_r(rs, r, 0, p, hv[u] & kHeadTokenMask, &pos))
+                            keep = false;
+                    }
                 }
             }
             if (keep && pe.y > 8) {
