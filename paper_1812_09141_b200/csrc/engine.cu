@@ -368,9 +368,11 @@ int ensure_tile_scratch(ssjb::SliceDesc** slices, size_t* capS, uint32_t** bits,
     return SSJ_OK;
 }
 
+// want_stats = false: the caller reports no VerifyStats (the all-GPU join), so the kernels
+// skip their per-pair stats accumulation.
 cudaError_t launch_strategy(const ssj_engine& e, const KParams& p, int out, uint32_t tile_begin,
-                            uint32_t tile_end, cudaStream_t st) {
-    const bool stats = e.strategy.kind != SSJ_STRATEGY_C;
+                            uint32_t tile_end, cudaStream_t st, bool want_stats = true) {
+    const bool stats = want_stats && e.strategy.kind != SSJ_STRATEGY_C;
     switch (e.strategy.kind) {
         case SSJ_STRATEGY_B: return ssjb::launch_block(p, out, stats, e.strategy.group_size, st);
         case SSJ_STRATEGY_C: return ssjb::launch_path(p, out, e.strategy.group_size, st);
@@ -1070,7 +1072,7 @@ namespace {
 // result buffers; e->d_res_n is zeroed here). d_acc: SSJ_RESULT_WORDS words.
 int verify_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, const uint32_t* d_C_O,
                   uint64_t nCO, int out, uint8_t* d_flags, unsigned long long* d_acc,
-                  cudaStream_t st) {
+                  cudaStream_t st, bool stats = true) {
     int rc;
     const uint32_t n_slices = (uint32_t)(nCO / 2);
     const uint32_t n_tiles = (uint32_t)((nC + ssjb::kTile - 1) / ssjb::kTile);
@@ -1143,7 +1145,7 @@ int verify_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, const uint32_
         ++e->prof_used;
         SSJ_CK(cudaEventRecord(k0, st));
     }
-    SSJ_CK(launch_strategy(*e, p, out, 0, n_tiles, st));
+    SSJ_CK(launch_strategy(*e, p, out, 0, n_tiles, st, stats));
     if (k1) SSJ_CK(cudaEventRecord(k1, st));
     return SSJ_OK;
 }
@@ -1535,7 +1537,7 @@ int ssj_gpu_join_shard(ssj_engine* e, int32_t algorithm, uint32_t shard, uint32_
         int r;
         const int out = want_pairs ? ssjb::kOutResults : ssjb::kOutCount;
         if ((r = verify_device(e, g.C.as<uint32_t>(), nC, g.CO.as<uint32_t>(), nCO, out, nullptr,
-                               acc.as<unsigned long long>(), st)))
+                               acc.as<unsigned long long>(), st, /*stats=*/false)))
             return r;
         unsigned long long words[SSJ_RESULT_WORDS];
         SSJ_CK(cudaMemcpyAsync(words, acc.p, sizeof(words), cudaMemcpyDeviceToHost, st));
