@@ -342,7 +342,15 @@ __global__ void compact_kernel(uint32_t a, uint32_t b, const unsigned long long*
         if (!n) continue;
         const uint32_t* src = C + (base[k] - base0);
         uint32_t* dst = outC + out_base[k];
-        for (uint32_t q = lane; q < n; q += 32) dst[q] = src[q];
+        uint32_t q = lane;
+        for (; q + 96 < n; q += 128) {  // 4 loads in flight per lane
+            const uint32_t v0 = src[q], v1 = src[q + 32], v2 = src[q + 64], v3 = src[q + 96];
+            dst[q] = v0;
+            dst[q + 32] = v1;
+            dst[q + 64] = v2;
+            dst[q + 96] = v3;
+        }
+        for (; q < n; q += 32) dst[q] = src[q];
         if (lane == 0) {
             outCO[2 * (size_t)slot[k]] = a + (uint32_t)k;
             outCO[2 * (size_t)slot[k] + 1] = (uint32_t)(out_base[k] + n);
