@@ -201,32 +201,31 @@ __device__ __forceinline__ bool candidate_keep(const FilterIndex& ix, const uint
             // pos8 / |s| from the record's top bytes (build_heads_kernel): no descriptor load
             const uint32_t pos8 = __byte_perm(__byte_perm(hv[0], hv[1], 0x0073), __byte_perm(hv[2], hv[3], 0x0073), 0x5410);
             ns = __byte_perm(__byte_perm(hv[4], hv[5], 0x0073), __byte_perm(hv[6], hv[7], 0x0073), 0x5410);
-            const uint32_t lim = min(pe.y, 8u);
-            if (kExact) {  // branch-free: all 8 lookups, hits below lim decide
+            // 8 tokens at a time: all lookups branch-free, the hits below the position decide
+            // (Bloom hits are confirmed by the exact search); tokens 8.. come from the CSR by
+            // 32-byte loads (reads past |s| stay inside the padded token array)
+            auto dup8 = [&](const uint32_t (&t)[8], uint32_t lim, uint32_t mask) -> bool {
                 uint32_t hit = 0;
 #pragma unroll
                 for (uint32_t u = 0; u < 8; ++u)
-                    hit |= (uint32_t)filter_hit<true>(bm, hv[u] & kHeadTokenMask, flo, fbits) << u;
-                keep = (hit & ((1u << lim) - 1u)) == 0;
-            } else {  // Bloom: branch-free screen, then the exact search for the hits only
-                uint32_t hit = 0;
+                    hit |= (uint32_t)filter_hit<kExact>(bm, t[u] & mask, flo, fbits) << u;
+                hit &= lim >= 8 ? 0xFFu : (1u << lim) - 1u;
+                if (kExact || !hit) return hit != 0;
+                bool d = false;
 #pragma unroll
-                for (uint32_t u = 0; u < 8; ++u)
-                    hit |= (uint32_t)filter_hit<false>(bm, hv[u] & kHeadTokenMask, flo, fbits) << u;
-                hit &= (1u << lim) - 1u;
-                if (hit) {
-#pragma unroll
-                    for (uint32_t u = 0; u < 8; ++u) {
-                        uint32_t pos;
-                        if ((hit >> u & 1u) && keep && in_r(rs, r, 0, p, hv[u] & kHeadTokenMask, &pos))
-                            keep = false;
-                    }
+                for (uint32_t u = 0; u < 8; ++u) {
+                    uint32_t pos;
+                    if ((hit >> u & 1u) && !d && in_r(rs, r, 0, p, t[u] & mask, &pos)) d = true;
                 }
-            }
+                return d;
+            };
+            keep = !dup8(hv, pe.y, kHeadTokenMask);
             if (keep && pe.y > 8) {
                 const uint32_t* st = ix.tokens + (size_t)pos8 * 8;
-                for (uint32_t u = 8; u < pe.y; ++u) {
-                    if (member(__ldg(st + u))) {
+                for (uint32_t u0 = 8; u0 < pe.y; u0 += 8) {
+                    uint32_t tv[8];
+                    ld8(st + u0, tv);
+                    if (dup8(tv, pe.y - u0, 0xFFFFFFFFu)) {
                         keep = false;
                         break;
                     }
