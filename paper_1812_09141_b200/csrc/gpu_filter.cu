@@ -175,6 +175,9 @@ __device__ __forceinline__ bool in_r(const uint32_t* __restrict__ rs,
     return l < p && (l < kGenRStage ? rs[l] : __ldg(r + l)) == v;
 }
 
+#ifndef SSJB_GEN_POS_FIRST
+#define SSJB_GEN_POS_FIRST 1
+#endif
 // Keep posting q of probe r (size m) at prefix position p? *s_out = the posting's set.
 // Duplicate iff an index-prefix token of s below r[p] is in r (then it is in r[0..p), where s
 // was already emitted); PPJoin also applies the positional filter at this first match.
@@ -194,6 +197,16 @@ __device__ __forceinline__ bool candidate_keep(const FilterIndex& ix, const uint
         return filter_hit<kExact>(bm, v, flo, fbits) && (kExact || in_r(rs, r, 0, p, v, &pos));
     };
     uint32_t ns = 0;  // |s| when the head record was read
+#if SSJB_GEN_POS_FIRST
+    // PPJoin: the positional filter (filters.hpp:174-181, current_overlap = 1,
+    // joiners.hpp:94) first -- keep = first occurrence AND positional, so the order of the two
+    // tests does not change the stream, and the candidates it rejects skip the dedup
+    if (positional) {
+        ns = set_size(ix, s);
+        const uint64_t a = m - p - 1, b = ns - pe.y - 1;
+        if (1 + (a < b ? a : b) < dev_required_fast(ix.pred, m, ns)) return false;
+    }
+#endif
     if (p && pe.y) {  // pe.y = position of r[p] in s: the tokens before it are < r[p]
         if (ix.heads) {
             uint32_t hv[8];
@@ -241,7 +254,7 @@ __device__ __forceinline__ bool candidate_keep(const FilterIndex& ix, const uint
             }
         }
     }
-    if (keep && positional) {
+    if (!SSJB_GEN_POS_FIRST && keep && positional) {
         // filters.hpp:174-181 positional_filter with current_overlap = 1 (joiners.hpp:94)
         if (!ns) ns = set_size(ix, s);  // sets in an index are never empty
         const uint64_t a = m - p - 1, b = ns - pe.y - 1;
