@@ -154,7 +154,10 @@ class ClockSampler:
                 self._smi_loop()
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
-        time.sleep(0.01)  # first sample before the timed region starts
+        # the first sample (NVML initialised) before the timed region starts
+        deadline = time.time() + 2.0
+        while not self.samples and self._t.is_alive() and time.time() < deadline:
+            time.sleep(0.001)
         return self
 
     def __exit__(self, *exc):
