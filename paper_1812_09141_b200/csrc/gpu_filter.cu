@@ -266,6 +266,9 @@ __device__ __forceinline__ bool candidate_keep(const FilterIndex& ix, const uint
 #ifndef SSJB_GEN_EXACT
 #define SSJB_GEN_EXACT 1
 #endif
+#ifndef SSJB_GEN_DYN
+#define SSJB_GEN_DYN 1
+#endif
 #ifndef SSJB_GEN_MINB
 #define SSJB_GEN_MINB 4
 #endif
@@ -281,7 +284,20 @@ __global__ void __launch_bounds__(kGenThreads, SSJB_GEN_MINB)
     const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const bool positional = ix.algorithm == 1;
+#if SSJB_GEN_DYN
+    // dynamic schedule, largest probes first (sizes ascend with the set id): a warp takes the
+    // next probe when it is done, so a few heavy probes do not make the launch's tail
+    (void)w;
+    (void)nw;
+    for (;;) {
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(ix.work, 1ull);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= (unsigned long long)(b - a)) break;
+        const uint64_t k = (uint64_t)(b - a) - 1 - t;
+#else
     for (uint64_t k = w; k < (uint64_t)(b - a); k += nw) {
+#endif
         const uint32_t i = a + (uint32_t)k;
         const uint32_t m = set_size(ix, i);
         uint32_t n_out = 0;
@@ -387,6 +403,7 @@ cudaError_t filter_index_build(FilterIndex* ix, const uint32_t* d_tokens, const 
     ix->pred = pred;
     ix->algorithm = algorithm;
     ix->universe = 0;
+    if (cudaMalloc(&ix->work, sizeof(unsigned long long)) != cudaSuccess) return cudaErrorMemoryAllocation;
     if (!n_sets) return cudaSuccess;
     uint32_t *ilen = nullptr, *off = nullptr, *mx = nullptr, *keys = nullptr, *keys2 = nullptr,
              *count = nullptr;
@@ -474,8 +491,10 @@ done:
 void filter_index_free(FilterIndex* ix) {
     cudaFree(ix->head);
     cudaFree(ix->post);
+    cudaFree(ix->work);
     ix->head = nullptr;
     ix->post = nullptr;
+    ix->work = nullptr;
     ix->n_post = 0;
 }
 
@@ -491,6 +510,11 @@ cudaError_t filter_generate(const FilterIndex& ix, uint32_t a, uint32_t b,
                             uint32_t* d_C, unsigned long long* d_count, uint32_t* d_flag,
                             cudaStream_t st) {
     if (b <= a) return cudaSuccess;
+    if (SSJB_GEN_DYN) {
+        if (!ix.work) return cudaErrorInvalidValue;
+        cudaError_t e = cudaMemsetAsync(ix.work, 0, sizeof(unsigned long long), st);
+        if (e != cudaSuccess) return e;
+    }
     generate_kernel<<<warps_grid(b - a), kGenThreads, 0, st>>>(ix, a, b, d_base, base0, d_C,
                                                                 d_count, d_flag);
     return cudaGetLastError();

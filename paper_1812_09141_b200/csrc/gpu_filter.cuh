@@ -37,6 +37,7 @@ struct FilterIndex {
     const uint32_t* tokens = nullptr;  // padded CSR (engine-owned)
     const uint2* sets = nullptr;       // {pos8, size} (engine-owned)
     const uint4* heads = nullptr;      // packed head records (engine-owned, nullable)
+    unsigned long long* work = nullptr;  // generate_kernel's probe counter (dynamic schedule)
 };
 
 // Build the index (synchronous on `st`). Returns cudaSuccess or the first error.
