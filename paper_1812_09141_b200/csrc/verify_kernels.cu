@@ -1261,6 +1261,9 @@ constexpr uint32_t kLongPerLane = SSJB_LONG_PER_LANE;  // candidate tokens per l
 #ifndef SSJB_LONG_V2
 #define SSJB_LONG_V2 1
 #endif
+#ifndef SSJB_LONG_DYN_SLICES
+#define SSJB_LONG_DYN_SLICES 1
+#endif
 
 // Next-step token loads of the long pass. ptxas sinks plain (.nc) loads below the step's exit
 // branches, next to their first use; a strong load keeps its place ahead of the lookups.
@@ -1302,7 +1305,18 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
     constexpr uint32_t W = kLongThreads / 32;
     const uint64_t n_items = min((uint64_t)*p.defer_n, p.defer_cap);
     unsigned count = 0, prunes = 0, verified = 0;
+#if SSJB_LONG_DYN_SLICES
+    // slices taken dynamically (p.defer_n[3] counts them out): their long-pair work varies by
+    // orders of magnitude, so a static round-robin leaves SMs idle in the launch's tail
+    __shared__ unsigned long long s_it;
+    for (;;) {
+        if (tid == 0) s_it = atomicAdd(p.defer_n + 3, 1ull);
+        __syncthreads();
+        const uint64_t it = s_it;  // read by all before the slice's first barrier below
+        if (it >= n_items) break;
+#else
     for (uint64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+#endif
         const uint32_t e = __ldg(p.defer + it);
         const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(p.slices + e));
         const uint32_t m = d0.z;
