@@ -66,7 +66,8 @@ struct DeviceScope {
 constexpr int kEventsPerSlot = 96;
 constexpr uint64_t kPieceMinSlots = 1ull << 22;  // 4M candidates = 16 MB of C per piece
 constexpr int kMaxPieces = 32;
-constexpr int kCounters = 4;  // per piece: deferred long slices, runs, short tiles, long-pass work
+constexpr int kCounters = 5;  // per piece: deferred long slices, runs, short tiles, long-pass
+                              // work, short-tile work
 
 template <typename T>
 int ensure_device(T** ptr, size_t* cap, size_t need) {

@@ -29,6 +29,10 @@
 #include "verify_kernels.cuh"
 #include "../../include/ssjoin_b200.h"
 
+#ifndef SSJB_TILE_DYN
+#define SSJB_TILE_DYN 1  // warp_tile_kernel takes short tiles from a per-launch counter
+#endif
+
 namespace ssjb {
 
 namespace {
@@ -491,18 +495,37 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) warp_tile_kernel(co
     const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     unsigned count = 0, prunes = 0, verified = 0;
     // software pipeline over the warp's tiles: the next tile's C ids and slice bounds are in
-    // flight while this tile is verified, the tile after next's index one step earlier
-    uint32_t tile = gw < n ? __ldg(p.short_tiles + gw) : 0u;
-    uint32_t tile_n = gw + n_warps < n ? __ldg(p.short_tiles + gw + n_warps) : 0u;
+    // flight while this tile is verified, the tile after next's index one step earlier.
+    // Tiles are taken dynamically from a per-launch counter (p.defer_n[4]): their cost varies
+    // with the pair lengths, and a static stride leaves SMs idle in the launch's tail.
+    const uint32_t lane = threadIdx.x & 31;
+    // (only when warps get several tiles each: with ~2 per warp the atomics cost more than
+    // the tail they remove)
+    unsigned long long* const ctr =
+        SSJB_TILE_DYN && p.defer_n && n >= 4 * n_warps ? p.defer_n + 4 : nullptr;
+    uint64_t step_i = 0;
+    auto next_index = [&]() -> uint64_t {  // warp-uniform
+        if (!ctr) return gw + (step_i++) * n_warps;
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(ctr, 1ull);
+        return __shfl_sync(0xffffffffu, t, 0);
+    };
+    uint64_t w = next_index();
+    uint64_t wn = w < n ? next_index() : n;
+    uint32_t tile = w < n ? __ldg(p.short_tiles + w) : 0u;
+    uint32_t tile_n = wn < n ? __ldg(p.short_tiles + wn) : 0u;
     TilePre cur;
-    if (gw < n) tile_prefetch(p, tile, cur);
-    for (uint64_t w = gw; w < n; w += n_warps) {
+    if (w < n) tile_prefetch(p, tile, cur);
+    while (w < n) {
         TilePre nxt;
-        const bool more = w + n_warps < n;
+        const bool more = wn < n;
         if (more) tile_prefetch(p, tile_n, nxt);
-        const uint32_t tile_nn = w + 2 * n_warps < n ? __ldg(p.short_tiles + w + 2 * n_warps) : 0u;
+        const uint64_t wnn = more ? next_index() : n;
+        const uint32_t tile_nn = wnn < n ? __ldg(p.short_tiles + wnn) : 0u;
         warp_tile<kOut, kStats, kPacked>(p, tile, cur, count, prunes, verified);
         if (more) cur = nxt;
+        w = wn;
+        wn = wnn;
         tile = tile_n;
         tile_n = tile_nn;
     }
