@@ -15,18 +15,28 @@ Arms:
          the launching stream, max over ranks);
   e2e    through the C ABI with host buffers: ssj_verify_chunk from pinned C/C_O, H2D + kernels
          + D2H of the flags inside the timed region;
+  parity the step's flags (all candidates) compared byte for byte with the reference's own
+         VerificationEngine::verify_chunk on the same batch (the cpu_baseline leg) and with the
+         committed golden digest (tests/golden/bench_golden.json); the whole-join pairs of
+         `join` compared with the reference run_join's golden digest;
   --impl reference: the reference's own VerificationEngine::verify_chunk (strategy A, all host
-         threads) compiled from its headers (oracle/_ref/libssjref.so), bounded sample per step.
+         threads) compiled from its headers (oracle/_ref/libssjref.so) on the SAME batch, plus
+         the reference run_join on the join workload. This arm never loads libssjoin_b200.so:
+         its workload comes from the generator sources linked into libssjref.so
+         (oracle/work_shim.cpp).
 
-Multi-GPU (torchrun): weak scaling -- every rank verifies its own batch (different probe
-windows); the collection is uploaded by rank 0 and broadcast once over NVLink (NCCL); no
-collective in the timed region.
+Multi-GPU: `--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU). Weak scaling -- every rank verifies its own
+batch (different probe windows); the collection is uploaded by rank 0 and broadcast once over
+NVLink (NCCL); no collective in the timed region.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -37,14 +47,20 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_1812_09141_b200.parallel import broadcast_device_collection, shard_probe_windows  # noqa: E402
+GOLDEN = os.path.join(ROOT, "tests", "golden", "bench_golden.json")
 
+_CFG2 = dict(sets=1_000_000, min_size=40, max_size=120, universe=7200, zipf_tokens=True,
+             token_skew=1.0, duplicate_fraction=0.01, max_edits=2, distinct_tokens=True)
 WORKLOADS = {
     # name: (synth kwargs, threshold, algorithm, description)
-    "cfg2": (dict(sets=1_000_000, min_size=40, max_size=120, universe=7200, zipf_tokens=True,
-                  token_skew=1.0, duplicate_fraction=0.01, max_edits=2, distinct_tokens=True),
-             (4, 5), "allpairs",
+    "cfg2": (_CFG2, (4, 5), "allpairs",
              "DBLP-like Zipf self-join, 1M sets, avg 80 tokens, universe 7200, Jaccard 0.80"),
+    "cfg2_085": (_CFG2, (17, 20), "allpairs",
+                 "DBLP-like Zipf self-join, 1M sets, avg 80 tokens, universe 7200, Jaccard 0.85"),
+    "cfg2_090": (_CFG2, (9, 10), "allpairs",
+                 "DBLP-like Zipf self-join, 1M sets, avg 80 tokens, universe 7200, Jaccard 0.90"),
+    "cfg2_095": (_CFG2, (19, 20), "allpairs",
+                 "DBLP-like Zipf self-join, 1M sets, avg 80 tokens, universe 7200, Jaccard 0.95"),
     "cfg1": (dict(sets=100_000, min_size=5, max_size=15, universe=10_000, zipf_tokens=False,
                   duplicate_fraction=0.10, max_edits=1, distinct_tokens=True),
              (9, 10), "allpairs",
@@ -64,6 +80,8 @@ WORKLOADS = {
              (4, 5), "allpairs",
              "~1B-candidate DBLP-like Zipf join, 550K sets, Jaccard 0.8 (probe-sharded)"),
 }
+BIG = ("cfg2", "cfg2_085", "cfg2_090", "cfg2_095", "cfg5")  # stratified 256M-candidate batches
+ALG = {"allpairs": 0, "ppjoin": 1, "groupjoin": 2}
 
 
 def log(*a):
@@ -75,28 +93,93 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def build_batch(ssj, coll, pred, algorithm, rank, world, target, windows, threads):
-    """Stratified probe windows over the collection; rank r takes window offset r."""
-    n = coll.size()
-    alg = ssj.Algorithm.AllPairs if algorithm == "allpairs" else ssj.Algorithm.PPJoin
-    if target <= 0:  # the whole join's candidate stream
-        chunk = ssj.generate_candidates_windows(coll, pred, alg,
-                                                shard_probe_windows(n, world, n, rank, world)
-                                                if world > 1 else [(0, n)], threads)
-        return chunk, n
-    # calibrate the window width on a small probe sample
+def sha256(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).view(np.uint8).data).hexdigest()
+
+
+def load_golden():
+    try:
+        with open(GOLDEN) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ---- workload (shared by both arms; the generator is passed in) ---------------------------
+def shard_probe_windows(n_sets, windows, width, rank, world):
+    """Stratified probe windows for `rank` (paper_1812_09141_b200/parallel.py restated here so
+    that the reference arm does not import the product package): the collection is cut into
+    `windows` strides; each rank takes its own `width`-wide window inside every stride."""
+    stride = n_sets // windows
+    width = min(width, stride // max(world, 1))
+    return [(k * stride + rank * width, min(k * stride + rank * width + width, n_sets))
+            for k in range(windows)]
+
+
+def batch_windows(gen, n, rank, world, target, windows):
+    """The probe windows of rank `rank`'s step batch. gen(windows) -> (C, C_O). target <= 0:
+    the whole join (probe shards of n / world); else `windows` stratified windows whose width is
+    calibrated on a 64-probe sample to give ~target candidates."""
+    if target <= 0:
+        return (shard_probe_windows(n, world, n, rank, world) if world > 1 else [(0, n)]), n
     stride = n // windows
     sample_w = max(1, min(64, stride // max(world, 1)))
-    cal = ssj.generate_candidates_windows(coll, pred, alg,
-                                          [(k * stride, k * stride + sample_w)
-                                           for k in range(windows)], threads)
-    per_probe = max(cal.C.size / (windows * sample_w), 1e-9)
+    cal_C, _ = gen([(k * stride, k * stride + sample_w) for k in range(windows)])
+    per_probe = max(cal_C.size / (windows * sample_w), 1e-9)
     width = int(min(stride // max(world, 1), max(1, target / (per_probe * windows))))
-    wins = shard_probe_windows(n, windows, width, rank, world)
-    chunk = ssj.generate_candidates_windows(coll, pred, alg, wins, threads)
-    return chunk, width
+    return shard_probe_windows(n, windows, width, rank, world), width
 
 
+class OursWorkload:
+    """The workload through the product library (GPU arm)."""
+
+    def __init__(self, name, seed, threads):
+        import paper_1812_09141_b200 as ssj
+        self.ssj = ssj
+        synth_kw, self.pred_t, self.algorithm, self.desc = WORKLOADS[name]
+        self.coll = ssj.synth_collection(seed, ssj.SynthConfig(**synth_kw))
+        self.tokens, self.offsets = self.coll.tokens, self.coll.offsets
+        self.original_id = self.coll.original_id
+        self.pred = ssj.jaccard(*self.pred_t)
+        self.threads = threads
+
+    def gen(self, wins):
+        ch = self.ssj.generate_candidates_windows(self.coll, self.pred,
+                                                  self.ssj.Algorithm(ALG[self.algorithm]), wins,
+                                                  self.threads)
+        return ch.C, ch.C_O
+
+
+class RefWorkload:
+    """The same workload through oracle/_ref/libssjref.so only (reference arm)."""
+
+    def __init__(self, name, seed, threads, R):
+        self.R = R
+        synth_kw, self.pred_t, self.algorithm, self.desc = WORKLOADS[name]
+        self.tokens, self.offsets, self.original_id = R.work_synth(seed, **synth_kw)
+        self.threads = threads
+
+    def gen(self, wins):
+        return self.R.work_generate_windows(self.tokens, self.offsets, 0, self.pred_t[0],
+                                            self.pred_t[1], 1, ALG[self.algorithm], wins,
+                                            self.threads)
+
+
+def workload_config(name, w, C, C_O, width, windows):
+    """The `config` object both arms print (identical for the same workload and batch)."""
+    n = int(w.offsets.size - 1)
+    return {"workload": w.desc, "name": name, "n_sets": n,
+            "avg_set_size": round(int(w.tokens.size) / max(n, 1), 2),
+            "threshold": f"{w.pred_t[0]}/{w.pred_t[1]}", "algorithm": w.algorithm,
+            "candidates_per_step_per_gpu": int(C.size), "slices_per_step": int(C_O.size // 2),
+            "probe_windows": windows if name in BIG else 1, "window_width": int(width),
+            "mode": "pairs (flags)",
+            "l2": f"inputs larger than L2: C = {4 * C.size / 2**30:.2f} GiB per step"
+                  if 4 * C.size > (126 << 20) else
+                  "inputs smaller than L2 (126 MB): whole-join batch re-verified each step"}
+
+
+# ---- clocks ----------------------------------------------------------------------------
 class ClockSampler:
     """SM clocks + throttle reasons sampled during the timed region: NVML polled every ~2 ms
     (the timed region of a default run is tens of ms), nvidia-smi as the fallback."""
@@ -179,13 +262,6 @@ class ClockSampler:
                 "samples": len(self.samples), "source": self.source}
 
 
-def measure_read_gbs(local):
-    """Streaming-read bandwidth of an L2-resident (48 MiB) and an HBM-sized (4 GiB) buffer,
-    measured in this run by the library's diagnostic kernel (16-byte loads, grid-stride)."""
-    from paper_1812_09141_b200.verify import measure_read_bandwidth
-    return (measure_read_bandwidth(local, 48 << 20, 50), measure_read_bandwidth(local, 4 << 30, 5))
-
-
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -207,57 +283,119 @@ def ncu_traffic(workload):
         return None
 
 
-def stratified_sample(chunk, sample):
-    """Every k-th slice of the batch (k chosen so that ~`sample` candidates are picked), so the
-    CPU sample has the batch's mix of probe sizes (slices are in probe = size order).
-    Returns (C_sub, C_O_sub, slot_index_of_sub) as numpy arrays."""
-    CO = chunk.C_O.reshape(-1, 2).astype(np.int64)
-    n_sl = CO.shape[0]
-    if n_sl == 0:
-        return np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.int64)
-    ends = CO[:, 1]
-    begins = np.concatenate([[0], ends[:-1]])
-    total = int(ends[-1])
-    k = max(1, int(np.ceil(total / max(sample, 1))))
-    pick = np.arange(0, n_sl, k)
-    lens = ends[pick] - begins[pick]
-    idx = np.concatenate([np.arange(b, e) for b, e in zip(begins[pick], ends[pick])]) \
-        if lens.sum() else np.zeros(0, np.int64)
-    sub_C = chunk.C[idx]
-    sub_CO = np.stack([CO[pick, 0], np.cumsum(lens)], 1).reshape(-1).astype(np.uint32)
-    return sub_C, sub_CO, idx
+# ---- reference (CPU) pieces --------------------------------------------------------------
+def ref_verify(R, w, C, C_O, reps, want_flags):
+    """The reference's VerificationEngine::verify_chunk (strategy A, Pairs mode, all host
+    threads) on the batch: (best seconds, count, flags or None, workers)."""
+    h = R.coll(w.tokens, w.offsets, w.original_id)
+    workers = int(R.L.ref_hardware_concurrency())
+    pool = R.pool(workers)
+    flags = np.zeros(max(C.size, 1), np.uint8) if want_flags else None
+    sec, cnt = R.time_verify_chunk(h, pool, 0, w.pred_t[0], w.pred_t[1], 1, 0, 1, True, C, C_O,
+                                   reps=reps, flags_out=flags)
+    R.L.ref_pool_free(pool)
+    R.L.ref_coll_free(h)
+    return sec, cnt, (flags[: C.size] if want_flags else None), workers
 
 
-def cpu_reference_rate(coll, pred_t, chunk, sample, reps=3):
-    """The reference's verify_chunk (strategy A, all host threads) on a stratified sample of
-    ~`sample` candidates of the batch (every k-th slice). Returns
-    (pairs/s, cores, kind, n_sample, count, slot_index)."""
-    from oracle import pyoracle as po
-    sub_C, sub_CO, idx = stratified_sample(chunk, sample)
-    nC = int(sub_C.size)
-    if po.ref_available():
-        R = po.Ref()
-        h = R.coll(coll.tokens, coll.offsets, coll.original_id)
-        workers = R.L.ref_hardware_concurrency()
-        pool = R.pool(workers)
-        sec, cnt = R.time_verify_chunk(h, pool, 0, pred_t[0], pred_t[1], 1, 0, 1, True, sub_C,
-                                       sub_CO, reps=reps)
-        return nC / sec, int(workers), "reference", nC, cnt, idx
+def ref_join(R, name, seed, threads):
+    """The reference's CPU run_join (pipeline.hpp:150-361) on the join workload: the same
+    algorithm, Pairs mode, M_c = 64 MiB, strategy A, all host threads as workers."""
+    w = RefWorkload(name, seed, threads, R)
+    h = R.coll(w.tokens, w.offsets, w.original_id)
+    workers = int(R.L.ref_hardware_concurrency())
     t0 = time.perf_counter()
-    res = po.verify_chunk(coll.tokens, coll.offsets, sub_C, sub_CO, po.pred(0, *pred_t))
-    sec = time.perf_counter() - t0
-    return nC / sec, 1, "port", nC, res["count"], idx
+    rep, pairs, _ = R.run_join(h, 0, w.pred_t[0], w.pred_t[1], 1, algorithm=ALG[w.algorithm],
+                               budget=64 << 20, kind=0, group=1, pairs_mode=True,
+                               workers=workers)
+    wall = time.perf_counter() - t0
+    R.L.ref_coll_free(h)
+    pairs = np.ascontiguousarray(pairs, np.uint32)
+    return {"workload": w.desc, "name": name, "n_sets": int(w.offsets.size - 1),
+            "threshold": f"{w.pred_t[0]}/{w.pred_t[1]}", "algorithm": w.algorithm,
+            "join_ms": rep["join_ms"], "wall_s": wall, "count": rep["count"],
+            "candidates": rep["candidate_count"], "filtering_ms": rep["filtering_ms"],
+            "serialization_ms": rep["serialization_ms"],
+            "verification_ms": rep["verification_ms"], "workers": workers,
+            "pairs_sha256": sha256(pairs), "n_pairs": int(pairs.shape[0]),
+            "path": "reference run_join (pipeline.hpp:150-361), strategy A, Pairs mode, "
+                    "M_c 64 MiB; pairs sorted like write_pairs (report.hpp:39-42)"}
 
 
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import pyoracle as po
+    if not po.ref_available():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libssjref.so missing (reference not built)"}))
+        return 0
+    R = po.Ref()
+    t0 = time.perf_counter()
+    w = RefWorkload(args.workload, args.seed, args.threads, R)
+    n = int(w.offsets.size - 1)
+    wins, width = batch_windows(w.gen, n, 0, world, args.candidates, args.windows)
+    C, C_O = w.gen(wins)
+    config = workload_config(args.workload, w, C, C_O, width, args.windows)
+    log(f"[reference] batch {C.size} candidates in {C_O.size // 2} slices "
+        f"({time.perf_counter() - t0:.1f}s setup)")
+    h = R.coll(w.tokens, w.offsets, w.original_id)
+    workers = int(R.L.ref_hardware_concurrency())
+    pool = R.pool(workers)
+    for _ in range(args.warmup):
+        R.time_verify_chunk(h, pool, 0, w.pred_t[0], w.pred_t[1], 1, 0, 1, True, C, C_O, reps=1)
+    elapsed = 0.0
+    flags = np.zeros(max(C.size, 1), np.uint8)
+    cnt = 0
+    for k in range(args.steps):  # each step: verify_chunk of the whole batch, timed in the shim
+        sec, cnt = R.time_verify_chunk(h, pool, 0, w.pred_t[0], w.pred_t[1], 1, 0, 1, True, C,
+                                       C_O, reps=1,
+                                       flags_out=flags if k == args.steps - 1 else None)
+        elapsed += sec
+    R.L.ref_pool_free(pool)
+    R.L.ref_coll_free(h)
+    value = C.size * args.steps / elapsed
+    join = None
+    if args.join_workload != "none" and not args.no_ref_join:
+        try:
+            join = ref_join(R, args.join_workload, args.seed if args.join_workload != "cfg5"
+                            else args.join_seed, args.threads)
+        except Exception as e:  # reported, never fatal
+            join = {"error": str(e)[:300]}
+    line = {
+        "impl": "reference", "metric": "candidate pairs verified/sec", "value": value,
+        "unit": "pairs/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": config,
+        "arm": {"strategy": "A", "workers": workers, "mode": "Pairs",
+                "path": "reference VerificationEngine::verify_chunk (verify.hpp:257-275), "
+                        "oracle/_ref/libssjref.so (reference headers, -O3 -DNDEBUG)"},
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": workers,
+                         "kind": "reference",
+                         "sample": f"the whole step batch ({C.size} candidates) per step"},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "parity": {"count": int(cnt), "flags_sha256": sha256(flags[: C.size])},
+        "join": join,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- GPU arm -----------------------------------------------------------------------------
 def gpu_join_shards(ssj, args, rank, world, local, dev):
     """BASELINE cfg5 (or --join-workload) self-join run entirely on the GPUs: rank r joins
     probe shard r of N (equal candidate upper bounds, no exchange step); counts summed, time
-    = max over ranks of the join call (device filtering + verification + pair decoding)."""
+    = max over ranks of the join call (device filtering + verification + pair decoding);
+    the pairs of all shards gathered on rank 0 and compared with the reference run_join's."""
     import torch
     synth_kw, pred_t, algorithm, desc = WORKLOADS[args.join_workload]
-    coll = ssj.synth_collection(args.seed, ssj.SynthConfig(**synth_kw))
+    seed = args.join_seed if args.join_workload == "cfg5" else args.seed
+    coll = ssj.synth_collection(seed, ssj.SynthConfig(**synth_kw))
     pred = ssj.jaccard(*pred_t)
-    alg = 0 if algorithm == "allpairs" else 1
+    alg = ALG[algorithm]
     eng = ssj.VerificationEngine(coll, pred, ssj.OutputMode.Pairs,
                                  ssj.Strategy(ssj.StrategyKind.Auto, 32), device=local)
     eng.set_original_ids(coll.original_id)
@@ -266,7 +404,7 @@ def gpu_join_shards(ssj, args, rank, world, local, dev):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
-    _, rep = eng.gpu_join(alg, pairs=True, pairs_cap=1 << 22, shard=rank, n_shards=world)
+    pairs, rep = eng.gpu_join(alg, pairs=True, pairs_cap=1 << 22, shard=rank, n_shards=world)
     eng.close()
     vals = torch.tensor([rep["join_ms"], float(rep["count"]), float(rep["candidate_count"]),
                          rep["filtering_ms"], rep["verification_ms"]], dtype=torch.float64,
@@ -277,68 +415,48 @@ def gpu_join_shards(ssj, args, rank, world, local, dev):
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         sm = vals.clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        parts = [None] * world
+        dist.all_gather_object(parts, pairs)
+        allp = np.concatenate([p.reshape(-1, 2) for p in parts], 0)
+        order = np.lexsort((allp[:, 1], allp[:, 0]))
+        pairs = np.ascontiguousarray(allp[order], np.uint32)
     else:
         mx = sm = vals
     ms = float(mx[0].item())
-    return {"workload": desc, "n_sets": coll.size(), "threshold": f"{pred_t[0]}/{pred_t[1]}",
-            "algorithm": algorithm, "n_gpus": world, "join_ms": ms,
-            "count": int(sm[1].item()), "candidates": int(sm[2].item()),
-            "candidates_per_s": float(sm[2].item()) / (ms / 1e3) if ms else None,
-            "filtering_ms_max": float(mx[3].item()), "verification_ms_max": float(mx[4].item()),
-            "path": "ssj_gpu_join_shard: static index on the device, candidate generation and "
-                    "verification in device-resident chunks, pairs decoded + sorted on the "
-                    "device (pairs mode); rank r = probe shard r of N, no exchange step",
-            "reference": "profiles/r1_join_e2e.json: the reference CPU run_join on cfg5"}
+    pairs = np.ascontiguousarray(pairs, np.uint32)
+    digest = sha256(pairs)
+    gold = load_golden().get("join", {}).get(args.join_workload)
+    out = {"workload": desc, "name": args.join_workload, "n_sets": coll.size(),
+           "threshold": f"{pred_t[0]}/{pred_t[1]}", "algorithm": algorithm, "n_gpus": world,
+           "join_ms": ms, "count": int(sm[1].item()), "candidates": int(sm[2].item()),
+           "candidates_per_s": float(sm[2].item()) / (ms / 1e3) if ms else None,
+           "filtering_ms_max": float(mx[3].item()), "verification_ms_max": float(mx[4].item()),
+           "pairs_sha256": digest, "n_pairs": int(pairs.shape[0]),
+           "path": "ssj_gpu_join_shard: static index on the device, candidate generation and "
+                   "verification in device-resident chunks, pairs decoded + sorted on the "
+                   "device (pairs mode); rank r = probe shard r of N, no exchange step"}
+    if gold:
+        out["reference"] = {"join_ms": gold.get("join_ms"), "count": gold["count"],
+                            "pairs_sha256": gold["pairs_sha256"],
+                            "source": "tests/golden/bench_golden.json (reference run_join, "
+                                      "made by tests/golden/make_bench_golden.py)"}
+        out["pairs_match"] = (digest == gold["pairs_sha256"]
+                              and int(pairs.shape[0]) == gold["count"])
+        if gold.get("join_ms"):
+            out["speedup_vs_reference_join"] = gold["join_ms"] / ms if ms else None
+    return out
 
 
-def run_reference_arm(args):
-    rank, world, local = dist_env()
-    if rank != 0:
-        return 0
-    import paper_1812_09141_b200 as ssj
-    synth_kw, pred_t, algorithm, desc = WORKLOADS[args.workload]
-    coll = ssj.synth_collection(args.seed, ssj.SynthConfig(**synth_kw))
-    pred = ssj.jaccard(*pred_t)
-    chunk, width = build_batch(ssj, coll, pred, algorithm, 0, 1,
-                               256e6 if args.workload in ("cfg2", "cfg5") else 0, args.windows,
-                               args.threads)
-    sub_C, sub_CO, _ = stratified_sample(chunk, args.ref_sample)
-    chunk = ssj.CandidateChunk(sub_C, sub_CO)
-    from oracle import pyoracle as po
-    if not po.ref_available():
-        print(json.dumps({"impl": "reference",
-                          "unavailable": "oracle/_ref/libssjref.so missing (reference not built)"}))
-        return 0
-    R = po.Ref()
-    h = R.coll(coll.tokens, coll.offsets, coll.original_id)
-    workers = R.L.ref_hardware_concurrency()
-    pool = R.pool(workers)
-    for _ in range(args.warmup):
-        R.time_verify_chunk(h, pool, 0, pred_t[0], pred_t[1], 1, 0, 1, True, chunk.C, chunk.C_O,
-                            reps=1)
-    elapsed = 0.0
-    for _ in range(args.steps):  # each step: verify_chunk timed inside the reference shim
-        sec, cnt = R.time_verify_chunk(h, pool, 0, pred_t[0], pred_t[1], 1, 0, 1, True, chunk.C,
-                                       chunk.C_O, reps=1)
-        elapsed += sec
-    pairs = chunk.C.size * args.steps
-    value = pairs / elapsed
-    line = {
-        "impl": "reference", "metric": "candidate pairs verified/sec", "value": value,
-        "unit": "pairs/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": desc, "sample_candidates_per_step": int(chunk.C.size),
-                   "sample": "every k-th slice of the GPU arm's batch (stratified)",
-                   "strategy": "A", "workers": int(workers)},
-        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": int(workers),
-                         "kind": "reference",
-                         "sample": f"{chunk.C.size} candidates of the {args.workload} batch"},
-        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line))
-    return 0
+def spawn_ranks(args):
+    """`--gpus N` outside torchrun: re-launch this script under torch.distributed.run with N
+    ranks on 127.0.0.1 (one process per GPU)."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -349,37 +467,46 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--candidates", type=float, default=None,
-                    help="candidates per step (default: 256M for cfg2/cfg5, the whole join "
-                         "for the smaller configs)")
+                    help="candidates per step (default: 256M for the cfg2/cfg5 rows, the whole "
+                         "join for the smaller configs)")
     ap.add_argument("--windows", type=int, default=64)
     ap.add_argument("--seed", type=int, default=1812)
+    ap.add_argument("--join-seed", type=int, default=1812)
     ap.add_argument("--threads", type=int, default=0, help="host generator threads (0 = all)")
     ap.add_argument("--strategy", default="Auto")
     ap.add_argument("--group", type=int, default=32)
-    ap.add_argument("--cpu-sample", type=float, default=24e6)
-    ap.add_argument("--ref-sample", type=float, default=24e6)
+    ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ref-join", action="store_true",
+                    help="reference arm: skip the reference run_join on the join workload")
     ap.add_argument("--join-workload", default="cfg5",
-                    help="workload of the extra whole-join measurement on the GPU ('none' = off)")
+                    help="workload of the extra whole-join measurement ('none' = off)")
     args = ap.parse_args()
-    args.ref_sample = int(args.ref_sample)
     if args.candidates is None:
-        args.candidates = 256e6 if args.workload in ("cfg2", "cfg5") else 0
+        args.candidates = 256e6 if args.workload in BIG else 0
 
+    rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch "
+                         "N ranks with torchrun, or run without torchrun to self-spawn)")
     if args.impl == "reference":
         return run_reference_arm(args)
 
     import torch
     import paper_1812_09141_b200 as ssj
+    from paper_1812_09141_b200.parallel import broadcast_device_collection
+    from paper_1812_09141_b200.verify import measure_read_bandwidth
 
-    rank, world, local = dist_env()
     # one GPU per rank; with fewer visible GPUs than ranks (a functional check of the
     # multi-rank path on a single GPU) ranks share devices and use gloo instead of NCCL
     ndev = max(torch.cuda.device_count(), 1)
     local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    dist = None
     if world > 1:
         import torch.distributed as dist
         if ndev >= world:
@@ -387,14 +514,14 @@ def main():
         else:
             dist.init_process_group("gloo")
 
-    synth_kw, pred_t, algorithm, desc = WORKLOADS[args.workload]
     t0 = time.perf_counter()
-    coll = ssj.synth_collection(args.seed, ssj.SynthConfig(**synth_kw))
-    pred = ssj.jaccard(*pred_t)
-    chunk, width = build_batch(ssj, coll, pred, algorithm, rank, world, args.candidates,
-                               args.windows, args.threads)
-    nC, nCO = chunk.C.size, chunk.C_O.size
-    log(f"[rank {rank}] collection {coll.size()} sets avg {coll.tokens.size / coll.size():.1f}; "
+    w = OursWorkload(args.workload, args.seed, args.threads)
+    coll, pred, pred_t = w.coll, w.pred, w.pred_t
+    wins, width = batch_windows(w.gen, coll.size(), rank, world, args.candidates, args.windows)
+    C_h, CO_h = w.gen(wins)
+    nC, nCO = int(C_h.size), int(CO_h.size)
+    config = workload_config(args.workload, w, C_h, CO_h, width, args.windows)
+    log(f"[rank {rank}] collection {coll.size()} sets avg {config['avg_set_size']}; "
         f"batch {nC} candidates in {nCO // 2} slices ({time.perf_counter() - t0:.1f}s setup)")
 
     strategy = ssj.Strategy(ssj.StrategyKind[args.strategy], args.group)
@@ -410,11 +537,12 @@ def main():
         eng, keep = broadcast_device_collection(eng0, coll.size(), int(coll.tokens.size),
                                                 coll.offsets, pred, mode, strategy, local, rank)
         bcast_ms = 1e3 * (time.perf_counter() - tb)
-    resolved = eng.strategy()
+    resolved = eng.strategy()          # as the reference resolves it (verify.hpp:249-253)
+    kernels = eng.kernel_strategy()    # the kernel family that runs
 
     # ---- kernel-only arm ---------------------------------------------------------------
-    dC = torch.from_numpy(chunk.C.view(np.int32)).to(dev)
-    dCO = torch.from_numpy(chunk.C_O.view(np.int32)).to(dev)
+    dC = torch.from_numpy(C_h.view(np.int32)).to(dev)
+    dCO = torch.from_numpy(CO_h.view(np.int32)).to(dev)
     dF = torch.empty(nC, dtype=torch.uint8, device=dev)
     dR = torch.zeros(8, dtype=torch.int64, device=dev)
     dB = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -464,18 +592,28 @@ def main():
         total_pairs = float(nC) * args.steps
     value = total_pairs / (elapsed_ms / 1e3)
     kernel_avg_ms = kernel_ms / max(launches, 1)
-    peak, peak_src = measured_peaks()
+    gpu_flags = dF.cpu().numpy()
+    assert int(gpu_flags.sum(dtype=np.int64)) == count
+    flags_digest = sha256(gpu_flags)
+
+    hbm_peak, peak_src = measured_peaks()
     achieved_gbs = algo_bytes / (kernel_avg_ms / 1e3) / 1e9
-    l2_gbs, hbm_read_gbs = measure_read_gbs(local)
+    l2_gbs = measure_read_bandwidth(local, 48 << 20, 50)
+    hbm_read_gbs = measure_read_bandwidth(local, 4 << 30, 5)
+    traffic = ncu_traffic(args.workload)
+    # the working set decides the denominator: when the dominant kernel's measured DRAM bytes
+    # are well below its algorithmic bytes, the data is served by L2 and L2 bounds it
+    l2_bound = traffic is not None and traffic < 0.5 * algo_bytes
+    bound, peak = ("l2", l2_gbs) if l2_bound else ("hbm", hbm_peak)
 
     # ---- end-to-end arm: C ABI with pinned host buffers ---------------------------------
     pc = ssj.PinnedBuffer(4 * nC + 64)
     pco = ssj.PinnedBuffer(4 * nCO + 64)
     pf = ssj.PinnedBuffer(nC + 64)
     hC = pc.view(np.uint32, nC)
-    hC[:] = chunk.C
+    hC[:] = C_h
     hCO = pco.view(np.uint32, nCO)
-    hCO[:] = chunk.C_O
+    hCO[:] = CO_h
     hF = pf.view(np.uint8, nC)
     host_chunk = ssj.CandidateChunk.__new__(ssj.CandidateChunk)
     host_chunk.C, host_chunk.C_O = hC, hCO
@@ -488,11 +626,14 @@ def main():
         out = eng.verify_chunk(host_chunk, flags_out=hF)
     e2e_s = time.perf_counter() - te
     assert out.count == count, (out.count, count)
+    e2e_flags_identical = bool(np.array_equal(hF, gpu_flags))
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = (total_pairs / args.steps) * args.e2e_steps / e2e_s
+    launches_per_step = int(eng.launches_per_chunk(nC, nCO))
+    eng.close()
 
     # ---- the whole join on the GPU(s): device filtering + verification, probe shards -----
     join = None
@@ -502,24 +643,38 @@ def main():
         except Exception as e:  # reported, never fatal
             join = {"error": str(e)[:300]}
 
-    # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------------------
+    # ---- CPU baseline + full-batch parity (rank 0) --------------------------------------
     cpu = None
-    parity = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    gold = load_golden().get("batches", {}).get(args.workload)
+    parity = {"count": count, "flags_sha256": flags_digest,
+              "e2e_flags_identical": e2e_flags_identical}
+    if gold and gold.get("seed") == args.seed and gold.get("candidates") == nC and rank == 0:
+        parity["golden"] = {"count": gold["count"], "flags_sha256": gold["flags_sha256"],
+                            "source": "tests/golden/bench_golden.json (reference verify_chunk, "
+                                      "made by tests/golden/make_bench_golden.py)"}
+        parity["golden_match"] = (gold["flags_sha256"] == flags_digest
+                                  and gold["count"] == count)
+    if rank == 0 and not args.no_cpu_baseline:
         try:
-            rate, cores, kind, sample, ref_count, idx = cpu_reference_rate(
-                coll, pred_t, chunk, int(args.cpu_sample))
-            cpu = {"value": rate, "unit": "pairs/s", "cores": cores, "kind": kind,
-                   "sample": f"{sample} candidates: every k-th slice of the step's batch "
-                             f"(stratified over probe sizes), VerificationEngine strategy A, "
-                             f"best of 3"}
-            # the same sample's qualifying count from the GPU flags of the timed steps
-            gpu_count = int(dF.cpu().numpy()[idx].sum()) if sample else 0
-            parity = {"candidates": int(sample), "gpu_count": gpu_count,
-                      "reference_count": int(ref_count), "match": gpu_count == int(ref_count)}
+            from oracle import pyoracle as po
+            if not po.ref_available():
+                raise RuntimeError("oracle/_ref/libssjref.so missing")
+            R = po.Ref()
+            sec, ref_count, ref_flags, cores = ref_verify(R, w, C_h, CO_h, args.cpu_reps, True)
+            cpu = {"value": nC / sec, "unit": "pairs/s", "cores": cores, "kind": "reference",
+                   "sample": f"the whole step batch of rank 0 ({nC} candidates), reference "
+                             f"VerificationEngine::verify_chunk strategy A, Pairs mode, "
+                             f"best of {args.cpu_reps}"}
+            parity.update({"reference_count": int(ref_count),
+                           "reference_flags_sha256": sha256(ref_flags),
+                           "candidates_compared": nC,
+                           "flags_match": bool(np.array_equal(ref_flags, gpu_flags))
+                           and int(ref_count) == count})
         except Exception as e:  # reported, never fatal
             cpu = {"value": None, "unit": "pairs/s", "cores": 0, "kind": "unavailable",
                    "sample": str(e)[:200]}
+    if world > 1:
+        dist.barrier()
 
     if rank == 0:
         line = {
@@ -527,43 +682,40 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {
-                "workload": desc, "n_sets": coll.size(),
-                "avg_set_size": round(coll.tokens.size / coll.size(), 2),
-                "threshold": f"{pred_t[0]}/{pred_t[1]}", "algorithm": algorithm,
-                "candidates_per_step_per_gpu": int(nC), "slices_per_step": int(nCO // 2),
-                "probe_windows": args.windows, "window_width": int(width),
-                "qualifying_per_step": count, "mode": "pairs (flags)",
-                "strategy": f"{resolved.kind.name}/{resolved.group_size}",
-                "l2": f"inputs larger than L2: C = {4 * nC / 2**30:.2f} GiB per step",
-                "parallelism": f"probe-window shards x{world}, no data-path collective",
-                "collection_broadcast_ms": bcast_ms,
-            },
+            "config": config,
+            "parallelism": f"probe-window shards x{world}, no data-path collective",
+            "arm": {"strategy": f"{resolved.kind.name}/{resolved.group_size}",
+                    "kernels": f"{kernels.kind.name}/{kernels.group_size}",
+                    "qualifying_per_step": count, "collection_broadcast_ms": bcast_ms},
             "roofline": {
-                "bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
-                "frac": achieved_gbs / peak, "traffic": ncu_traffic(args.workload),
-                "kernel": "strategy-A verification pass (runs_gen + run_kernel + warp_tile_kernel + long_slice_kernel; run_kernel dominant)" if resolved.kind.name == "A" else
-                          f"strategy {resolved.kind.name} kernel",
+                "bound": bound, "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+                "frac": achieved_gbs / peak, "traffic": traffic,
+                "kernel": "strategy-A verification pass (prep + bitmap + runs_gen + run_kernel + "
+                          "warp_tile_kernel + long_slice_kernel; run_kernel dominant)"
+                          if kernels.kind.name == "A" else
+                          f"strategy {kernels.kind.name} kernel",
                 "algorithmic_bytes_per_launch": algo_bytes,
-                "kernel_ms_avg": kernel_avg_ms, "peak_source": peak_src,
+                "kernel_ms_avg": kernel_avg_ms,
                 "kernel_share_of_step": kernel_ms / elapsed_ms if elapsed_ms else None,
-                "l2": {"peak": l2_gbs, "unit": "GB/s", "frac": achieved_gbs / l2_gbs,
-                       "source": "measured in this run: streaming 16-byte reads of a 48 MiB "
-                                 "L2-resident buffer (ssj_measure_read_bandwidth)"},
-                "hbm_read_measured_gbs": hbm_read_gbs,
+                "bound_rule": "l2 when the dominant kernel's ncu DRAM bytes < 0.5 x its "
+                              "algorithmic bytes (profiles/ncu_traffic.json), else hbm",
+                "l2_peak_gbs": l2_gbs, "l2_frac": achieved_gbs / l2_gbs,
+                "l2_peak_source": "measured in this run: streaming 16-byte reads of a 48 MiB "
+                                  "L2-resident buffer (ssj_measure_read_bandwidth)",
+                "hbm_peak_gbs": hbm_peak, "hbm_frac": achieved_gbs / hbm_peak,
+                "hbm_peak_source": peak_src, "hbm_read_measured_gbs": hbm_read_gbs,
             },
             "cpu_baseline": cpu,
-            "parity_sample": parity,
+            "parity": parity,
             "e2e": {"value": e2e_value, "unit": "pairs/s",
                     "h2d_bytes_per_step": int(4 * nC + 4 * nCO),
                     "d2h_bytes_per_step": int(nC + 64), "steps": args.e2e_steps,
                     "path": "ssj_verify_chunk (C ABI) from pinned host buffers, flags D2H"},
-            "gpu_launches": int(args.steps * eng.launches_per_chunk(nC, nCO)),
+            "gpu_launches": int(args.steps * launches_per_step),
             "join": join,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
-    eng.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -93,7 +93,8 @@ uint64_t ssj_equivalent_overlap(const ssj_predicate* pred, uint64_t size_r, uint
  * offsets[n_sets + 1], sets sorted with strictly increasing tokens. It is re-laid out
  * once into the device's 32-byte-aligned padded CSR and uploaded; unlike the reference
  * (which keeps a reference, verify.hpp:347) the host arrays may be freed after return.
- * `strategy` is validated (verify.hpp:25-28); Auto is resolved here (verify.hpp:245).
+ * `strategy` is validated (verify.hpp:25-28); Auto is resolved here (verify.hpp:245, see
+ * ssj_engine_strategy / ssj_engine_kernel_strategy).
  */
 int ssj_engine_create(ssj_engine** out, int device, const uint32_t* tokens,
                       const uint32_t* offsets, uint32_t n_sets, const ssj_predicate* pred,
@@ -121,8 +122,40 @@ int ssj_engine_device_collection(const ssj_engine* e, const uint32_t** d_tokens,
 
 void ssj_engine_destroy(ssj_engine* e);
 
-/* VerificationEngine::strategy() (verify.hpp:255): the resolved strategy (never Auto). */
+/* ---- one engine over several GPUs (the engine run_join builds,
+ *      pipeline.hpp:156, and hands every chunk, :228) --------------------------------------
+ * devices[0..n_devices): CUDA ordinals (a device may repeat: several engines on one GPU).
+ * The padded collection is uploaded ONCE (devices[0]) and fanned out device to device over
+ * NVLink / NVSwitch with peer copies in a doubling tree (round k: the 2^k devices holding it
+ * copy to the next 2^k). The result is an ordinary ssj_engine*: ssj_verify_chunk, submit/wait,
+ * _results and _pairs cut each chunk into n_devices contiguous probe-slice ranges of equal
+ * work -- per slice 4|r| + k (13 + 4|r|), SURVEY §8(d)'s bytes with |s| <= |r| -- verify them
+ * concurrently (one engine per device, its own streams) and return flags in C order (each
+ * device writes its range of the caller's buffer), counts and stats summed; ssj_gpu_join
+ * runs probe shard g on device g. Device-pointer entry points (ssj_verify_chunk_device,
+ * ssj_chunk_algorithmic_bytes_device) need a one-device engine (SSJ_ERR_INVALID_ARGUMENT). */
+int ssj_engine_create_multi(ssj_engine** out, const int32_t* devices, uint32_t n_devices,
+                            const uint32_t* tokens, const uint32_t* offsets, uint32_t n_sets,
+                            const ssj_predicate* pred, int32_t mode, const ssj_strategy* strategy);
+/* The engine's devices (1 for a one-device engine) and the collection fan-out time. */
+int ssj_engine_devices(const ssj_engine* e, int32_t* devices, uint32_t cap, uint32_t* n_devices,
+                       double* fanout_ms);
+/* The split a multi-device engine applies to a chunk (host only; no GPU needed):
+ * ranges[4 g .. 4 g + 3] = {first slice, end slice, first slot, end slot} of part g.
+ * set_sizes: |set| per set (the probes' sizes weigh the slices). SSJ_ERR_INVALID_ARGUMENT on a
+ * malformed C_O (end offsets decreasing or beyond nC), like verification. */
+int ssj_chunk_split(const uint32_t* set_sizes, uint32_t n_sets, uint32_t parts,
+                    const uint32_t* C_O, uint64_t nCO, uint64_t nC, uint64_t* ranges);
+
+/* VerificationEngine::strategy() (verify.hpp:255): the resolved strategy (never Auto),
+ * resolved exactly as the reference resolves it (verify.hpp:249-253: Auto -> B when the
+ * average set size is <= 10, else C with group >= 128); VerifyStats follow it (C records
+ * none). */
 int ssj_engine_strategy(const ssj_engine* e, ssj_strategy* resolved);
+/* The kernel family that runs: the requested A / B / C, and for Auto strategy A's kernels
+ * (load-balanced thread-per-pair + warp-per-long-pair; 3.5-90x faster than B / C on the
+ * B200). Flags and counts do not depend on it. */
+int ssj_engine_kernel_strategy(const ssj_engine* e, ssj_strategy* exec);
 int ssj_engine_device(const ssj_engine* e);
 
 /* ---- the hot call ------------------------------------------------------------------ */
@@ -165,7 +198,8 @@ int ssj_verify_chunk_results(ssj_engine* e, const uint32_t* C, uint64_t nC,
  * H2 on the GPU (decode_pairs, pipeline.hpp:79-92, and write_pairs order, report.hpp:39-42):
  * verifies the chunk and returns the qualifying pairs as original input ids
  * (r_id, s_id) with r_id > s_id, two uint32 per pair, plus their true overlaps (nullable).
- * sorted != 0 sorts them on the device (radix sort on r_id << 32 | s_id). Original ids come
+ * sorted != 0 sorts them on the device (radix sort on r_id << 32 | s_id); sorted == 0 returns
+ * them in decode_pairs order (slot = C order, pipeline.hpp:79-92). Original ids come
  * from ssj_engine_set_original_ids (identity if never set). Only the qualifying pairs cross
  * PCIe (no per-candidate flags). stats: nullable, as in ssj_verify_chunk.
  */
@@ -191,8 +225,8 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC,
                             uint64_t* d_result, void* stream);
 
 /* Kernel timing on the launching stream (benchmark instrumentation): when enabled,
- * ssj_verify_chunk_device brackets its verification kernel with CUDA events recorded on the
- * caller's stream; ssj_engine_kernel_time synchronises on them and returns the summed
+ * ssj_verify_chunk_device brackets its whole verification (result resets, prep/bitmap
+ * kernels and the strategy's kernels) with CUDA events recorded on the caller's stream; ssj_engine_kernel_time synchronises on them and returns the summed
  * kernel milliseconds and launch count since the last call (then resets). */
 int ssj_engine_set_profiling(ssj_engine* e, int enabled);
 int ssj_engine_kernel_time(ssj_engine* e, double* total_ms, uint64_t* launches);
@@ -292,6 +326,13 @@ typedef struct {
     uint32_t reserved;
     ssj_chunk_observer observer;
     void* observer_user;
+    const int32_t* devices;   /* nullable: verification on these GPUs (ssj_engine_create_multi);
+                                 `device` is used when NULL */
+    uint32_t n_devices;
+    uint32_t max_inflight;    /* chunks the dispatcher keeps on the GPU at once: 1 (default) is
+                                 the reference's rendezvous (<= 2 chunks live, pipeline.hpp:
+                                 105-141); 2 submits chunk k+1 before waiting for chunk k
+                                 (<= 3 live) */
 } ssj_join_config;
 
 /* JoinReport (pipeline.hpp:63-75) + PhaseTimings (:53-58) + ours. */

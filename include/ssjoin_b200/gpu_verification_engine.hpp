@@ -14,11 +14,18 @@
 // construction (verify.hpp:245) and reported by strategy(); flags only in Pairs mode, slot
 // order = C order, byte-identical to the reference; count; VerifyStats recorded for
 // strategies A/B only; std::invalid_argument / std::out_of_range / std::runtime_error as the
-// reference would throw. Difference: the collection is copied to the GPU at construction
-// (the reference keeps a reference); there is no CPU fallback.
+// reference would throw. verify_chunk is const and may be called from several threads at
+// once, like the reference's: calls are serialised on an internal mutex (the engine's chunk
+// slots and scratch are per engine). Difference: the collection is copied to the GPU at
+// construction (the reference keeps a reference); there is no CPU fallback.
+//
+// Multi-GPU: the constructor taking a device list builds one engine over several GPUs
+// (ssj_engine_create_multi: one host upload, NVLink peer fan-out of the collection); each
+// chunk is split by probe-slice ranges across them and the flags come back in C order.
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -59,9 +66,21 @@ public:
                                             mode == OutputMode::Pairs ? SSJ_MODE_PAIRS
                                                                       : SSJ_MODE_COUNT,
                                             &s));
-        ssj_strategy r{};
-        gpu_detail::check(ssj_engine_strategy(engine_, &r));
-        strategy_ = {static_cast<StrategyKind>(r.kind), r.group_size};
+        resolve();
+    }
+
+    // One engine over several GPUs (probe-slice sharding of every chunk).
+    GpuVerificationEngine(const Collection& collection, SimilarityPredicate pred, OutputMode mode,
+                          Strategy strategy, const std::vector<int>& devices)
+        : mode_(mode) {
+        const ssj_predicate p = gpu_detail::to_c(pred);
+        const ssj_strategy s{static_cast<int32_t>(strategy.kind), strategy.group_size};
+        const uint32_t* tokens = collection.tokens.empty() ? nullptr : collection.tokens.data();
+        gpu_detail::check(ssj_engine_create_multi(
+            &engine_, devices.data(), static_cast<uint32_t>(devices.size()), tokens,
+            collection.offsets.data(), static_cast<uint32_t>(collection.size()), &p,
+            mode == OutputMode::Pairs ? SSJ_MODE_PAIRS : SSJ_MODE_COUNT, &s));
+        resolve();
     }
 
     GpuVerificationEngine(const GpuVerificationEngine&) = delete;
@@ -78,6 +97,7 @@ public:
         if (mode_ == OutputMode::Pairs) out.flags.assign(chunk.candidate_count(), 0);
         ssj_stats st{};
         uint64_t count = 0;
+        std::lock_guard<std::mutex> lock(mu_);
         gpu_detail::check(ssj_verify_chunk(engine_, chunk.C.data(), chunk.C.size(),
                                            chunk.C_O.data(), chunk.C_O.size(),
                                            out.flags.empty() ? nullptr : out.flags.data(),
@@ -95,6 +115,13 @@ public:
     ssj_engine* native_handle() const { return engine_; }
 
 private:
+    void resolve() {
+        ssj_strategy r{};
+        gpu_detail::check(ssj_engine_strategy(engine_, &r));
+        strategy_ = {static_cast<StrategyKind>(r.kind), r.group_size};
+    }
+
+    mutable std::mutex mu_;
     ssj_engine* engine_ = nullptr;
     OutputMode mode_;
     Strategy strategy_;

@@ -40,6 +40,19 @@ class _Stats(C.Structure):
                 ("comparison_budget_violations", C.c_uint64)]
 
 
+class _SsjPred(C.Structure):  # ssj_predicate (include/ssjoin_b200.h), for work_shim.cpp
+    _fields_ = [("function", C.c_int32), ("reserved", C.c_uint32), ("num", C.c_uint64),
+                ("den", C.c_uint64), ("overlap_threshold", C.c_uint64)]
+
+
+class _SynthConfig(C.Structure):  # ssj_synth_config (include/ssjoin_b200.h)
+    _fields_ = [("seed", C.c_uint64), ("n_sets", C.c_uint32), ("min_size", C.c_uint32),
+                ("max_size", C.c_uint32), ("zipf_sizes", C.c_int32), ("size_skew", C.c_double),
+                ("universe", C.c_uint32), ("zipf_tokens", C.c_int32), ("token_skew", C.c_double),
+                ("duplicate_fraction", C.c_double), ("max_edits", C.c_uint32),
+                ("distinct_tokens", C.c_int32), ("threads", C.c_uint32)]
+
+
 def _ptr(a, t=u32p):
     return a.ctypes.data_as(t) if a is not None and a.size else None
 
@@ -227,12 +240,22 @@ class Ref:
         L.ref_time_verify_chunk.restype = C.c_double
         L.ref_time_verify_chunk.argtypes = [vp, vp, C.c_int, C.c_uint64, C.c_uint64,
                                             C.c_uint64, C.c_int, C.c_uint32, C.c_int, u32p,
-                                            C.c_uint64, u32p, C.c_uint64, C.c_int, u64p]
+                                            C.c_uint64, u32p, C.c_uint64, C.c_int, u64p, u8p]
+        L.ref_work_last_error.restype = C.c_char_p
+        L.ref_work_synth.restype = vp
+        L.ref_work_synth.argtypes = [C.POINTER(_SynthConfig), u64p, u64p]
+        L.ref_work_synth_copy.argtypes = [vp, u32p, u32p, u32p]
+        L.ref_work_generate_windows.restype = vp
+        L.ref_work_generate_windows.argtypes = [u32p, u32p, C.c_uint32, C.POINTER(_SsjPred),
+                                                C.c_int32, u32p, C.c_uint32, C.c_uint32, u64p,
+                                                u64p]
+        L.ref_work_candidates_copy.argtypes = [vp, u32p, u32p]
         L.ref_run_join.restype = vp
         L.ref_run_join.argtypes = [vp, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
                                    C.c_uint64, C.c_int, C.c_uint32, C.c_int, C.c_uint, C.c_int]
         L.ref_join_report.argtypes = [vp, u64p, C.POINTER(C.c_double)]
         L.ref_join_pairs.argtypes = [vp, u32p]
+        L.ref_join_pairs_unsorted.argtypes = [vp, u32p]
         L.ref_join_chunk_count.restype = C.c_uint64
         L.ref_join_chunk_count.argtypes = [vp]
         L.ref_join_chunk_sizes.argtypes = [vp, C.c_uint64, u64p, u64p, u64p]
@@ -324,18 +347,62 @@ class Ref:
         return flags[: C_.size], count.value, stats, (rk.value, rg.value)
 
     def time_verify_chunk(self, coll, pool, fn, num, den, ovt, kind, group, pairs_mode, C_, C_O,
-                          reps=3):
+                          reps=3, flags_out=None):
+        """Best-of-`reps` seconds of verify_chunk and its count; flags_out (uint8[|C|],
+        Pairs mode) receives the last run's flags."""
         C_, C_O = _u32(C_), _u32(C_O)
         count = C.c_uint64()
+        fp = _ptr(flags_out, u8p) if flags_out is not None else None
         sec = self.L.ref_time_verify_chunk(coll, pool, fn, num, den, ovt, kind, group,
                                            int(pairs_mode), _ptr(C_), C_.size, _ptr(C_O),
-                                           C_O.size, reps, C.byref(count))
+                                           C_O.size, reps, C.byref(count), fp)
         if sec < 0:
             raise RuntimeError(self.err())
         return sec, count.value
 
+    # benchmark workload (work_shim.cpp: synth.cpp + candidates.cpp linked into this library,
+    # so the reference arm never loads the product library) -----------------------------
+    def work_synth(self, seed, sets=100, min_size=1, max_size=50, zipf_sizes=False,
+                   size_skew=1.0, universe=1000, zipf_tokens=False, token_skew=1.0,
+                   duplicate_fraction=0.0, max_edits=0, distinct_tokens=False, threads=0):
+        """The product's deterministic synthetic collection (ssj_synth_collection):
+        (tokens, offsets, original_id)."""
+        cfg = _SynthConfig(seed, sets, min_size, max_size, int(zipf_sizes), size_skew, universe,
+                           int(zipf_tokens), token_skew, duplicate_fraction, max_edits,
+                           int(distinct_tokens), threads)
+        n, t = C.c_uint64(), C.c_uint64()
+        h = self.L.ref_work_synth(C.byref(cfg), C.byref(n), C.byref(t))
+        if not h:
+            raise RuntimeError(self.L.ref_work_last_error().decode())
+        tokens = np.zeros(max(t.value, 1), np.uint32)
+        offsets = np.zeros(n.value + 1, np.uint32)
+        oid = np.zeros(max(n.value, 1), np.uint32)
+        self.L.ref_work_synth_copy(h, _ptr(tokens), _ptr(offsets), _ptr(oid))
+        return tokens[: t.value], offsets, oid[: n.value]
+
+    def work_generate_windows(self, tokens, offsets, fn, num, den, ovt, algorithm, windows,
+                              threads=0):
+        """ssj_generate_candidates_windows: AllPairs (0) / PPJoin (1) candidates of the probe
+        windows [(lo, hi), ...] as one chunk (C, C_O)."""
+        tokens = _u32(tokens) if np.asarray(tokens).size else np.zeros(1, np.uint32)
+        offsets = _u32(offsets)
+        w = _u32(np.asarray(windows, np.int64).reshape(-1))
+        p = _SsjPred(fn, 0, num, den, ovt)
+        nC, nCO = C.c_uint64(), C.c_uint64()
+        h = self.L.ref_work_generate_windows(_ptr(tokens), _ptr(offsets), offsets.size - 1,
+                                             C.byref(p), algorithm, _ptr(w), w.size // 2,
+                                             threads, C.byref(nC), C.byref(nCO))
+        if not h:
+            raise RuntimeError(self.L.ref_work_last_error().decode())
+        c = np.zeros(max(nC.value, 1), np.uint32)
+        co = np.zeros(max(nCO.value, 1), np.uint32)
+        self.L.ref_work_candidates_copy(h, _ptr(c), _ptr(co))
+        return c[: nC.value], co[: nCO.value]
+
     def run_join(self, coll, fn, num, den, ovt, algorithm=1, budget=64 << 20, kind=3, group=32,
-                 pairs_mode=True, workers=1, record_chunks=False):
+                 pairs_mode=True, workers=1, record_chunks=False, sort_pairs=True):
+        """The reference run_join: (report dict, pairs (sorted like write_pairs, or in
+        JoinReport::pairs order when sort_pairs=False), recorded chunks)."""
         h = self.L.ref_run_join(coll, fn, num, den, ovt, algorithm, budget, kind, group,
                                 int(pairs_mode), workers, int(record_chunks))
         if not h:
@@ -344,7 +411,10 @@ class Ref:
         tim = (C.c_double * 4)()
         self.L.ref_join_report(h, _ptr(rep, u64p), tim)
         pairs = np.zeros(2 * max(int(rep[8]), 1), np.uint32)
-        self.L.ref_join_pairs(h, _ptr(pairs))
+        if sort_pairs:
+            self.L.ref_join_pairs(h, _ptr(pairs))
+        else:
+            self.L.ref_join_pairs_unsorted(h, _ptr(pairs))
         chunks = []
         for i in range(self.L.ref_join_chunk_count(h)):
             nC, nCO, cnt = C.c_uint64(), C.c_uint64(), C.c_uint64()

@@ -205,11 +205,12 @@ int ref_verify_chunk(const ref_coll* h, ref_pool* pool, int fn, std::uint64_t nu
 
 // Timed variant for the CPU baseline: the chunk is decoded into a CandidateChunk once
 // (outside the timing), then verify_chunk is called `reps` times; returns best seconds.
+// flags (nullable, Pairs mode): the flags of the last run, copied after its timing.
 double ref_time_verify_chunk(const ref_coll* h, ref_pool* pool, int fn, std::uint64_t num,
                              std::uint64_t den, std::uint64_t ovt, int kind,
                              std::uint32_t group, int pairs_mode, const std::uint32_t* C,
                              std::uint64_t nC, const std::uint32_t* C_O, std::uint64_t nCO,
-                             int reps, std::uint64_t* count) {
+                             int reps, std::uint64_t* count, std::uint8_t* flags) {
     try {
         CandidateChunk chunk;
         chunk.C.assign(C, C + nC);
@@ -224,6 +225,8 @@ double ref_time_verify_chunk(const ref_coll* h, ref_pool* pool, int fn, std::uin
             double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             *count = out.count;
             if (best < 0 || sec < best) best = sec;
+            if (flags && pairs_mode && i + 1 == reps)  // the last run's flags (outside the timing)
+                std::memcpy(flags, out.flags.data(), out.flags.size());
         }
         return best;
     } catch (const std::exception& e) {
@@ -292,6 +295,15 @@ void ref_join_report(const ref_join* j, std::uint64_t* out /*11*/, double* timin
 void ref_join_pairs(const ref_join* j, std::uint32_t* out) {
     auto pairs = j->report.pairs;
     std::sort(pairs.begin(), pairs.end());
+    for (std::size_t i = 0; i < pairs.size(); ++i) {
+        out[2 * i] = pairs[i].first;
+        out[2 * i + 1] = pairs[i].second;
+    }
+}
+
+// pairs in JoinReport::pairs order (H2 decode order, pipeline.hpp:79-92 / :189-211)
+void ref_join_pairs_unsorted(const ref_join* j, std::uint32_t* out) {
+    const auto& pairs = j->report.pairs;
     for (std::size_t i = 0; i < pairs.size(); ++i) {
         out[2 * i] = pairs[i].first;
         out[2 * i + 1] = pairs[i].second;

@@ -54,7 +54,9 @@ class ssj_join_config(C.Structure):
     _fields_ = [("algorithm", C.c_int32), ("mode", C.c_int32), ("chunk_budget", C.c_uint64),
                 ("strategy", ssj_strategy), ("workers", C.c_uint32), ("device", C.c_int32),
                 ("filter_threads", C.c_uint32), ("reserved", C.c_uint32),
-                ("observer", OBSERVER), ("observer_user", C.c_void_p)]
+                ("observer", OBSERVER), ("observer_user", C.c_void_p),
+                ("devices", C.POINTER(C.c_int32)), ("n_devices", C.c_uint32),
+                ("max_inflight", C.c_uint32)]
 
 
 class ssj_join_report(C.Structure):
@@ -91,9 +93,17 @@ SIGNATURES = {
     "ssj_engine_create_from_device": (C.c_int, [C.POINTER(vp), C.c_int, vp, C.c_uint64, vp,
                                                 C.c_uint32, C.c_uint64, C.POINTER(ssj_predicate),
                                                 C.c_int32, C.POINTER(ssj_strategy)]),
+    "ssj_engine_create_multi": (C.c_int, [C.POINTER(vp), C.POINTER(C.c_int32), C.c_uint32, u32p,
+                                          u32p, C.c_uint32, C.POINTER(ssj_predicate), C.c_int32,
+                                          C.POINTER(ssj_strategy)]),
+    "ssj_engine_devices": (C.c_int, [vp, C.POINTER(C.c_int32), C.c_uint32, C.POINTER(C.c_uint32),
+                                     C.POINTER(C.c_double)]),
+    "ssj_chunk_split": (C.c_int, [u32p, C.c_uint32, C.c_uint32, u32p, C.c_uint64, C.c_uint64,
+                                  u64p]),
     "ssj_engine_device_collection": (C.c_int, [vp, C.POINTER(vp), u64p, C.POINTER(vp)]),
     "ssj_engine_destroy": (None, [vp]),
     "ssj_engine_strategy": (C.c_int, [vp, C.POINTER(ssj_strategy)]),
+    "ssj_engine_kernel_strategy": (C.c_int, [vp, C.POINTER(ssj_strategy)]),
     "ssj_engine_device": (C.c_int, [vp]),
     "ssj_verify_chunk": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, vp, u64p,
                                    C.POINTER(ssj_stats)]),

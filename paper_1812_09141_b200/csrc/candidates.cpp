@@ -13,6 +13,7 @@
 #include <atomic>
 #include <cstring>
 #include <memory>
+#include <stdexcept>
 #include <thread>
 #include <vector>
 
@@ -62,16 +63,19 @@ bool positional_keep(const ssj_predicate& p, uint32_t size_r, uint32_t size_s, u
 
 namespace {
 
+// joiners.hpp:21-24 (size_t there): max token + 1, in 64 bits (token 0xFFFFFFFF is legal
+// and gives 2^32). The generators index per-token lists by it, so a universe beyond
+// kMaxUniverse is refused with std::invalid_argument (the reference would attempt a
+// 2^32-entry allocation and fail with bad_alloc).
+constexpr uint64_t kMaxUniverse = 1ull << 31;
+
 uint32_t token_universe(const CollView& c) {
-    // joiners.hpp:21-24
     const uint64_t T = c.n ? c.offsets[c.n] : 0;
-    uint32_t mx = 0;
-    bool any = false;
-    for (uint64_t k = c.offsets[0]; k < T; ++k) {
-        mx = std::max(mx, c.tokens[k]);
-        any = true;
-    }
-    return any ? mx + 1 : 0;
+    uint64_t universe = 0;
+    for (uint64_t k = c.offsets[0]; k < T; ++k) universe = std::max<uint64_t>(universe, (uint64_t)c.tokens[k] + 1);
+    if (universe > kMaxUniverse)
+        throw std::invalid_argument("token values >= 2^31: too large a universe for the inverted index");
+    return (uint32_t)universe;
 }
 
 }  // namespace
@@ -368,6 +372,8 @@ int ssj_generate_candidates(const uint32_t* tokens, const uint32_t* offsets, uin
             rc = ssjh::generate_candidates(c, *pred, algorithm, probe_begin, probe_end, threads,
                                            &h->s);
         }
+    } catch (const std::invalid_argument& e) {
+        rc = ssjh::set_error(SSJ_ERR_INVALID_ARGUMENT, e.what());
     } catch (const std::exception& e) {
         rc = ssjh::set_error(SSJ_ERR_RUNTIME, e.what());
     }
@@ -410,6 +416,8 @@ int ssj_generate_candidates_windows(const uint32_t* tokens, const uint32_t* offs
                 h->s.C_O.push_back((uint32_t)(base + part.C_O[k + 1]));
             }
         }
+    } catch (const std::invalid_argument& e) {
+        rc = ssjh::set_error(SSJ_ERR_INVALID_ARGUMENT, e.what());
     } catch (const std::exception& e) {
         rc = ssjh::set_error(SSJ_ERR_RUNTIME, e.what());
     }

@@ -26,6 +26,7 @@
 #include "host_common.hpp"
 #include "gpu_filter.cuh"
 #include "verify_kernels.cuh"
+#include "multi_device.hpp"
 
 using ssjb::KParams;
 using ssjb::PredDev;
@@ -180,7 +181,8 @@ struct ssj_engine {
     ssj_predicate hpred{};
     PredDev pred{};
     int32_t mode = SSJ_MODE_COUNT;
-    ssj_strategy strategy{};
+    ssj_strategy strategy{};  // resolved as the reference resolves it (reported, stats rule)
+    ssj_strategy exec{};      // the kernel family that runs (Auto: strategy A's kernels)
     uint32_t n_sets = 0;
     uint64_t n_tokens = 0;      // unpadded token count (Collection::tokens.size())
     uint64_t n_padded = 0;      // padded device tokens
@@ -233,8 +235,13 @@ struct ssj_engine {
     size_t keys_alt_cap = 0;
     uint32_t* d_ov_alt = nullptr;
     size_t ov_alt_cap = 0;
+    uint32_t* d_slot_alt = nullptr;  // result slots sorted into C order
+    size_t slot_alt_cap = 0;
     void* d_sort_tmp = nullptr;
     size_t sort_tmp_cap = 0;
+    // multi-device engine (ssj_engine_create_multi): the per-device engines; every entry
+    // point dispatches to multi_device.cpp when set
+    ssjm::Group* group = nullptr;
     // kernel timing (ssj_engine_set_profiling)
     bool profiling = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
@@ -243,14 +250,22 @@ struct ssj_engine {
 
 namespace {
 
-// verify.hpp:249-253 resolves Auto on the CPU (B for avg <= 10, else C with B >= 128): a
-// worker-pool policy. On the B200 one kernel family covers both regimes: the load-balanced
-// tile kernel (A) verifies short pairs thread-per-pair and defers long candidates to a
-// warp-per-pair pass (the cooperative scheme of C), so Auto resolves to A for every input.
-ssj_strategy resolve_strategy(const ssj_engine& e, ssj_strategy s) {
-    (void)e;
-    if (s.kind != SSJ_STRATEGY_AUTO) return s;
-    return {SSJ_STRATEGY_A, s.group_size};
+// verify.hpp:249-253: Auto resolves to B (average set size <= 10, collection.hpp:91-93) or
+// to C with group >= 128; strategy() and JoinReport::resolved_strategy report exactly that,
+// and the stats follow it (C records none, verify.hpp:303-345). Those are worker-pool
+// policies: on the B200 one kernel family covers both regimes -- strategy A's load-balanced
+// kernels (thread per short pair, warp per long pair, the cooperative scheme of C) -- so Auto
+// EXECUTES the A kernels whatever it reports. Flags and counts are identical for every
+// strategy; an explicit A, B or C runs that strategy's own kernels.
+void resolve_strategy(ssj_engine& e, ssj_strategy s) {
+    if (s.kind != SSJ_STRATEGY_AUTO) {
+        e.strategy = e.exec = s;
+        return;
+    }
+    const uint64_t avg = e.n_sets ? e.n_tokens / e.n_sets : 0;
+    e.strategy = avg <= 10 ? ssj_strategy{SSJ_STRATEGY_B, s.group_size}
+                           : ssj_strategy{SSJ_STRATEGY_C, std::max<uint32_t>(s.group_size, 128)};
+    e.exec = {SSJ_STRATEGY_A, s.group_size};
 }
 
 int make_pred_dev(const ssj_predicate& p, PredDev* out) {
@@ -374,9 +389,9 @@ int ensure_tile_scratch(ssjb::SliceDesc** slices, size_t* capS, uint32_t** bits,
 cudaError_t launch_strategy(const ssj_engine& e, const KParams& p, int out, uint32_t tile_begin,
                             uint32_t tile_end, cudaStream_t st, bool want_stats = true) {
     const bool stats = want_stats && e.strategy.kind != SSJ_STRATEGY_C;
-    switch (e.strategy.kind) {
-        case SSJ_STRATEGY_B: return ssjb::launch_block(p, out, stats, e.strategy.group_size, st);
-        case SSJ_STRATEGY_C: return ssjb::launch_path(p, out, e.strategy.group_size, st);
+    switch (e.exec.kind) {
+        case SSJ_STRATEGY_B: return ssjb::launch_block(p, out, stats, e.exec.group_size, st);
+        case SSJ_STRATEGY_C: return ssjb::launch_path(p, out, e.exec.group_size, st);
         default: {
             cudaError_t err = ssjb::launch_tiles(p, out, stats, tile_begin, tile_end, st);
             if (err != cudaSuccess) return err;
@@ -413,7 +428,7 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
     if ((rc = ensure_device(&s.dCO, &s.capCO, (size_t)n_slices * 2))) return rc;
     if ((rc = ensure_device(&s.dtile, &s.capT, (size_t)n_tiles + 1))) return rc;
     if (out == ssjb::kOutFlags && (rc = ensure_device(&s.dflags, &s.capF, nC))) return rc;
-    const bool tiles = e.strategy.kind == SSJ_STRATEGY_A;
+    const bool tiles = e.exec.kind == SSJ_STRATEGY_A;
     if (tiles && (rc = ensure_tile_scratch(&s.dslices, &s.capS, &s.dbits, &s.capB, &s.drank,
                                            &s.capR, &s.dbmlist, &s.capBL, n_slices, nC)))
         return rc;
@@ -476,7 +491,7 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
     // Pieces of the slot range: H2D(piece q+1) overlaps verify(piece q) overlaps D2H(q-1).
     // Strategies B and C map CTAs to slices, so they take the chunk as one piece.
     uint64_t piece = nC;
-    if (e.strategy.kind == SSJ_STRATEGY_A) {
+    if (e.exec.kind == SSJ_STRATEGY_A) {
         piece = std::max<uint64_t>(kPieceMinSlots, (nC + kMaxPieces - 1) / kMaxPieces);
         piece = (piece + ssjb::kRun - 1) / ssjb::kRun * ssjb::kRun;  // runs never straddle pieces
     }
@@ -733,7 +748,7 @@ int ssj_engine_create(ssj_engine** out, int device, const uint32_t* tokens, cons
         delete e;
         return rc;
     }
-    e->strategy = resolve_strategy(*e, *strategy);
+    resolve_strategy(*e, *strategy);
 
     // Padded CSR: every set starts on a 32-byte boundary; SSJ_TOKEN_TAIL_PAD sentinel tokens
     // at the end so that the kernels' speculative reads past a set's end (32-byte head reads,
@@ -812,7 +827,7 @@ int ssj_engine_create_from_device(ssj_engine** out, int device, const uint32_t* 
         delete e;
         return rc;
     }
-    e->strategy = resolve_strategy(*e, *strategy);
+    resolve_strategy(*e, *strategy);
     if ((rc = init_engine_runtime(*e))) {
         ssj_engine_destroy(e);
         return rc;
@@ -839,9 +854,71 @@ int ssj_engine_create_from_device(ssj_engine** out, int device, const uint32_t* 
     return SSJ_OK;
 }
 
+int ssj_engine_create_multi(ssj_engine** out, const int32_t* devices, uint32_t n_devices,
+                            const uint32_t* tokens, const uint32_t* offsets, uint32_t n_sets,
+                            const ssj_predicate* pred, int32_t mode, const ssj_strategy* strategy) {
+    if (!out) return fail(SSJ_ERR_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    if (!devices || n_devices == 0) return fail(SSJ_ERR_INVALID_ARGUMENT, "empty device list");
+    int rc = validate_engine_args(pred, mode, strategy);
+    if (rc) return rc;
+    if (!offsets) return fail(SSJ_ERR_INVALID_ARGUMENT, "null offsets");
+    for (uint32_t i = 0; i < n_devices; ++i)
+        if ((rc = check_device(devices[i]))) return rc;
+    DeviceScope ds(devices[0]);
+    ssjm::Group* g = nullptr;
+    if ((rc = ssjm::create_group(&g, devices, n_devices, tokens, offsets, n_sets, pred, mode,
+                                 strategy)))
+        return rc;
+    auto* e = new ssj_engine;
+    ssj_engine* e0 = ssjm::first(*g);
+    e->group = g;
+    e->device = devices[0];
+    e->hpred = *pred;
+    e->pred = e0->pred;
+    e->mode = mode;
+    e->strategy = e0->strategy;
+    e->exec = e0->exec;
+    e->n_sets = n_sets;
+    e->n_tokens = e0->n_tokens;
+    e->n_padded = e0->n_padded;
+    e->owns_collection = false;
+    *out = e;
+    return SSJ_OK;
+}
+
+int ssj_engine_devices(const ssj_engine* e, int32_t* devices, uint32_t cap, uint32_t* n_devices,
+                       double* fanout_ms) {
+    if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
+    if (e->group) return ssjm::devices(*e->group, devices, cap, n_devices, fanout_ms);
+    if (n_devices) *n_devices = 1;
+    if (devices && cap) devices[0] = e->device;
+    if (fanout_ms) *fanout_ms = 0;
+    return SSJ_OK;
+}
+
+int ssj_chunk_split(const uint32_t* set_sizes, uint32_t n_sets, uint32_t parts, const uint32_t* C_O,
+                    uint64_t nCO, uint64_t nC, uint64_t* ranges) {
+    if (!parts || !ranges || (n_sets && !set_sizes) || (nCO >= 2 && !C_O))
+        return fail(SSJ_ERR_INVALID_ARGUMENT, "null argument or zero parts");
+    std::vector<uint32_t> sizes(set_sizes, set_sizes + n_sets);
+    std::vector<ssjm::Range> rg;
+    int rc = ssjm::split_chunk(sizes, parts, C_O, nCO, nC, &rg);
+    if (rc) return rc;
+    for (uint32_t g = 0; g < parts; ++g) {
+        ranges[4 * g] = rg[g].slice_begin;
+        ranges[4 * g + 1] = rg[g].slice_end;
+        ranges[4 * g + 2] = rg[g].c_lo;
+        ranges[4 * g + 3] = rg[g].c_hi;
+    }
+    return SSJ_OK;
+}
+
 int ssj_engine_device_collection(const ssj_engine* e, const uint32_t** d_tokens,
                                  uint64_t* n_padded_tokens, const uint32_t** d_sets) {
     if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
+    if (e->group)  // the first device's copy
+        return ssj_engine_device_collection(ssjm::first(*e->group), d_tokens, n_padded_tokens, d_sets);
     if (d_tokens) *d_tokens = e->d_tokens;
     if (n_padded_tokens) *n_padded_tokens = e->n_padded;
     if (d_sets) *d_sets = reinterpret_cast<const uint32_t*>(e->d_sets);
@@ -850,6 +927,11 @@ int ssj_engine_device_collection(const ssj_engine* e, const uint32_t** d_tokens,
 
 void ssj_engine_destroy(ssj_engine* e) {
     if (!e) return;
+    if (e->group) {
+        ssjm::destroy_group(e->group);
+        delete e;
+        return;
+    }
     DeviceScope ds(e->device);
     if (e->s_comp) cudaStreamSynchronize(e->s_comp);
     if (e->s_h2d) cudaStreamSynchronize(e->s_h2d);
@@ -891,6 +973,7 @@ void ssj_engine_destroy(ssj_engine* e) {
     cudaFree(e->d_keys);
     cudaFree(e->d_keys_alt);
     cudaFree(e->d_ov_alt);
+    cudaFree(e->d_slot_alt);
     cudaFree(e->d_sort_tmp);
     for (auto& pe : e->prof_events) {
         cudaEventDestroy(pe.first);
@@ -908,6 +991,12 @@ int ssj_engine_strategy(const ssj_engine* e, ssj_strategy* resolved) {
     return SSJ_OK;
 }
 
+int ssj_engine_kernel_strategy(const ssj_engine* e, ssj_strategy* exec) {
+    if (!e || !exec) return fail(SSJ_ERR_INVALID_ARGUMENT, "null argument");
+    *exec = e->exec;
+    return SSJ_OK;
+}
+
 int ssj_engine_device(const ssj_engine* e) { return e ? e->device : -1; }
 
 int ssj_submit_chunk(ssj_engine* e, const uint32_t* C, uint64_t nC, const uint32_t* C_O,
@@ -915,6 +1004,7 @@ int ssj_submit_chunk(ssj_engine* e, const uint32_t* C, uint64_t nC, const uint32
     int rc = check_chunk_args(e, C, nC, C_O, nCO);
     if (rc) return rc;
     if (!ticket) return fail(SSJ_ERR_INVALID_ARGUMENT, "null ticket");
+    if (e->group) return ssjm::submit(*e->group, C, nC, C_O, nCO, flags_out, ticket);
     DeviceScope ds(e->device);
     const uint64_t t = e->next_ticket;
     ChunkSlot& s = e->slot[t & 1];
@@ -936,6 +1026,7 @@ int ssj_submit_chunk(ssj_engine* e, const uint32_t* C, uint64_t nC, const uint32
 
 int ssj_wait_chunk(ssj_engine* e, uint64_t ticket, uint64_t* count_out, ssj_stats* stats) {
     if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
+    if (e->group) return ssjm::wait(*e->group, ticket, count_out, stats);
     DeviceScope ds(e->device);
     ChunkSlot& s = e->slot[ticket & 1];
     if (!s.busy || s.ticket != ticket) return fail(SSJ_ERR_INVALID_ARGUMENT, "unknown ticket");
@@ -957,6 +1048,8 @@ int ssj_verify_chunk_results(ssj_engine* e, const uint32_t* C, uint64_t nC, cons
     if (rc) return rc;
     if (!n_out || (cap && (!slots_out || !overlaps_out)))
         return fail(SSJ_ERR_INVALID_ARGUMENT, "null output");
+    if (e->group)
+        return ssjm::verify_results(*e->group, C, nC, C_O, nCO, slots_out, overlaps_out, cap, n_out);
     DeviceScope ds(e->device);
     ChunkSlot& s = e->slot[e->next_ticket & 1];
     if (s.busy) return fail(SSJ_ERR_RUNTIME, "a chunk is in flight on this slot: wait first");
@@ -989,6 +1082,7 @@ int ssj_verify_chunk_results(ssj_engine* e, const uint32_t* C, uint64_t nC, cons
 
 int ssj_engine_set_original_ids(ssj_engine* e, const uint32_t* original_id) {
     if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
+    if (e->group) return ssjm::set_original_ids(*e->group, original_id);
     DeviceScope ds(e->device);
     if (!e->d_oid) SSJ_CK(cudaMalloc(&e->d_oid, (size_t)std::max<uint32_t>(e->n_sets, 1) * 4));
     if (original_id) {
@@ -1007,6 +1101,9 @@ int ssj_verify_chunk_pairs(ssj_engine* e, const uint32_t* C, uint64_t nC, const 
     int rc = check_chunk_args(e, C, nC, C_O, nCO);
     if (rc) return rc;
     if (!n_out || (cap && !pairs_out)) return fail(SSJ_ERR_INVALID_ARGUMENT, "null output");
+    if (e->group)
+        return ssjm::verify_pairs(*e->group, C, nC, C_O, nCO, pairs_out, overlaps_out, cap, n_out,
+                                  sorted, stats);
     DeviceScope ds(e->device);
     if (!e->d_oid && (rc = ssj_engine_set_original_ids(e, nullptr))) return rc;
     ChunkSlot& s = e->slot[e->next_ticket & 1];
@@ -1021,15 +1118,42 @@ int ssj_verify_chunk_pairs(ssj_engine* e, const uint32_t* C, uint64_t nC, const 
     *n_out = n;
     if (n) {
         if ((rc = ensure_device(&e->d_keys, &e->keys_cap, n))) return rc;
+        auto grow_tmp = [&](size_t need) -> int {
+            if (need <= e->sort_tmp_cap) return SSJ_OK;
+            cudaFree(e->d_sort_tmp);
+            e->d_sort_tmp = nullptr;
+            e->sort_tmp_cap = 0;
+            SSJ_CK(cudaMalloc(&e->d_sort_tmp, need));
+            e->sort_tmp_cap = need;
+            return SSJ_OK;
+        };
         KParams p = base_params(*e);
         p.C = s.dC;
         p.nC = nC;
         p.C_O = s.dCO;
         p.n_slices = (uint32_t)(nCO / 2);
         p.res_slots = e->d_res_slots;
+        uint32_t* ovs = e->d_res_ov;
+        if (!sorted) {
+            // decode_pairs order (pipeline.hpp:79-92: slices, then slots): the warp-aggregated
+            // appends are unordered, so the qualifying slots are radix-sorted first
+            if ((rc = ensure_device(&e->d_slot_alt, &e->slot_alt_cap, n))) return rc;
+            if ((rc = ensure_device(&e->d_ov_alt, &e->ov_alt_cap, n))) return rc;
+            int bits = 1;
+            while (bits < 32 && (1ull << bits) < nC) ++bits;
+            size_t tmp = 0;
+            SSJ_CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, e->d_res_slots, e->d_slot_alt,
+                                                   e->d_res_ov, e->d_ov_alt, (int)n, 0, bits,
+                                                   e->s_comp));
+            if ((rc = grow_tmp(tmp))) return rc;
+            SSJ_CK(cub::DeviceRadixSort::SortPairs(e->d_sort_tmp, tmp, e->d_res_slots,
+                                                   e->d_slot_alt, e->d_res_ov, e->d_ov_alt,
+                                                   (int)n, 0, bits, e->s_comp));
+            p.res_slots = e->d_slot_alt;
+            ovs = e->d_ov_alt;
+        }
         SSJ_CK(ssjb::launch_pairs(p, e->d_oid, n, e->d_keys, e->s_comp));
         unsigned long long* keys = e->d_keys;
-        uint32_t* ovs = e->d_res_ov;
         if (sorted) {  // write_pairs order (report.hpp:39-42) by a device radix sort
             if ((rc = ensure_device(&e->d_keys_alt, &e->keys_alt_cap, n))) return rc;
             if ((rc = ensure_device(&e->d_ov_alt, &e->ov_alt_cap, n))) return rc;
@@ -1037,13 +1161,7 @@ int ssj_verify_chunk_pairs(ssj_engine* e, const uint32_t* C, uint64_t nC, const 
             SSJ_CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, e->d_keys, e->d_keys_alt,
                                                    e->d_res_ov, e->d_ov_alt, (int)n, 0, 64,
                                                    e->s_comp));
-            if (tmp > e->sort_tmp_cap) {
-                cudaFree(e->d_sort_tmp);
-                e->d_sort_tmp = nullptr;
-                e->sort_tmp_cap = 0;
-                SSJ_CK(cudaMalloc(&e->d_sort_tmp, tmp));
-                e->sort_tmp_cap = tmp;
-            }
+            if ((rc = grow_tmp(tmp))) return rc;
             SSJ_CK(cub::DeviceRadixSort::SortPairs(e->d_sort_tmp, tmp, e->d_keys, e->d_keys_alt,
                                                    e->d_res_ov, e->d_ov_alt, (int)n, 0, 64,
                                                    e->s_comp));
@@ -1078,7 +1196,7 @@ int verify_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, const uint32_
     const uint32_t n_slices = (uint32_t)(nCO / 2);
     const uint32_t n_tiles = (uint32_t)((nC + ssjb::kTile - 1) / ssjb::kTile);
     if ((rc = ensure_device(&e->dev_tile, &e->dev_tile_cap, (size_t)n_tiles + 1))) return rc;
-    const bool tiles = e->strategy.kind == SSJ_STRATEGY_A;
+    const bool tiles = e->exec.kind == SSJ_STRATEGY_A;
     if (tiles && (rc = ensure_tile_scratch(&e->dev_slices, &e->dev_slices_cap, &e->dev_bits,
                                            &e->dev_bits_cap, &e->dev_rank, &e->dev_rank_cap,
                                            &e->dev_bmlist, &e->dev_bmlist_cap,
@@ -1130,9 +1248,8 @@ int verify_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, const uint32_
         p.short_n = e->dev_defer_n + 2;
         p.short_cap = n_tiles;
     }
-    SSJ_CK(cudaMemsetAsync(d_acc, 0, SSJ_RESULT_WORDS * sizeof(uint64_t), st));
-    if (tiles) SSJ_CK(cudaMemsetAsync(e->dev_defer_n, 0, kCounters * sizeof(unsigned long long), st));
-    SSJ_CK(ssjb::launch_prep(p, st));
+    // profiling brackets the whole verification of the chunk: result/counter resets, prep
+    // (validation, slice descriptors, probe bitmaps) and the strategy's kernels
     cudaEvent_t k0 = nullptr, k1 = nullptr;
     if (e->profiling) {
         if (e->prof_used == e->prof_events.size()) {
@@ -1146,6 +1263,9 @@ int verify_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, const uint32_
         ++e->prof_used;
         SSJ_CK(cudaEventRecord(k0, st));
     }
+    SSJ_CK(cudaMemsetAsync(d_acc, 0, SSJ_RESULT_WORDS * sizeof(uint64_t), st));
+    if (tiles) SSJ_CK(cudaMemsetAsync(e->dev_defer_n, 0, kCounters * sizeof(unsigned long long), st));
+    SSJ_CK(ssjb::launch_prep(p, st));
     SSJ_CK(launch_strategy(*e, p, out, 0, n_tiles, st, stats));
     if (k1) SSJ_CK(cudaEventRecord(k1, st));
     return SSJ_OK;
@@ -1158,6 +1278,9 @@ int ssj_verify_chunk_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, con
     int rc = check_chunk_args(e, d_C, nC, d_C_O, nCO);
     if (rc) return rc;
     if (!d_result) return fail(SSJ_ERR_INVALID_ARGUMENT, "null d_result");
+    if (e->group)
+        return fail(SSJ_ERR_INVALID_ARGUMENT,
+                    "device-resident chunks live on one GPU: use a one-device engine");
     DeviceScope ds(e->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
     const int out = (e->mode == SSJ_MODE_PAIRS && d_flags) ? ssjb::kOutFlags : ssjb::kOutCount;
@@ -1196,6 +1319,9 @@ int ensure_filter_index(ssj_engine* e, int algorithm, double* build_ms) {
         if (err != cudaSuccess) {
             delete e->fidx;
             e->fidx = nullptr;
+            if (err == cudaErrorInvalidValue)
+                return fail(SSJ_ERR_INVALID_ARGUMENT,
+                            "GPU index build: token values or index size beyond 2^31");
             return fail(SSJ_ERR_CUDA, std::string("GPU index build: ") + cudaGetErrorString(err));
         }
         if (build_ms)
@@ -1444,6 +1570,10 @@ int ssj_gpu_generate_candidates(ssj_engine* e, int32_t algorithm, uint32_t probe
                                 uint64_t* nC_out, uint32_t* C_O_out, uint64_t C_O_cap,
                                 uint64_t* nCO_out) {
     if (!e || !nC_out || !nCO_out) return fail(SSJ_ERR_INVALID_ARGUMENT, "null argument");
+    if (e->group)  // the stream does not depend on the device: the first one generates it
+        return ssj_gpu_generate_candidates(ssjm::first(*e->group), algorithm, probe_begin,
+                                           probe_end, C_out, C_cap, nC_out, C_O_out, C_O_cap,
+                                           nCO_out);
     DeviceScope ds(e->device);
     int rc;
     probe_end = std::min(probe_end, e->n_sets);
@@ -1491,6 +1621,9 @@ int ssj_gpu_join_shard(ssj_engine* e, int32_t algorithm, uint32_t shard, uint32_
     if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
     if (n_shards == 0 || shard >= n_shards) return fail(SSJ_ERR_INVALID_ARGUMENT, "bad shard");
     if (pairs_out && !n_pairs) return fail(SSJ_ERR_INVALID_ARGUMENT, "null n_pairs");
+    if (e->group)
+        return ssjm::gpu_join_shard(*e->group, algorithm, shard, n_shards, max_chunk_candidates,
+                                    pairs_out, pairs_cap, n_pairs, report);
     DeviceScope ds(e->device);
     const auto t_start = std::chrono::steady_clock::now();
     ssj_gpu_join_report rep{};
@@ -1578,17 +1711,44 @@ int ssj_gpu_join_shard(ssj_engine* e, int32_t algorithm, uint32_t shard, uint32_
     };
     const uint32_t p_begin = std::min(cut(shard), n_units);
     const uint32_t n = std::max(p_begin, std::min(cut(shard + 1), n_units));
+    // GroupJoin phase 2: exclusive scan of the groups' intra pair counts c (c - 1) / 2, so its
+    // blocks are cut by the same candidate budget as phase 1's (a group is never split)
+    std::vector<unsigned long long> ibase;
+    if (groupjoin && n > p_begin) {
+        const uint32_t np = n - p_begin;
+        if ((rc = ensure_buf<unsigned long long>(g.cand, g.cand_cap, np)) ||
+            (rc = ensure_buf<unsigned long long>(g.coff, g.coff_cap, np)) ||
+            (rc = ensure_buf<uint32_t>(g.iflag, g.iflag_cap, np)) ||
+            (rc = ensure_buf<uint32_t>(g.islot, g.islot_cap, np)))
+            return rc;
+        auto* cand = g.cand.as<unsigned long long>();
+        auto* coff = g.coff.as<unsigned long long>();
+        SSJ_CK(ssjb::group_intra_sizes(*e->gidx, p_begin, n, cand, g.iflag.as<uint32_t>(), st));
+        if ((rc = cub_run(g, [&](void* t, size_t& bb) {
+                 return cub::DeviceScan::ExclusiveSum(t, bb, cand, coff, (int)np, st);
+             }, st)))
+            return rc;
+        ibase.resize((size_t)np + 1);
+        unsigned long long last = 0;
+        SSJ_CK(cudaMemcpyAsync(ibase.data(), coff, (size_t)np * 8, cudaMemcpyDeviceToHost, st));
+        SSJ_CK(cudaMemcpyAsync(&last, cand + np - 1, 8, cudaMemcpyDeviceToHost, st));
+        SSJ_CK(cudaStreamSynchronize(st));
+        ibase[np] = ibase[np - 1] + last;
+    }
     for (int phase = 0; phase < (groupjoin ? 2 : 1); ++phase) {
         for (uint32_t a = p_begin; a < n;) {
-            // the longest block whose candidate upper bound fits the budget (>= 1 unit); the
-            // intra-group phase takes all groups at once
-            uint32_t b = n;
+            // the longest block whose candidate count (bound) fits the budget (>= 1 unit)
+            uint32_t b;
             if (phase == 0) {
                 b = (uint32_t)(std::upper_bound(g.hbase.begin() + a + 1, g.hbase.end(),
                                                 g.hbase[a] + cap) - g.hbase.begin()) - 1;
-                if (b <= a) b = a + 1;
-                b = std::min(b, n);
+            } else {
+                const size_t k = a - p_begin;  // ibase[k] = intra pairs of groups [p_begin, a)
+                b = p_begin + (uint32_t)(std::upper_bound(ibase.begin() + k + 1, ibase.end(),
+                                                          ibase[k] + cap) - ibase.begin()) - 1;
             }
+            if (b <= a) b = a + 1;
+            b = std::min(b, n);
             uint64_t nC = 0, nCO = 0;
             SSJ_CK(cudaEventRecord(ev[0], st));
             if (!groupjoin) rc = gen_block(e, g, a, b, &nC, &nCO);
@@ -1641,6 +1801,7 @@ int ssj_gpu_join_shard(ssj_engine* e, int32_t algorithm, uint32_t shard, uint32_
 
 int ssj_engine_set_profiling(ssj_engine* e, int enabled) {
     if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
+    if (e->group) return ssjm::set_profiling(*e->group, enabled);
     e->profiling = enabled != 0;
     e->prof_used = 0;
     return SSJ_OK;
@@ -1648,6 +1809,7 @@ int ssj_engine_set_profiling(ssj_engine* e, int enabled) {
 
 int ssj_engine_kernel_time(ssj_engine* e, double* total_ms, uint64_t* launches) {
     if (!e) return fail(SSJ_ERR_INVALID_ARGUMENT, "null engine");
+    if (e->group) return ssjm::kernel_time(*e->group, total_ms, launches);
     DeviceScope ds(e->device);
     double sum = 0;
     for (size_t i = 0; i < e->prof_used; ++i) {
@@ -1665,6 +1827,7 @@ int ssj_engine_kernel_time(ssj_engine* e, double* total_ms, uint64_t* launches) 
 int ssj_engine_export_collection(const ssj_engine* e, uint32_t* d_tokens, uint32_t* d_sets,
                                  void* stream) {
     if (!e || !d_tokens || !d_sets) return fail(SSJ_ERR_INVALID_ARGUMENT, "null argument");
+    if (e->group) return ssj_engine_export_collection(ssjm::first(*e->group), d_tokens, d_sets, stream);
     DeviceScope ds(e->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
     SSJ_CK(cudaMemcpyAsync(d_tokens, e->d_tokens, e->n_padded * sizeof(uint32_t),
@@ -1678,13 +1841,18 @@ int ssj_launches_per_chunk(const ssj_engine* e, uint64_t nC, uint64_t nCO) {
     // prep + one verification kernel (B, C); the memset of the result block is not ours.
     // Strategy A: prep, probe bitmaps (when there are slices), then per chunk segment the
     // run list, run_kernel and warp_tile_kernel (when there are slots), and long pairs.
-    if (e && e->strategy.kind == SSJ_STRATEGY_A) return (nCO >= 2 ? 2 : 1) + (nC ? 3 : 0) + 1;
-    return 2;
+    const int per = (e && e->exec.kind == SSJ_STRATEGY_A)
+                        ? (nCO >= 2 ? 2 : 1) + (nC ? 3 : 0) + 1
+                        : 2;
+    return e && e->group ? per * (int)ssjm::size(*e->group) : per;
 }
 
 int ssj_chunk_algorithmic_bytes_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC,
                                        const uint32_t* d_C_O, uint64_t nCO, uint64_t* d_bytes,
                                        void* stream) {
+    if (e && e->group)
+        return fail(SSJ_ERR_INVALID_ARGUMENT,
+                    "device-resident chunks live on one GPU: use a one-device engine");
     int rc = check_chunk_args(e, d_C, nC, d_C_O, nCO);
     if (rc) return rc;
     DeviceScope ds(e->device);

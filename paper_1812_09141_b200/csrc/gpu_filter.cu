@@ -439,7 +439,13 @@ cudaError_t filter_index_build(FilterIndex* ix, const uint32_t* d_tokens, const 
             err = cudaErrorInvalidValue;
             goto done;
         }
-        ix->universe = max_tok + 1;  // joiners.hpp:21-24 (every set non-empty here or max 0)
+        // joiners.hpp:21-24 (every set non-empty here or max 0); the per-token heads and cub's
+        // int item counts need universe + 1 < 2^31 (refused: cudaErrorInvalidValue)
+        if (max_tok >= 0x7FFFFFFEu) {
+            err = cudaErrorInvalidValue;
+            goto done;
+        }
+        ix->universe = max_tok + 1;
         ix->n_post = E;
         if (!ck(cudaMalloc(&count, ((size_t)ix->universe + 1) * 4)) ||
             !ck(cudaMemsetAsync(count, 0, ((size_t)ix->universe + 1) * 4, st)) ||

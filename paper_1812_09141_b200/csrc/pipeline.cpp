@@ -78,12 +78,14 @@ struct PinnedVec {
 struct Chunk {
     PinnedVec<uint32_t> C, CO;
     PinnedVec<uint8_t> flags;
-    std::vector<uint32_t> pairs;  // pairs decoded on the GPU (pairs mode without observer)
+    PinnedVec<uint32_t> pairs;  // pairs decoded on the GPU (pairs mode without observer);
+                                // capacity reused across chunks, never zero-filled
     bool decoded = false;
+    uint64_t ticket = 0;        // dispatcher: the engine ticket while in flight
     uint64_t byte_size() const { return 4ull * (C.n + CO.n); }  // chunk.hpp:25-27
     void clear() {
         C.n = CO.n = 0;
-        pairs.clear();
+        pairs.n = 0;
         decoded = false;
     }
 };
@@ -200,6 +202,10 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
         return ssjh::set_error(SSJ_ERR_INVALID_ARGUMENT, "unknown algorithm");
     if (cfg->mode != SSJ_MODE_COUNT && cfg->mode != SSJ_MODE_PAIRS)
         return ssjh::set_error(SSJ_ERR_INVALID_ARGUMENT, "bad output mode");
+    if (cfg->max_inflight > 2)
+        return ssjh::set_error(SSJ_ERR_INVALID_ARGUMENT, "max_inflight must be 0, 1 or 2");
+    if (cfg->devices && !cfg->n_devices)
+        return ssjh::set_error(SSJ_ERR_INVALID_ARGUMENT, "empty device list");
 
     const bool pairs_mode = cfg->mode == SSJ_MODE_PAIRS;
     const uint64_t budget = cfg->chunk_budget;
@@ -215,9 +221,15 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
     ssj_join_report& report = result->report;
     const auto setup_start = Clock::now();
     EngineHolder engine, host_engine;
-    if ((rc = ssj_engine_create(&engine.e, cfg->device, tokens, offsets, n_sets, pred, cfg->mode,
-                                &cfg->strategy)))
+    // pipeline.hpp:156: the engine -- one GPU, or one engine over several (probe-slice split
+    // of every chunk, ssj_engine_create_multi)
+    if ((rc = cfg->devices ? ssj_engine_create_multi(&engine.e, cfg->devices, cfg->n_devices, tokens,
+                                                     offsets, n_sets, pred, cfg->mode,
+                                                     &cfg->strategy)
+                           : ssj_engine_create(&engine.e, cfg->device, tokens, offsets, n_sets, pred,
+                                               cfg->mode, &cfg->strategy)))
         return rc;
+    const int engine_device = ssj_engine_device(engine.e);
     ssj_engine_strategy(engine.e, &report.resolved_strategy);
     if (pairs_mode && (rc = ssj_engine_set_original_ids(engine.e, original_id))) return rc;
     report.setup_ms = ms_since(setup_start);
@@ -260,7 +272,9 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
         return SSJ_OK;
     }
 
-    ChunkPool pool(3);
+    // chunks in flight on the dispatcher (1: the reference's rendezvous, at most 2 live)
+    const uint32_t inflight = std::max<uint32_t>(cfg->max_inflight, 1);
+    ChunkPool pool(2 + inflight);
     Handoff to_dispatcher;
     std::mutex h2_mutex;
     std::condition_variable h2_cv;
@@ -270,7 +284,8 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
     std::vector<uint32_t> engine_pairs;
     uint64_t engine_count = 0, verified_chunks = 0, verified_candidates = 0;
     double verification_ms = 0;
-    ssj_stats stats{};
+    ssj_stats stats{};       // H1's chunks (written by the dispatcher thread only)
+    ssj_stats host_stats{};  // GroupJoin phase 2 (written by H0 only); summed after the joins
 
     std::mutex fail_mutex;
     int fail_code = 0;
@@ -302,7 +317,7 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
                 lk.unlock();
                 uint64_t prev = 0;
                 if (ch->decoded)
-                    engine_pairs.insert(engine_pairs.end(), ch->pairs.begin(), ch->pairs.end());
+                    engine_pairs.insert(engine_pairs.end(), ch->pairs.p, ch->pairs.p + ch->pairs.n);
                 for (size_t e = 0; !ch->decoded && e + 1 < ch->CO.n; e += 2) {
                     const uint32_t pid = original_id[ch->CO.p[e]];
                     const uint64_t end = ch->CO.p[e + 1];
@@ -329,50 +344,75 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
     });
 
     // ---- H1: dispatch sealed chunks to the GPU engine (pipeline.hpp:215-258) ---------------
+    // With max_inflight = 2 the dispatcher submits chunk k+1 before it waits for chunk k, so
+    // the engine's copy and compute streams always have the next chunk queued.
     std::thread h1([&] {
+        std::vector<Chunk*> queue;  // submitted, not yet finished (oldest first)
+        auto to_h2_or_free = [&](Chunk* ch) {
+            if (pairs_mode) {
+                std::unique_lock<std::mutex> lk(h2_mutex);
+                h2_cv.wait(lk, [&] { return !h2_busy; });
+                h2_busy = true;
+                h2_slot = ch;
+                h2_cv.notify_all();
+            } else {
+                {
+                    std::lock_guard<std::mutex> live(live_mutex);
+                    sealed_live -= ch->byte_size();
+                }
+                pool.release(ch);
+            }
+        };
+        auto finish = [&](Chunk* ch, uint64_t count) {
+            ++verified_chunks;
+            verified_candidates += ch->C.n;
+            if (cfg->observer)
+                cfg->observer(cfg->observer_user, ch->C.p, ch->C.n, ch->CO.p, ch->CO.n,
+                              pairs_mode ? ch->flags.p : nullptr, count);
+            engine_count += count;
+            to_h2_or_free(ch);
+        };
+        auto wait_oldest = [&]() {
+            Chunk* ch = queue.front();
+            queue.erase(queue.begin());
+            uint64_t count = 0;
+            const auto t0 = Clock::now();
+            ck(ssj_wait_chunk(engine.e, ch->ticket, &count, &stats));
+            verification_ms += ms_since(t0);
+            finish(ch, count);
+        };
         try {
             for (;;) {
-                if (pairs_mode) {
+                if (pairs_mode && inflight == 1) {
                     std::unique_lock<std::mutex> lk(h2_mutex);
                     h2_cv.wait(lk, [&] { return !h2_busy; });
                 }
                 Chunk* ch = to_dispatcher.take();
                 if (!ch) break;
-                uint64_t count = 0;
                 const auto t0 = Clock::now();
                 if (pairs_mode && !cfg->observer) {
-                    // H2 on the GPU: only the qualifying pairs (original ids) cross PCIe
-                    ch->pairs.resize(2 * (ch->C.n + 1));
+                    // H2 on the GPU: only the qualifying pairs (original ids) cross PCIe, in
+                    // decode_pairs order (synchronous: one chunk at a time)
+                    while (!queue.empty()) wait_oldest();
+                    uint64_t count = 0;
+                    ch->pairs.reserve(2 * (ch->C.n + 1));
                     ck(ssj_verify_chunk_pairs(engine.e, ch->C.p, ch->C.n, ch->CO.p, ch->CO.n,
-                                              ch->pairs.data(), nullptr, ch->C.n + 1, &count,
-                                              0, &stats));
-                    ch->pairs.resize(2 * count);
+                                              ch->pairs.p, nullptr, ch->C.n + 1, &count, 0,
+                                              &stats));
+                    ch->pairs.n = 2 * count;
                     ch->decoded = true;
-                } else {
-                    if (pairs_mode) ch->flags.reserve(ch->C.n + 1);
-                    ck(ssj_verify_chunk(engine.e, ch->C.p, ch->C.n, ch->CO.p, ch->CO.n,
-                                        pairs_mode ? ch->flags.p : nullptr, &count, &stats));
+                    verification_ms += ms_since(t0);
+                    finish(ch, count);
+                    continue;
                 }
+                if (pairs_mode) ch->flags.reserve(ch->C.n + 1);
+                ck(ssj_submit_chunk(engine.e, ch->C.p, ch->C.n, ch->CO.p, ch->CO.n,
+                                    pairs_mode ? ch->flags.p : nullptr, &ch->ticket));
                 verification_ms += ms_since(t0);
-                ++verified_chunks;
-                verified_candidates += ch->C.n;
-                if (cfg->observer)
-                    cfg->observer(cfg->observer_user, ch->C.p, ch->C.n, ch->CO.p, ch->CO.n,
-                                  pairs_mode ? ch->flags.p : nullptr, count);
-                engine_count += count;
-                if (pairs_mode) {
-                    std::lock_guard<std::mutex> lk(h2_mutex);
-                    h2_busy = true;
-                    h2_slot = ch;
-                    h2_cv.notify_all();
-                } else {
-                    {
-                        std::lock_guard<std::mutex> live(live_mutex);
-                        sealed_live -= ch->byte_size();
-                    }
-                    pool.release(ch);
-                }
+                queue.push_back(ch);
+                if (queue.size() >= inflight) wait_oldest();
             }
+            while (!queue.empty()) wait_oldest();
             std::unique_lock<std::mutex> lk(h2_mutex);
             h2_cv.wait(lk, [&] { return !h2_busy && !h2_slot; });
             h2_closed = true;
@@ -383,6 +423,10 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
             capture(SSJ_ERR_RUNTIME, e.what());
         }
         if (fail_code) {
+            for (Chunk* ch : queue) {  // drain what is still on the GPU (errors already captured)
+                uint64_t c = 0;
+                ssj_wait_chunk(engine.e, ch->ticket, &c, nullptr);
+            }
             to_dispatcher.close();
             std::lock_guard<std::mutex> lk(h2_mutex);
             h2_closed = true;
@@ -458,14 +502,14 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
             uint64_t np = 0;
             ck(ssj_engine_device_collection(engine.e, &dt, &np, &ds));
             ssj_strategy a{SSJ_STRATEGY_A, 1};  // host_verify always records stats (:304)
-            ck(ssj_engine_create_from_device(&host_engine.e, cfg->device, dt, np, ds, n_sets,
+            ck(ssj_engine_create_from_device(&host_engine.e, engine_device, dt, np, ds, n_sets,
                                              n_sets ? (uint64_t)offsets[n_sets] - offsets[0] : 0,
                                              pred, SSJ_MODE_PAIRS, &a));
         }
         host_chunk.flags.reserve(host_chunk.C.n + 1);
         uint64_t cnt = 0;
         ck(ssj_verify_chunk(host_engine.e, host_chunk.C.p, host_chunk.C.n, host_chunk.CO.p,
-                            host_chunk.CO.n, host_chunk.flags.p, &cnt, &stats));
+                            host_chunk.CO.n, host_chunk.flags.p, &cnt, &host_stats));
         host_count += cnt;
         if (pairs_mode) {
             uint64_t prev = 0;
@@ -526,6 +570,8 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
         if (std::string(e.what()) != "dispatcher stopped") capture(e.code, e.what());
     } catch (const std::bad_alloc&) {
         capture(SSJ_ERR_RUNTIME, "pinned host allocation failed");
+    } catch (const std::invalid_argument& e) {
+        capture(SSJ_ERR_INVALID_ARGUMENT, e.what());
     } catch (const std::exception& e) {
         capture(SSJ_ERR_RUNTIME, e.what());
     }
@@ -544,9 +590,10 @@ int ssj_run_join(const uint32_t* tokens, const uint32_t* offsets, uint32_t n_set
     report.candidate_count = verified_candidates;
     report.host_verified_pairs = host_count;
     report.max_live_candidate_bytes = max_live;
-    report.pairs_verified = stats.pairs_verified;
-    report.early_exit_prunes = stats.early_exit_prunes;
-    report.comparison_budget_violations = stats.comparison_budget_violations;
+    report.pairs_verified = stats.pairs_verified + host_stats.pairs_verified;
+    report.early_exit_prunes = stats.early_exit_prunes + host_stats.early_exit_prunes;
+    report.comparison_budget_violations =
+        stats.comparison_budget_violations + host_stats.comparison_budget_violations;
     report.serialization_ms = serialization_ms;
     report.filtering_ms = std::max(0.0, generation_ms - serialization_ms);
     report.verification_ms = verification_ms;

@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass, field
 from enum import IntEnum
-from typing import Callable, Optional, Tuple
+from typing import Callable, Optional, Tuple, Sequence
 
 import numpy as np
 
@@ -40,6 +40,8 @@ class PipelineConfig:
     chunk_observer: Optional[Callable[[CandidateChunk, VerificationOutput], None]] = None
     device: int = 0
     filter_threads: int = 1  # FILTER_ON_GPU: candidate generation on the device too
+    devices: Optional[Sequence[int]] = None  # several GPUs behind the engine (probe-slice split)
+    max_inflight: int = 1    # chunks the dispatcher keeps on the GPU (1 = the reference's)
 
 
 @dataclass
@@ -87,6 +89,12 @@ def run_join(collection: Collection, pred: SimilarityPredicate,
     cfg.workers = max(0, int(config.workers))
     cfg.device = config.device
     cfg.filter_threads = config.filter_threads
+    cfg.max_inflight = config.max_inflight
+    devs = None
+    if config.devices is not None:
+        devs = (C.c_int32 * len(config.devices))(*config.devices)
+        cfg.devices = C.cast(devs, C.POINTER(C.c_int32))
+        cfg.n_devices = len(config.devices)
     errors = []
     if config.chunk_observer is not None:
         def _obs(user, Cp, nC, COp, nCO, flagsp, count):

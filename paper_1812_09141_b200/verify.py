@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass, field
 from enum import IntEnum
-from typing import Optional, Tuple
+from typing import Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -72,7 +72,9 @@ class VerificationEngine:
     """
 
     def __init__(self, collection: Collection, pred: SimilarityPredicate, mode: OutputMode,
-                 strategy: Strategy, device: int = 0):
+                 strategy: Strategy, device: int = 0, devices: Optional[Sequence[int]] = None):
+        """devices: several GPUs behind one engine (ssj_engine_create_multi: one upload,
+        NVLink fan-out, every chunk split by probe-slice ranges); `device` otherwise."""
         self._lib = N.lib()
         self._h = C.c_void_p()
         self.collection = collection
@@ -81,10 +83,18 @@ class VerificationEngine:
         p = pred._c()
         s = N.ssj_strategy(int(strategy.kind), strategy.group_size)
         tokens = collection.tokens if collection.tokens.size else np.zeros(1, np.uint32)
-        N.check(self._lib.ssj_engine_create(
-            C.byref(self._h), device, tokens.ctypes.data_as(N.u32p),
-            collection.offsets.ctypes.data_as(N.u32p), collection.size(), C.byref(p),
-            int(self.mode), C.byref(s)))
+        if devices is not None:
+            devs = (C.c_int32 * len(devices))(*devices)
+            N.check(self._lib.ssj_engine_create_multi(
+                C.byref(self._h), devs, len(devices), tokens.ctypes.data_as(N.u32p),
+                collection.offsets.ctypes.data_as(N.u32p), collection.size(), C.byref(p),
+                int(self.mode), C.byref(s)))
+            device = int(devices[0])
+        else:
+            N.check(self._lib.ssj_engine_create(
+                C.byref(self._h), device, tokens.ctypes.data_as(N.u32p),
+                collection.offsets.ctypes.data_as(N.u32p), collection.size(), C.byref(p),
+                int(self.mode), C.byref(s)))
         r = N.ssj_strategy()
         N.check(self._lib.ssj_engine_strategy(self._h, C.byref(r)))
         self._strategy = Strategy(StrategyKind(r.kind), r.group_size)
@@ -113,6 +123,14 @@ class VerificationEngine:
         self.device = device
         return self
 
+    def devices(self) -> Tuple[list, float]:
+        """(the engine's CUDA devices, collection fan-out ms)."""
+        buf = (C.c_int32 * 64)()
+        n = C.c_uint32()
+        ms = C.c_double()
+        N.check(self._lib.ssj_engine_devices(self._h, buf, 64, C.byref(n), C.byref(ms)))
+        return [buf[i] for i in range(min(n.value, 64))], ms.value
+
     def device_collection(self) -> Tuple[int, int, int]:
         """(d_tokens, n_padded_tokens, d_sets) of the engine's resident collection."""
         t, s = C.c_void_p(), C.c_void_p()
@@ -139,8 +157,15 @@ class VerificationEngine:
         self.close()
 
     def strategy(self) -> Strategy:
-        """verify.hpp:255: the resolved strategy (never Auto)."""
+        """verify.hpp:255: the resolved strategy (never Auto), resolved like the reference
+        (verify.hpp:249-253)."""
         return self._strategy
+
+    def kernel_strategy(self) -> Strategy:
+        """The kernel family that runs (Auto: strategy A's kernels)."""
+        r = N.ssj_strategy()
+        N.check(self._lib.ssj_engine_kernel_strategy(self._h, C.byref(r)))
+        return Strategy(StrategyKind(r.kind), r.group_size)
 
     # -- the hot call ----------------------------------------------------------------
     def verify_chunk(self, chunk: CandidateChunk, pool=None,
@@ -306,6 +331,18 @@ def measure_read_bandwidth(device: int, nbytes: int, reps: int = 20) -> float:
     g = C.c_double()
     N.check(N.lib().ssj_measure_read_bandwidth(device, nbytes, reps, C.byref(g)))
     return g.value
+
+
+def chunk_split(set_sizes: np.ndarray, parts: int, C_O: np.ndarray, nC: int) -> np.ndarray:
+    """The probe-slice split a multi-device engine applies to a chunk (host only):
+    (parts, 4) uint64 rows {first slice, end slice, first slot, end slot}."""
+    sz = np.ascontiguousarray(np.asarray(set_sizes, np.uint32))
+    co = np.ascontiguousarray(np.asarray(C_O, np.uint32))
+    out = np.zeros(4 * parts, np.uint64)
+    N.check(N.lib().ssj_chunk_split(sz.ctypes.data_as(N.u32p) if sz.size else None, sz.size,
+                                    parts, co.ctypes.data_as(N.u32p) if co.size else None,
+                                    co.size, nC, out.ctypes.data_as(N.u64p)))
+    return out.reshape(parts, 4)
 
 
 def device_count() -> int:

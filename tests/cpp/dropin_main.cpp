@@ -62,13 +62,16 @@ int main() {
                            (unsigned long long)seed, (unsigned long long)num,
                            (unsigned long long)den, (int)kind, group);
                     EXPECT(go.count == ro.count && go.count == truth.count(), "count");
-                    EXPECT(gpu.strategy().kind != StrategyKind::Auto, "auto resolved");
-                    if (kind == StrategyKind::A || kind == StrategyKind::B) {
-                        EXPECT(gs.pairs_verified.load() == rs.pairs_verified.load() &&
-                                   gs.early_exit_prunes.load() == rs.early_exit_prunes.load() &&
-                                   gs.comparison_budget_violations.load() == 0,
-                               "stats");
-                    }
+                    // resolved exactly like the reference (verify.hpp:249-253), Auto included
+                    EXPECT(gpu.strategy().kind == ref.strategy().kind &&
+                               gpu.strategy().group_size == ref.strategy().group_size,
+                           "resolved strategy kind=%d B=%u", (int)kind, group);
+                    // stats equal for every strategy (C, and Auto resolved to C, record none)
+                    EXPECT(gs.pairs_verified.load() == rs.pairs_verified.load() &&
+                               gs.early_exit_prunes.load() == rs.early_exit_prunes.load() &&
+                               gs.comparison_budget_violations.load() ==
+                                   rs.comparison_budget_violations.load(),
+                           "stats kind=%d B=%u", (int)kind, group);
                     auto got = decode_pairs(chunk, go.flags, c.original_id);
                     std::sort(got.begin(), got.end());
                     std::vector<ResultPair> want;

@@ -384,16 +384,28 @@ def test_c4_golden_on_gpu(ssj, gpu):
             assert hashlib.sha256(text.encode()).hexdigest() == str(g["out_sha256"][0])
 
 
-def test_auto_resolution_never_auto(ssj, gpu):
+def test_auto_resolution_like_the_reference(ssj, gpu):
+    """verify.hpp:249-253: Auto reports B (average set size <= 10) or C with group >= 128,
+    and the stats follow the reported strategy (C records none); the A kernels run."""
     small = ssj.Collection.from_sets([[1], [2, 3]])
     with engine(ssj, small, ssj.jaccard(1, 2), "Auto", 32) as eng:
-        assert eng.strategy().kind != ssj.StrategyKind.Auto
+        r = eng.strategy()
+        assert (r.kind, r.group_size) == (ssj.StrategyKind.B, 32)
+        assert eng.kernel_strategy().kind == ssj.StrategyKind.A
+        st = ssj.VerifyStats()
+        out = eng.verify_chunk(ssj.CandidateChunk([0], [1, 1]), None, st)
+        assert out.count == 0 and st.pairs_verified == 1  # B records stats
     big = ssj.Collection.from_sets([list(range(1000)), list(range(3, 1003))])
-    with engine(ssj, big, ssj.jaccard(1, 2), "Auto", 32) as eng:
-        # B200 policy: the tile kernel (A) with long pairs deferred to warp-per-pair
-        assert eng.strategy().kind == ssj.StrategyKind.A and eng.strategy().group_size == 32
-        out = eng.verify_chunk(ssj.CandidateChunk([0], [1, 1]))
-        assert out.count == 1
+    for group, want in ((32, 128), (256, 256)):
+        with engine(ssj, big, ssj.jaccard(1, 2), "Auto", group) as eng:
+            r = eng.strategy()
+            assert (r.kind, r.group_size) == (ssj.StrategyKind.C, want)
+            k = eng.kernel_strategy()
+            assert (k.kind, k.group_size) == (ssj.StrategyKind.A, group)
+            st = ssj.VerifyStats()
+            out = eng.verify_chunk(ssj.CandidateChunk([0], [1, 1]), None, st)
+            assert out.count == 1 and out.flags.tolist() == [1]
+            assert st.pairs_verified == 0  # C records nothing (verify.hpp:303-345)
 
 
 def test_long_sets_bitmaps_and_deferral(ssj, gpu, oracle):

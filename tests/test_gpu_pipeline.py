@@ -235,3 +235,49 @@ def test_config_shapes_join_vs_oracle(ssj, gpu, oracle, shape):
         rep = ssj.run_join(coll, ssj.jaccard(num, den),
                            cfg(ssj, algorithm=alg, mode=ssj.OutputMode.Count))
         assert rep.count == len(truth)
+
+
+@pytest.mark.parametrize("name", ["medium_s101", "medium_s202", "sweep_s1001", "c4_s777"])
+def test_join_report_fields_match_reference(ssj, gpu, name):
+    """The JoinReport of the default PipelineConfig (Auto/32, PPJoin, pipeline.hpp:36-51) and
+    of the other generators equals the reference run_join's field for field: count, chunks,
+    candidates, host-verified pairs, resolved_strategy (Auto resolved as verify.hpp:249-253),
+    VerifyStats (C records none) and, in Pairs mode, the pairs in JoinReport::pairs order."""
+    from oracle import pyoracle as po
+    if not po.ref_available():
+        pytest.skip("oracle/_ref/libssjref.so not built")
+    R = po.Ref()
+    g = golden(name)
+    c = coll_of(ssj, g)
+    h = R.coll(g["tokens"], g["offsets"], g["original_id"])
+    for (num, den), group in (((1, 2), 32), ((4, 5), 1)):
+        for alg in ssj.Algorithm:
+            for mode in (ssj.OutputMode.Count, ssj.OutputMode.Pairs):
+                for kind in (ssj.StrategyKind.Auto, ssj.StrategyKind.B):
+                    ref, ref_pairs, _ = R.run_join(h, J, num, den, 1, algorithm=int(alg),
+                                                   budget=16 << 10, kind=int(kind),
+                                                   group=group,
+                                                   pairs_mode=mode == ssj.OutputMode.Pairs,
+                                                   sort_pairs=False)
+                    rep = ssj.run_join(c, ssj.jaccard(num, den),
+                                       cfg(ssj, algorithm=alg, mode=mode, chunk_budget=16 << 10,
+                                           strategy=ssj.Strategy(kind, group)))
+                    key = (name, num, alg, mode, kind)
+                    assert rep.count == ref["count"], key
+                    assert rep.chunk_count == ref["chunk_count"], key
+                    assert rep.candidate_count == ref["candidate_count"], key
+                    assert rep.host_verified_pairs == ref["host_verified_pairs"], key
+                    assert (int(rep.resolved_strategy.kind), rep.resolved_strategy.group_size) \
+                        == (ref["resolved_kind"], ref["resolved_group"]), key
+                    assert rep.pairs_verified == ref["pairs_verified"], key
+                    assert rep.early_exit_prunes == ref["early_exit_prunes"], key
+                    assert rep.comparison_budget_violations == 0
+                    if mode == ssj.OutputMode.Pairs:
+                        if alg == ssj.Algorithm.GroupJoin:
+                            # the reference appends intra-group pairs on H0 as they are
+                            # verified (pipeline.hpp:299-312); here they come after the chunks
+                            assert np.array_equal(ssj.sorted_pairs(rep.pairs),
+                                                  ssj.sorted_pairs(ref_pairs)), key
+                        else:
+                            assert np.array_equal(rep.pairs, ref_pairs), key
+    R.L.ref_coll_free(h)
