@@ -324,6 +324,21 @@ int build_heads(ssj_engine& e) {
     return SSJ_OK;
 }
 
+// Cosine (similarity.hpp:93-102): the reference searches k with u128 products k^2 den^2 and
+// num^2 r s. They are exact while num * max_size + den < 2^64 (then k <= num sqrt(r s) / den
+// + 1 and every product is < 2^128); beyond that the reference's own arithmetic wraps, so
+// such a threshold is refused instead of being reproduced. Inside the range the device's
+// double-precision start value est - 2 is below the answer (est < 2^32, relative error
+// < 2^-50), so its upward search ends on the reference's k exactly.
+int check_cosine_range(const ssj_predicate& p, uint32_t max_size) {
+    if (p.function != SSJ_COSINE) return SSJ_OK;
+    if ((u128)p.num * max_size + p.den >= ((u128)1 << 64))
+        return fail(SSJ_ERR_INVALID_ARGUMENT,
+                    "Cosine threshold num * max set size overflows the reference's u128 "
+                    "arithmetic (similarity.hpp:93-102)");
+    return SSJ_OK;
+}
+
 // Jaccard and Dice: equivalent_overlap depends on |r| + |s| only (similarity.hpp:113-118),
 // so the kernels read it from a table built here with the exact u128 formula.
 int build_req_table(ssj_engine& e, uint32_t max_size) {
@@ -785,6 +800,7 @@ int ssj_engine_create(ssj_engine** out, int device, const uint32_t* tokens, cons
         return cleanup(fail(SSJ_ERR_CUDA, "collection upload failed"));
     uint32_t max_size = 0;
     for (uint32_t i = 0; i < n_sets; ++i) max_size = std::max(max_size, offsets[i + 1] - offsets[i]);
+    if ((rc = check_cosine_range(*pred, max_size))) return cleanup(rc);
     if ((rc = build_req_table(*e, max_size))) return cleanup(rc);
     if ((rc = build_heads(*e))) return cleanup(rc);
     *out = e;
@@ -832,7 +848,7 @@ int ssj_engine_create_from_device(ssj_engine** out, int device, const uint32_t* 
         ssj_engine_destroy(e);
         return rc;
     }
-    if (n_sets && (e->hpred.function == SSJ_JACCARD || e->hpred.function == SSJ_DICE)) {
+    if (n_sets && e->hpred.function != SSJ_OVERLAP) {
         std::vector<uint2> sets(n_sets);
         if (cudaMemcpy(sets.data(), d_sets, n_sets * sizeof(uint2), cudaMemcpyDeviceToHost) !=
             cudaSuccess) {
@@ -841,7 +857,7 @@ int ssj_engine_create_from_device(ssj_engine** out, int device, const uint32_t* 
         }
         uint32_t max_size = 0;
         for (const auto& sd : sets) max_size = std::max(max_size, sd.y);
-        if ((rc = build_req_table(*e, max_size))) {
+        if ((rc = check_cosine_range(*pred, max_size)) || (rc = build_req_table(*e, max_size))) {
             ssj_engine_destroy(e);
             return rc;
         }

@@ -146,8 +146,9 @@ def test_multi_errors(ssj, gpu):
             eng.verify_chunk(ssj.CandidateChunk([0, 7], [1, 1, 2, 2]))
         with pytest.raises(ValueError):  # device pointers belong to one GPU
             eng.verify_chunk_device(0, 0, 0, 0, 0, 1)
-        out = eng.verify_chunk(ssj.CandidateChunk([0, 0, 1], [1, 1, 2, 3]))  # still usable
-        assert out.flags.tolist() == [1, 1, 1]
+        # still usable after the errors: {1,2,3}~{1,2}, {2,3}~{1,2}, {2,3}~{1,2,3} at J >= 1/2
+        out = eng.verify_chunk(ssj.CandidateChunk([0, 0, 1], [1, 1, 2, 3]))
+        assert out.flags.tolist() == [1, 0, 1] and out.count == 2
         out = eng.verify_chunk(ssj.CandidateChunk([], []))  # empty chunk
         assert out.count == 0 and out.flags.size == 0
 

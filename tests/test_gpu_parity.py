@@ -221,13 +221,26 @@ def test_wide_threshold_u128_path(ssj, gpu, oracle):
     rng = np.random.default_rng(5)
     coll = random_collection(ssj, rng, 1500, 60, 500)
     chunk = random_chunk(ssj, rng, coll, 60_000, 900)
+    # Cosine / Dice with den > 2^32 (e.g. Threshold::parse("0.123456789012")): the device's
+    # double estimate still starts the reference's upward search below the answer
     for fn, num, den in ((J, (1 << 40) + 3, (1 << 41) + 7), (DICE, (1 << 35) + 1, (1 << 36)),
-                         (COS, 999983, 1000003)):
+                         (COS, 999983, 1000003), (COS, 30864197253, 250000000000),
+                         (COS, (1 << 40) + 3, (1 << 41) + 7), (DICE, 30864197253, 250000000000)):
         ref = oracle.verify_chunk(coll.tokens, coll.offsets, chunk.C, chunk.C_O,
                                   oracle.pred(fn, num, den))
         with engine(ssj, coll, make_pred(ssj, fn, num, den)) as eng:
             out = eng.verify_chunk(chunk)
             assert np.array_equal(out.flags, ref["flags"]) and out.count == ref["count"]
+
+
+def test_cosine_overflow_regime_refused(ssj, gpu):
+    """num * max|s| + den >= 2^64 wraps the reference's u128 products (similarity.hpp:
+    93-102): such a Cosine threshold is refused with std::invalid_argument, not reproduced."""
+    coll = ssj.Collection.from_sets([list(range(100)), list(range(1, 101))])
+    with pytest.raises(ValueError):
+        engine(ssj, coll, make_pred(ssj, COS, (1 << 62) + 1, (1 << 63) + 5))
+    with engine(ssj, coll, make_pred(ssj, COS, (1 << 56) + 1, (1 << 57) + 5)) as eng:
+        assert eng.verify_chunk(ssj.CandidateChunk([0], [1, 1])).count == 1
 
 
 def test_trailing_uncovered_slots(ssj, gpu, oracle):
