@@ -67,7 +67,7 @@ struct DeviceScope {
 constexpr int kEventsPerSlot = 96;
 constexpr uint64_t kPieceMinSlots = 1ull << 22;  // 4M candidates = 16 MB of C per piece
 constexpr int kMaxPieces = 32;
-constexpr int kCounters = 5;  // per piece: deferred long slices, runs, short tiles, long-pass
+using ssjb::kCounters;  // per piece: deferred long slices, runs, short tiles, long-pass
                               // work, short-tile work
 
 template <typename T>
@@ -123,6 +123,7 @@ struct ChunkSlot {
     uint32_t* ddefer = nullptr;          // long-pair slots (strategy A)
     size_t capDf = 0;
     unsigned long long* ddefer_n = nullptr;  // kCounters counters per piece
+    size_t capCtr = 0;
     uint32_t* dbmlist = nullptr;         // slices with a probe bitmap (strategy A)
     size_t capBL = 0;
     ssjb::RunDesc* druns = nullptr;      // runs of long slices (strategy A)
@@ -215,6 +216,7 @@ struct ssj_engine {
     uint32_t* dev_defer = nullptr;
     size_t dev_defer_cap = 0;
     unsigned long long* dev_defer_n = nullptr;  // kCounters
+    size_t dev_defer_n_cap = 0;
     uint32_t* dev_bmlist = nullptr;
     size_t dev_bmlist_cap = 0;
     ssjb::RunDesc* dev_runs = nullptr;
@@ -490,19 +492,6 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
         p.bm_cap = bitmap_words_for(nC);
     }
 
-    int ev = 0;
-    int turn = 0;
-    SSJ_CK(cudaMemsetAsync(s.dacc, 0, SSJ_RESULT_WORDS * sizeof(unsigned long long), e.s_comp));
-    if (tiles)
-        SSJ_CK(cudaMemsetAsync(s.ddefer_n, 0, kCounters * kMaxPieces * sizeof(unsigned long long),
-                               e.s_comp));
-    if (out == ssjb::kOutResults)
-        SSJ_CK(cudaMemsetAsync(e.d_res_n, 0, sizeof(unsigned long long), e.s_comp));
-    if ((rc = upload(e, s.dCO, C_O, (size_t)n_slices * 2 * sizeof(uint32_t), e.s_comp, co_pinned,
-                     &turn)))
-        return rc;
-    SSJ_CK(ssjb::launch_prep(p, e.s_comp));
-
     // Pieces of the slot range: H2D(piece q+1) overlaps verify(piece q) overlaps D2H(q-1).
     // Strategies B and C map CTAs to slices, so they take the chunk as one piece.
     uint64_t piece = nC;
@@ -511,6 +500,31 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
         piece = (piece + ssjb::kRun - 1) / ssjb::kRun * ssjb::kRun;  // runs never straddle pieces
     }
     if (piece == 0) piece = 1;
+    // per-piece counters of the work lists prep builds, then (one piece) the look-back words
+    // of its ordered run list
+    const size_t lb_words = 1 + ((size_t)n_slices + 255) / 256;
+    const size_t ctr_words = (size_t)kCounters * kMaxPieces + lb_words;
+    if (tiles) {
+        if ((rc = ensure_device(&s.ddefer_n, &s.capCtr, ctr_words))) return rc;
+        p.seg_slots = piece;
+        p.runs_all = s.druns;
+        p.short_all = s.dshort;
+        p.ctr_all = s.ddefer_n;
+        p.lb_status = s.ddefer_n + (size_t)kCounters * kMaxPieces;
+    }
+
+    int ev = 0;
+    int turn = 0;
+    SSJ_CK(cudaMemsetAsync(s.dacc, 0, SSJ_RESULT_WORDS * sizeof(unsigned long long), e.s_comp));
+    if (tiles)
+        SSJ_CK(cudaMemsetAsync(s.ddefer_n, 0, ctr_words * sizeof(unsigned long long), e.s_comp));
+    if (out == ssjb::kOutResults)
+        SSJ_CK(cudaMemsetAsync(e.d_res_n, 0, sizeof(unsigned long long), e.s_comp));
+    if ((rc = upload(e, s.dCO, C_O, (size_t)n_slices * 2 * sizeof(uint32_t), e.s_comp, co_pinned,
+                     &turn)))
+        return rc;
+    SSJ_CK(ssjb::launch_prep(p, e.s_comp));
+
     for (uint64_t lo = 0; lo < nC || (lo == 0 && nC == 0); lo += piece) {
         const uint64_t hi = std::min(nC, lo + piece);
         if (hi > lo) {
@@ -599,7 +613,6 @@ int init_engine_runtime(ssj_engine& e) {
         for (auto& ev : s.ev) SSJ_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         SSJ_CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
         SSJ_CK(cudaMalloc(&s.dacc, SSJ_RESULT_WORDS * sizeof(unsigned long long)));
-        SSJ_CK(cudaMalloc(&s.ddefer_n, kCounters * kMaxPieces * sizeof(unsigned long long)));
         SSJ_CK(cudaHostAlloc(&s.hacc, SSJ_RESULT_WORDS * sizeof(unsigned long long),
                              cudaHostAllocDefault));
     }
@@ -1220,8 +1233,8 @@ int verify_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, const uint32_
         return rc;
     if (tiles && (rc = ensure_device(&e->dev_defer, &e->dev_defer_cap, std::max<size_t>(nC, 1))))
         return rc;
-    if (tiles && !e->dev_defer_n)
-        SSJ_CK(cudaMalloc(&e->dev_defer_n, kCounters * sizeof(unsigned long long)));
+    const size_t ctr_words = tiles ? (size_t)kCounters + 1 + ((size_t)n_slices + 255) / 256 : 0;
+    if (tiles && (rc = ensure_device(&e->dev_defer_n, &e->dev_defer_n_cap, ctr_words))) return rc;
     if (tiles && (rc = ensure_device(&e->dev_runs, &e->dev_runs_cap, 2 * (size_t)n_tiles + 2)))
         return rc;
     if (tiles && (rc = ensure_device(&e->dev_short, &e->dev_short_cap, (size_t)n_tiles + 1)))
@@ -1263,6 +1276,11 @@ int verify_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, const uint32_
         p.short_tiles = e->dev_short;
         p.short_n = e->dev_defer_n + 2;
         p.short_cap = n_tiles;
+        p.seg_slots = std::max<uint64_t>(nC, 1);  // one segment
+        p.runs_all = e->dev_runs;
+        p.short_all = e->dev_short;
+        p.ctr_all = e->dev_defer_n;
+        p.lb_status = e->dev_defer_n + kCounters;
     }
     // profiling brackets the whole verification of the chunk: result/counter resets, prep
     // (validation, slice descriptors, probe bitmaps) and the strategy's kernels
@@ -1280,7 +1298,7 @@ int verify_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, const uint32_
         SSJ_CK(cudaEventRecord(k0, st));
     }
     SSJ_CK(cudaMemsetAsync(d_acc, 0, SSJ_RESULT_WORDS * sizeof(uint64_t), st));
-    if (tiles) SSJ_CK(cudaMemsetAsync(e->dev_defer_n, 0, kCounters * sizeof(unsigned long long), st));
+    if (tiles) SSJ_CK(cudaMemsetAsync(e->dev_defer_n, 0, ctr_words * sizeof(unsigned long long), st));
     SSJ_CK(ssjb::launch_prep(p, st));
     SSJ_CK(launch_strategy(*e, p, out, 0, n_tiles, st, stats));
     if (k1) SSJ_CK(cudaEventRecord(k1, st));
@@ -1854,11 +1872,12 @@ int ssj_engine_export_collection(const ssj_engine* e, uint32_t* d_tokens, uint32
 }
 
 int ssj_launches_per_chunk(const ssj_engine* e, uint64_t nC, uint64_t nCO) {
-    // prep + one verification kernel (B, C); the memset of the result block is not ours.
-    // Strategy A: prep, probe bitmaps (when there are slices), then per chunk segment the
-    // run list, run_kernel and warp_tile_kernel (when there are slots), and long pairs.
+    // prep + one verification kernel (B, C); the memsets of the result block are not ours.
+    // Strategy A: prep (validation, descriptors, tile index, run and short-tile lists), probe
+    // bitmaps (when there are slices), run_kernel and warp_tile_kernel (when there are
+    // slots), and the long-pair pass.
     const int per = (e && e->exec.kind == SSJ_STRATEGY_A)
-                        ? (nCO >= 2 ? 2 : 1) + (nC ? 3 : 0) + 1
+                        ? (nCO >= 2 ? 2 : 1) + (nC ? 2 : 0) + 1
                         : 2;
     return e && e->group ? per * (int)ssjm::size(*e->group) : per;
 }

@@ -4,8 +4,9 @@
 // assignments (verify.hpp:232-345, the paper's thread-allocation alternatives A/B/C,
 // PAPER.md:605-644). Here each becomes a grid:
 //   A  (= Auto) thread per pair, load-balanced independently of slice lengths:
-//      prep_kernel / bitmap_kernel : slice descriptors, tile index, probe bitmaps
-//      runs_gen_kernel   : slices with >= kRunMinSlice candidates -> runs, the rest -> tiles
+//      prep_kernel       : thread per slice: validation, slice descriptor, tile index, the
+//                          runs of long slices (>= kRunMinSlice) and the short-tile lists
+//      bitmap_kernel     : probe bitmaps of slices with >= kSliceBitmapMinCands candidates
 //      run_kernel        : runs; candidate head records by 256-bit loads, the probe as a
 //                          byte map in shared memory, first 8 tokens per thread and a
 //                          per-warp continuation queue (the headline kernel)
@@ -130,57 +131,265 @@ __device__ __forceinline__ uint32_t upper_bound_ends(const uint32_t* __restrict_
 }
 
 // ---------------------------------------------------------------------------------------
-// Prep: validate C_O (chunk.hpp:36-48 decode assumptions), compute the first slice of every
-// tile and -- for strategy A -- one descriptor per slice: probe position/size and, for slices
-// with >= kSliceBitmapMinCands candidates, a probe-bitmap allocation (global atomic bump).
-// Thread idx handles slice idx and tile idx.
-__global__ void prep_kernel(const KParams p) {
-    const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx < p.n_slices) {
-        const uint32_t end = p.C_O[2 * idx + 1];
-        const uint32_t begin = idx ? p.C_O[2 * idx - 1] : 0;
-        const uint32_t probe = p.C_O[2 * idx];
+// Prep (thread per slice): validate C_O (chunk.hpp:36-48 decode assumptions) and -- for
+// strategy A -- write the slice's descriptor (probe position/size; for slices with
+// >= kSliceBitmapMinCands candidates a probe-bitmap allocation), its part of the tile index
+// and its work lists:
+//   * tile_first[t] (the slice holding slot t * kTile) is read only for short tiles and their
+//     successors, so a short slice writes it for every tile starting inside it and a long
+//     slice only for its first and last such tile (a short tile's first slot and its
+//     successor's first slot lie in a short slice, or at a long slice's last / first tile);
+//   * a long slice (>= kRunMinSlice candidates) emits its runs of <= kRun slots into every
+//     segment it overlaps (runs never straddle segments);
+//   * a tile is short when it holds a slot of a short slice or an uncovered slot; it is listed
+//     by exactly one owner, without atomics on the tiles: the short slice holding its first
+//     slot, else (the tile starts inside a long slice, which then ends in it) the first short
+//     slice in it, else the uncovered tail. A short slice starting inside a tile owns that
+//     tile iff the slice before it (the previous non-empty one) is long.
+// Every list position comes from ONE atomic per warp (a scan over the lanes, keyed by the
+// segment: slices are in slot order, so a warp's lanes with equal segment are contiguous).
+
+// Warp-aggregated allocation: lane requests k items from counter(key); lanes with equal key
+// are contiguous. All 32 lanes call it. Returns the lane's first position.
+template <typename Ctr>
+__device__ __forceinline__ unsigned long long warp_alloc(uint64_t key, uint32_t k, Ctr counter) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t incl = k;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+        const uint64_t kk = __shfl_up_sync(0xffffffffu, key, off);
+        if (lane >= (uint32_t)off && kk == key) incl += v;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const uint32_t last = 31 - __clz(peers);
+    unsigned long long base = 0;
+    if (lane == last && incl) base = atomicAdd(counter(key), (unsigned long long)incl);
+    base = __shfl_sync(0xffffffffu, base, last);
+    return base + incl - k;
+}
+
+__device__ __forceinline__ unsigned long long* seg_counter(const KParams& p, uint64_t seg, int c) {
+    return p.ctr_all + kCounters * seg + c;
+}
+
+// Tiles of segment `seg` (its lists' capacities: short tiles 1x, runs 2x).
+__device__ __forceinline__ uint64_t seg_tiles(const KParams& p, uint64_t seg) {
+    const uint64_t t0 = seg * p.seg_slots / kTile;  // segments start on tile boundaries
+    const uint64_t t1 = ((seg + 1) * p.seg_slots + kTile - 1) / kTile;  // the last may be partial
+    return min(t1, (uint64_t)p.n_tiles) - min(t0, (uint64_t)p.n_tiles);
+}
+
+__device__ __forceinline__ void write_runs(const KParams& p, uint32_t e, uint64_t seg,
+                                           unsigned long long k, uint64_t lo, uint64_t hi) {
+    RunDesc* runs = p.runs_all + 2 * (seg * p.seg_slots / kTile) + k;
+    const uint64_t cap = 2 * seg_tiles(p, seg) + 2;  // only a malformed C_O could exceed it
+    for (uint64_t i = 0; lo + i * kRun < hi && k + i < cap; ++i) {
+        RunDesc d;
+        d.slice = e;
+        d.begin = (uint32_t)(lo + i * kRun);
+        d.end = (uint32_t)min(lo + (i + 1) * kRun, hi);
+        d.pad = 0;
+        runs[i] = d;
+    }
+}
+
+// Append tile t to its segment's short list (per-lane atomic: the rare paths).
+__device__ __forceinline__ void list_short_tile(const KParams& p, uint64_t t) {
+    const uint64_t seg = t * kTile / p.seg_slots;
+    const unsigned long long k = atomicAdd(seg_counter(p, seg, 2), 1ull);
+    if (k < seg_tiles(p, seg)) p.short_all[seg * p.seg_slots / kTile + k] = (uint32_t)t;
+}
+
+// Length of the last non-empty slice before slice `idx` whose slots end at `pos` (0 if none):
+// walks back over zero-width slices.
+__device__ __forceinline__ uint64_t prev_nonempty_len(const KParams& p, uint64_t idx, uint64_t pos) {
+    while (idx > 0) {
+        --idx;
+        const uint64_t pb = idx ? min((uint64_t)p.C_O[2 * idx - 1], p.nC) : 0;
+        if (pb < pos) return pos - pb;
+        if (pb > pos) return 0;  // malformed C_O (reported by validation)
+    }
+    return 0;
+}
+
+// The slots past the last slice's end `last_end`: never verified (flag 0); their tiles are
+// short. The tile holding last_end is the tail's unless a short slice overlaps it.
+__device__ __forceinline__ void uncovered_tail(const KParams& p, uint64_t n_entries,
+                                               uint64_t last_end) {
+    if (last_end >= p.nC) return;
+    for (uint64_t t = (last_end + kTile - 1) / kTile; t < p.n_tiles; ++t) {
+        p.tile_first[t] = p.n_slices;
+        list_short_tile(p, t);
+    }
+    if (last_end % kTile) {  // a short last slice already listed it
+        const uint64_t len = prev_nonempty_len(p, n_entries, last_end);
+        if (len == 0 || len >= kRunMinSlice) list_short_tile(p, last_end / kTile);
+    }
+}
+
+constexpr uint32_t kPrepThreads = 256;
+constexpr uint32_t kLbTicket = 0;  // lb_status[0]: CTA tickets; lb_status[1 + k]: CTA k's word
+constexpr unsigned long long kLbAggregate = 1ull << 62, kLbPrefix = 2ull << 62;
+constexpr unsigned long long kLbValue = (1ull << 62) - 1;
+
+// One segment (the device path): the runs are listed in slot order, so that run_kernel's CTAs,
+// which sweep the run list together, sweep the chunk in order. A run's position is the
+// exclusive prefix of the runs of all earlier slices: a block scan plus a decoupled look-back
+// over the CTAs (CTAs take their slice ranges in ticket order, so a CTA only waits for CTAs
+// that already run). status[k]: flag (aggregate / inclusive prefix) | value, one 64-bit word.
+__device__ __forceinline__ unsigned long long ordered_run_base(const KParams& p, uint32_t ticket,
+                                                              uint32_t nrun, uint32_t* s_tmp) {
+    using Scan = cub::BlockScan<uint32_t, kPrepThreads>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ unsigned long long s_base;
+    uint32_t excl = 0, total = 0;
+    Scan(scan_tmp).ExclusiveSum(nrun, excl, total);
+    unsigned long long* status = p.lb_status + 1;
+    if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 predecessors at a time
+        const uint32_t lane = threadIdx.x;
+        unsigned long long prefix = 0;
+        if (lane == 0) atomicExch(status + ticket, (ticket ? kLbAggregate : kLbPrefix) | total);
+        for (int64_t j = (int64_t)ticket - 1; j >= 0; j -= 32) {
+            const int64_t jj = j - (int64_t)lane;  // lane 0 = the nearest predecessor
+            unsigned long long v = kLbPrefix;     // before CTA 0: an inclusive prefix of 0
+            if (jj >= 0) {
+                do {
+                    v = *(volatile unsigned long long*)(status + jj);
+                } while (v == 0);
+            }
+            const unsigned pm = __ballot_sync(0xffffffffu, (v & kLbPrefix) != 0);
+            const uint32_t upto = pm ? (uint32_t)(__ffs(pm) - 1) : 31u;  // nearest prefix, inclusive
+            // run counts: every prefix is < 2^32 (a run covers >= 1 of < 2^32 slots)
+            const uint32_t part = lane <= upto ? (uint32_t)(v & kLbValue) : 0u;
+            prefix += __reduce_add_sync(0xffffffffu, part);
+            if (pm) break;
+        }
+        if (lane == 0) {
+            if (ticket) atomicExch(status + ticket, kLbPrefix | (prefix + total));
+            if (total) atomicAdd(p.ctr_all + 1, (unsigned long long)total);  // the run count
+            s_base = prefix;
+        }
+    }
+    __syncthreads();
+    (void)s_tmp;
+    return s_base + excl;
+}
+
+__global__ void __launch_bounds__(kPrepThreads) prep_kernel(const KParams p) {
+    // slices in ticket order (ordered run list) or by block index
+    __shared__ uint32_t s_ticket;
+    const bool ordered = p.ctr_all && p.lb_status && p.seg_slots >= p.nC;
+    if (ordered) {
+        if (threadIdx.x == 0) s_ticket = (uint32_t)atomicAdd(p.lb_status + kLbTicket, 1ull);
+        __syncthreads();
+    }
+    const uint32_t cta = ordered ? s_ticket : blockIdx.x;
+    const uint64_t idx = (uint64_t)cta * kPrepThreads + threadIdx.x;
+    const bool live = idx < p.n_slices;
+    uint32_t end = 0, begin = 0, probe = 0;
+    if (live) {
+        end = p.C_O[2 * idx + 1];
+        begin = idx ? p.C_O[2 * idx - 1] : 0;
+        probe = p.C_O[2 * idx];
         if (end < begin || (uint64_t)end > p.nC) flag_error(p.acc, kErrBadOffsets);
         if (end > begin && probe >= p.n_sets) flag_error(p.acc, kErrOutOfRange);
-        if (p.slices) {
-            uint4 d0 = make_uint4(end, 0, 0, kNone);
-            uint4 d1 = make_uint4(0, 0, 0, 0);
-            if (probe < p.n_sets) {
-                const uint2 rd = p.sets[probe];
-                d0.y = rd.x;
-                d0.z = rd.y;
-                // a probe bitmap pays off for long slices (long pairs build their own in
-                // shared memory, long_slice_kernel)
-                if (p.bm_cap && rd.y && end > begin && end - begin >= kSliceBitmapMinCands) {
-                    const uint32_t* r = p.tokens + (size_t)rd.x * 8;
-                    const uint32_t lo = r[0] & ~31u;
-                    const uint32_t hi = r[rd.y - 1];
-                    const uint32_t nw = ((hi - lo) >> 5) + 1;
-                    // allocation: the words plus at least one zero word (clamped lookups of
-                    // tokens beyond the range land there), rounded to 16 bytes for cp.async;
-                    // no bitmap when the probe holds token 0xFFFFFFFF (the padding value)
-                    const uint32_t na = bitmap_alloc_words(nw);
-                    if (nw <= kMaxBitmapWords && hi != 0xFFFFFFFFu) {
-                        const unsigned long long off = atomicAdd(p.acc + kAccBitmapWords, (unsigned long long)na);
-                        if (off + na <= p.bm_cap) {
-                            d0.w = (uint32_t)off;
-                            if (p.bm_list)
-                                p.bm_list[atomicAdd(p.acc + kAccBitmapSlices, 1ull)] = (uint32_t)idx;
-                            d1.x = lo;
-                            d1.y = nw;
-                        }
-                    }
+    }
+    if (p.slices) {  // launch-uniform
+        uint4 d0 = make_uint4(end, 0, 0, kNone);
+        uint4 d1 = make_uint4(0, 0, 0, 0);
+        uint32_t na = 0;  // bitmap words requested
+        if (live && probe < p.n_sets) {
+            const uint2 rd = p.sets[probe];
+            d0.y = rd.x;
+            d0.z = rd.y;
+            // a probe bitmap pays off for long slices (long pairs build their own in shared
+            // memory, long_slice_kernel)
+            if (p.bm_cap && rd.y && end > begin && end - begin >= kSliceBitmapMinCands) {
+                const uint32_t* r = p.tokens + (size_t)rd.x * 8;
+                const uint32_t lo = r[0] & ~31u;
+                const uint32_t hi = r[rd.y - 1];
+                const uint32_t nw = ((hi - lo) >> 5) + 1;
+                // the words plus at least one zero word (clamped lookups of tokens beyond the
+                // range land there), rounded to 16 bytes for cp.async; no bitmap when the
+                // probe holds token 0xFFFFFFFF (the padding value)
+                if (nw <= kMaxBitmapWords && hi != 0xFFFFFFFFu) {
+                    na = bitmap_alloc_words(nw);
+                    d1.x = lo;
+                    d1.y = nw;
                 }
             }
+        }
+        const unsigned long long off =
+            warp_alloc(0, na, [&](uint64_t) { return p.acc + kAccBitmapWords; });
+        const bool got = na && off + na <= p.bm_cap;
+        if (got) d0.w = (uint32_t)off;
+        else d1 = make_uint4(0, 0, 0, 0);
+        if (p.bm_list) {
+            const unsigned long long li =
+                warp_alloc(0, got ? 1u : 0u, [&](uint64_t) { return p.acc + kAccBitmapSlices; });
+            if (got) p.bm_list[li] = (uint32_t)idx;
+        }
+        if (live) {
             uint4* dst = reinterpret_cast<uint4*>(p.slices + idx);
             dst[0] = d0;
             dst[1] = d1;
         }
     }
-    if (idx <= p.n_tiles) {
-        p.tile_first[idx] = idx == p.n_tiles
-                                ? p.n_slices
-                                : upper_bound_ends(p.C_O, 0, p.n_slices, idx * (uint64_t)kTile);
+    if (!p.ctr_all) return;  // launch-uniform: strategies B and C need no work lists
+    // strategy A work lists (clamped: a malformed C_O only reports)
+    const uint64_t b = live ? min((uint64_t)begin, p.nC) : 0, e = live ? min((uint64_t)end, p.nC) : 0;
+    const bool any = e > b;
+    const bool is_long = any && e - b >= kRunMinSlice;
+    const uint64_t t_lo = (b + kTile - 1) / kTile, t_hi = (e + kTile - 1) / kTile;  // tiles starting in it
+    // short slice: the tiles it owns -- those starting in it, and the one it starts in when
+    // the previous non-empty slice is long
+    const bool own_first = any && !is_long && b % kTile && prev_nonempty_len(p, idx, b) >= kRunMinSlice;
+    const uint64_t t0 = own_first ? b / kTile : t_lo;  // owned tiles [t0, t_hi)
+    // the lane's key: its segment (slices are in slot order, so equal keys are contiguous);
+    // idle lanes after the last slice share the largest key
+    const uint64_t seg = live ? b / p.seg_slots : ~0ull;
+    const uint64_t seg_end = (seg + 1) * p.seg_slots;
+    // runs in the lane's first segment / short tiles in the key segment: warp-aggregated;
+    // whatever lies in later segments: per lane
+    const uint32_t nrun = is_long ? (uint32_t)((min(e, seg_end) - b + kRun - 1) / kRun) : 0u;
+    const uint64_t t_key_end = any && !is_long ? min(t_hi, seg_end / kTile) : 0;
+    const uint32_t nt = any && !is_long && t_key_end > t0 ? (uint32_t)(t_key_end - t0) : 0u;
+    const unsigned long long rk =
+        ordered ? ordered_run_base(p, cta, nrun, nullptr)
+                : warp_alloc(seg, nrun, [&](uint64_t s) { return seg_counter(p, s, 1); });
+    const unsigned long long sk = warp_alloc(seg, nt, [&](uint64_t s) { return seg_counter(p, s, 2); });
+    if (!live) return;
+    if (any) {
+        if (is_long) {
+            if (t_lo < t_hi) {
+                p.tile_first[t_lo] = (uint32_t)idx;
+                p.tile_first[t_hi - 1] = (uint32_t)idx;
+            }
+            write_runs(p, (uint32_t)idx, seg, rk, b, min(e, seg_end));
+            for (uint64_t s2 = seg + 1; s2 * p.seg_slots < e; ++s2) {
+                const uint64_t lo = s2 * p.seg_slots, hi = min(e, (s2 + 1) * p.seg_slots);
+                const unsigned long long k = atomicAdd(
+                    seg_counter(p, s2, 1), (unsigned long long)((hi - lo + kRun - 1) / kRun));
+                write_runs(p, (uint32_t)idx, s2, k, lo, hi);
+            }
+        } else {
+            for (uint64_t t = t_lo; t < t_hi; ++t) p.tile_first[t] = (uint32_t)idx;
+            uint32_t* list = p.short_all + seg * p.seg_slots / kTile + sk;
+            const uint64_t cap = seg_tiles(p, seg);
+            for (uint32_t q = 0; q < nt && sk + q < cap; ++q) list[q] = (uint32_t)(t0 + q);
+            for (uint64_t t = max(t0, t_key_end); t < t_hi; ++t) list_short_tile(p, t);
+        }
+    }
+    if (idx + 1 == p.n_slices) uncovered_tail(p, p.n_slices, e > b ? e : b);
+    if (idx == 0) p.tile_first[p.n_tiles] = p.n_slices;
+}
+
+// The empty chunk's tile index: every slot is uncovered.
+__global__ void prep_empty_kernel(const KParams p) {
+    if (threadIdx.x == 0 && blockIdx.x == 0 && p.ctr_all) {
+        p.tile_first[p.n_tiles] = 0;
+        uncovered_tail(p, 0, 0);
     }
 }
 
@@ -537,81 +746,6 @@ __global__ void __launch_bounds__(kThreadsA, kTileMinBlocks) warp_tile_kernel(co
 }
 
 // ---------------------------------------------------------------------------------------
-// Strategy A, long slices: runs.
-//
-// runs_gen_kernel (thread per tile of this segment): walks the tile's slices. A slice with
-// >= kRunMinSlice candidates is cut into runs of kRun slots from its first slot inside the
-// segment (all emitted by the tile holding that slot); a tile holding any slot of a short
-// slice, or a slot past the last slice, goes to the short-tile list.
-#ifndef SSJB_RG_THREADS
-#define SSJB_RG_THREADS 256
-#endif
-constexpr uint32_t kRunsGenThreads = SSJB_RG_THREADS;  // a multiple of 32 (warp ballots)
-
-__global__ void runs_gen_kernel(const KParams p, const uint32_t tile_begin,
-                                const uint32_t tile_end) {
-    const uint32_t t = tile_begin + blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t slot0 = (uint64_t)t * kTile;
-    bool has_short = false;
-    if (t < tile_end && slot0 < p.nC) {
-        const uint64_t slot1 = min(slot0 + (uint64_t)kTile, p.nC);
-        const uint64_t seg0 = (uint64_t)tile_begin * kTile;
-        const uint64_t seg1 = min((uint64_t)tile_end * kTile, p.nC);
-        // the tile's slices: tile_first[t] .. tile_first[t + 1] inclusive (the last one may
-        // start inside the tile); a known range, so the C_O loads are independent
-        const uint32_t e0 = __ldg(p.tile_first + t);
-        const uint32_t e1 = min(__ldg(p.tile_first + t + 1) + 1, p.n_slices);  // exclusive
-        uint64_t b = e0 ? min((uint64_t)__ldg(p.C_O + 2 * (size_t)e0 - 1), p.nC) : 0;  // decode: begin = previous end
-        uint64_t covered = slot0;
-        // the span's ends are loaded 8 at a time (independent loads), so a tile of many tiny
-        // slices costs a few memory round trips, not one per slice
-        for (uint32_t eb = e0; eb < e1; eb += 8) {
-            uint32_t en[8];
-#pragma unroll
-            for (uint32_t k = 0; k < 8; ++k)
-                en[k] = eb + k < e1 ? __ldg(p.C_O + 2 * (size_t)(eb + k) + 1) : 0u;
-#pragma unroll
-            for (uint32_t k = 0; k < 8; ++k) {
-                if (eb + k >= e1) break;
-                const uint32_t e = eb + k;
-                const uint64_t end = min((uint64_t)en[k], p.nC);
-                if (b < slot1 && end > b && end > slot0) {
-                    if (end - b >= kRunMinSlice) {
-                        const uint64_t start = max(b, seg0);
-                        if (start >= slot0 && start < slot1) {
-                            const uint64_t stop = min(end, seg1);
-                            const uint64_t nrun = (stop - start + kRun - 1) / kRun;
-                            const unsigned long long kk = atomicAdd(p.runs_n, (unsigned long long)nrun);
-                            for (uint64_t i = 0; i < nrun && kk + i < p.runs_cap; ++i) {
-                                RunDesc d;
-                                d.slice = e;
-                                d.begin = (uint32_t)(start + i * kRun);
-                                d.end = (uint32_t)min(start + (i + 1) * kRun, stop);
-                                d.pad = 0;
-                                p.runs[kk + i] = d;
-                            }
-                        }
-                    } else {
-                        has_short = true;
-                    }
-                    covered = max(covered, end);
-                }
-                b = max(b, end);
-            }
-        }
-        if (covered < slot1) has_short = true;  // slots past the last slice (flag 0)
-    }
-    // short tiles: one atomic per warp
-    const unsigned m = __ballot_sync(0xffffffffu, has_short);
-    if (m) {
-        const uint32_t lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-        unsigned long long k = 0;
-        if (lane == leader) k = atomicAdd(p.short_n, (unsigned long long)__popc(m));
-        k = __shfl_sync(0xffffffffu, k, leader) + __popc(m & ((1u << lane) - 1u));
-        if (has_short && k < p.short_cap) p.short_tiles[k] = t;
-    }
-}
-
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem) : "memory");
@@ -1674,10 +1808,11 @@ constexpr uint32_t kSliceRCap = 12288;  // tokens staged per CTA in strategies B
 }  // namespace
 
 cudaError_t launch_prep(const KParams& p, cudaStream_t st, int* launches) {
-    const uint64_t work = (uint64_t)max(p.n_slices, p.n_tiles + 1);
-    const uint32_t threads = 256;
-    const uint32_t grid = (uint32_t)((work + threads - 1) / threads);
-    prep_kernel<<<grid ? grid : 1, threads, 0, st>>>(p);
+    if (p.n_slices) {
+        prep_kernel<<<(uint32_t)((p.n_slices + kPrepThreads - 1) / kPrepThreads), kPrepThreads, 0, st>>>(p);
+    } else {
+        prep_empty_kernel<<<1, 32, 0, st>>>(p);
+    }
     int n = 1;
     if (p.slices && p.bm_cap && p.n_slices) {
         const uint64_t warps = p.n_slices < 148ull * 64 ? p.n_slices : 148ull * 64;
@@ -1737,10 +1872,9 @@ cudaError_t ensure_smem_attr(K kernel, int bytes, std::atomic<uint64_t>& done) {
 template <int kOut, bool kStats>
 cudaError_t launch_tiles_t(const KParams& p, uint32_t tile_begin, uint32_t tile_end,
                            cudaStream_t st) {
+    (void)tile_begin;
+    (void)tile_end;
     const int sms = sm_count();
-    const uint32_t nt = tile_end - tile_begin;
-    runs_gen_kernel<<<(nt + kRunsGenThreads - 1) / kRunsGenThreads, kRunsGenThreads, 0, st>>>(
-        p, tile_begin, tile_end);
     auto rk = p.heads ? run_kernel<kOut, kStats, true> : run_kernel<kOut, kStats, false>;
     static std::atomic<uint64_t> attr[2];  // per instantiation and device
     cudaError_t err = ensure_smem_attr(rk, (int)kRunSmemBytes, attr[p.heads ? 1 : 0]);

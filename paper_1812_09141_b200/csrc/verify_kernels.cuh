@@ -134,7 +134,21 @@ struct KParams {
     unsigned long long* res_n;
     uint64_t res_cap;
     unsigned long long* acc;  // SSJ_RESULT_WORDS: count, err, stats[3]
+    // strategy A, whole chunk (prep_kernel; ctr_all null for B / C): the chunk is cut into
+    // segments of seg_slots slots (the host path's H2D pieces; one segment on the device
+    // path). Segment k's runs start at runs_all + 2 * (k * seg_slots / kTile), its short tiles
+    // at short_all + k * seg_slots / kTile, its counters at ctr_all + kCounters * k (+1 runs,
+    // +2 short tiles).
+    uint64_t seg_slots;
+    RunDesc* runs_all;
+    uint32_t* short_all;
+    unsigned long long* ctr_all;
+    unsigned long long* lb_status;  // one segment: 1 + CTAs zeroed words (ordered run list)
 };
+
+// Per-segment counters: 0 long slices marked, 1 runs, 2 short tiles, 3 long-pass slices
+// taken, 4 short tiles taken.
+constexpr int kCounters = 5;
 
 enum OutKind : int { kOutCount = 0, kOutFlags = 1, kOutResults = 2 };
 
@@ -149,11 +163,12 @@ constexpr uint32_t kHeadTokenLimit = 0x00FFFFE0u;
 // Build the packed heads of a collection; *max_token receives the largest token (atomicMax).
 cudaError_t launch_build_heads(const uint32_t* tokens, const uint2* sets, uint32_t n_sets,
                                uint4* heads, unsigned* max_token, cudaStream_t st);
-// prep_kernel (+ bitmap_kernel when p.slices && p.bm_cap): validation, tile index, slice
-// descriptors and probe bitmaps. Returns the number of kernels launched through *launches.
+// prep_kernel (+ bitmap_kernel when p.slices && p.bm_cap): validation, slice descriptors,
+// probe bitmaps and -- strategy A -- the tile index, the runs of long slices and the short-tile
+// lists of every segment. Returns the number of kernels launched through *launches.
 cudaError_t launch_prep(const KParams& p, cudaStream_t st, int* launches = nullptr);
-// Strategy A, first pass over tiles [tile_begin, tile_end) of the chunk: runs_gen_kernel,
-// run_kernel (long slices), warp_tile_kernel (short slices)
+// Strategy A, first pass over the segment holding tiles [tile_begin, tile_end): run_kernel
+// (long slices), warp_tile_kernel (short slices)
 cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_begin,
                          uint32_t tile_end, cudaStream_t st);
 // Strategy A, second pass: slices the first pass marked for long pairs, slots of tiles
