@@ -192,6 +192,8 @@ struct ssj_engine {
     bool owns_collection = true;
     uint32_t* d_req_tab = nullptr;  // Jaccard/Dice required overlap by |r|+|s|
     uint4* d_heads = nullptr;       // packed set heads (null: tokens too large to pack)
+    unsigned long long heads_tex = 0;   // linear uint4 textures over d_heads / d_tokens for
+    unsigned long long tokens_tex = 0;  // the run kernel's gathers (0: not created)
     ssjb::FilterIndex* fidx = nullptr;  // GPU candidate generation index (built on first use)
     GenState* gen = nullptr;            // its bounds and block buffers
     ssjb::GroupIndex* gidx = nullptr;   // GroupJoin groups + representative index (first use)
@@ -303,8 +305,35 @@ KParams base_params(const ssj_engine& e) {
     p.pred = e.pred;
     p.req_tab = e.d_req_tab;
     p.req_tab_n = e.req_tab_n;
-    p.heads = e.d_heads;
+    // packed heads go to the kernels together with their texture (run_kernel gathers them
+    // through it); without one the kernels read descriptors and the CSR
+    p.heads = e.heads_tex ? e.d_heads : nullptr;
+    p.heads_tex = e.heads_tex;
+    p.tokens_tex = e.tokens_tex;
     return p;
+}
+
+// A linear texture of uint4 texels over `bytes` of device memory, or 0 when the buffer is
+// wider than the device's 1D linear texture limit (the kernels then gather with LDG).
+unsigned long long make_linear_tex(const void* ptr, size_t bytes) {
+    int dev = 0, max_w = 0;
+    if (!ptr || !bytes || cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&max_w, cudaDevAttrMaxTexture1DLinearWidth, dev) != cudaSuccess)
+        return 0;
+    if (bytes / sizeof(uint4) > (size_t)max_w || bytes / sizeof(uint4) > 0x7FFFFFFFull) return 0;
+    cudaResourceDesc rd{};
+    rd.resType = cudaResourceTypeLinear;
+    rd.res.linear.devPtr = const_cast<void*>(ptr);
+    rd.res.linear.desc = cudaCreateChannelDesc(32, 32, 32, 32, cudaChannelFormatKindUnsigned);
+    rd.res.linear.sizeInBytes = bytes;
+    cudaTextureDesc td{};
+    td.readMode = cudaReadModeElementType;
+    cudaTextureObject_t t = 0;
+    if (cudaCreateTextureObject(&t, &rd, &td, nullptr) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return (unsigned long long)t;
 }
 
 // Packed set heads (verify_kernels.cuh) for the run kernel; left null when some token is
@@ -323,6 +352,8 @@ int build_heads(ssj_engine& e) {
         cudaFree(e.d_heads);
         e.d_heads = nullptr;
     }
+    e.heads_tex = make_linear_tex(e.d_heads, (size_t)e.n_sets * 2 * sizeof(uint4));
+    e.tokens_tex = make_linear_tex(e.d_tokens, (size_t)e.n_padded * sizeof(uint32_t));
     return SSJ_OK;
 }
 
@@ -984,6 +1015,8 @@ void ssj_engine_destroy(ssj_engine* e) {
     cudaFree(e->dev_bmlist);
     cudaFree(e->dev_short);
     cudaFree(e->d_req_tab);
+    if (e->heads_tex) cudaDestroyTextureObject((cudaTextureObject_t)e->heads_tex);
+    if (e->tokens_tex) cudaDestroyTextureObject((cudaTextureObject_t)e->tokens_tex);
     cudaFree(e->d_heads);
     if (e->fidx) {
         ssjb::filter_index_free(e->fidx);

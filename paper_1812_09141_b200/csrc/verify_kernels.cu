@@ -30,6 +30,24 @@
 #include "verify_kernels.cuh"
 #include "../../include/ssjoin_b200.h"
 
+#ifndef SSJB_RUN_TEX
+#define SSJB_RUN_TEX 1  // run_kernel gathers candidate heads through the texture path
+#endif
+#ifndef SSJB_CONT_TEX
+#define SSJB_CONT_TEX 1  // run_kernel's continuation blocks read the CSR through the texture path
+#endif
+#ifndef SSJB_TILE_TEX
+#define SSJB_TILE_TEX 0  // 1: warp_tile_kernel gathers candidate heads through the texture path
+#endif
+#ifndef SSJB_RUN_RSIDE1
+#define SSJB_RUN_RSIDE1 0  // 1: run_kernel also applies the probe-side bound after the first block (slower: 2.82 vs 2.71 ms on cfg2)
+#endif
+#ifndef SSJB_RUN_REQTAB
+#define SSJB_RUN_REQTAB 1  // run_kernel reads the required overlap from the engine's table
+#endif
+#ifndef SSJB_RUN_MAPOFF
+#define SSJB_RUN_MAPOFF 0  // 1: run_kernel byte-map lookups at constant shared offsets (neutral on cfg2)
+#endif
 #ifndef SSJB_TILE_DYN
 #define SSJB_TILE_DYN 1  // warp_tile_kernel takes short tiles from a per-launch counter
 #endif
@@ -106,6 +124,18 @@ __device__ __forceinline__ void ld_tokens8(const uint32_t* __restrict__ s, uint3
                  : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]),
                    "=r"(t[6]), "=r"(t[7])
                  : "l"(s));
+}
+
+// The same 8 tokens through the texture path (two uint4 texels of a linear texture over the
+// array; texel = 4 tokens, so the 32-byte-aligned group at token offset 8k is texels 2k, 2k+1).
+// Scattered 32-byte gathers through TLD do not compete with the kernels' shared-memory lookups
+// for the LSU pipe the way LDG.256 does (tools/tex_microbench.cu: 8 byte-map lookups per row
+// cost 29 % of the gather rate behind LDG.256, 2 % behind TLD).
+__device__ __forceinline__ void tex_tokens8(unsigned long long tex, uint64_t group8, uint32_t t[8]) {
+    const uint4 a = tex1Dfetch<uint4>(tex, (int)(2 * group8));
+    const uint4 b = tex1Dfetch<uint4>(tex, (int)(2 * group8 + 1));
+    t[0] = a.x; t[1] = a.y; t[2] = a.z; t[3] = a.w;
+    t[4] = b.x; t[5] = b.y; t[6] = b.z; t[7] = b.w;
 }
 
 // A pair longer than kLongPair tokens is left to long_slice_kernel: the first pass marks its
@@ -540,7 +570,8 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
 #pragma unroll
         for (int q = 0; q < kItems; ++q) {
             if (cand[q] < p.n_sets) {
-                ld_tokens8(reinterpret_cast<const uint32_t*>(p.heads + 2 * (size_t)cand[q]), hr[q]);
+                if (SSJB_TILE_TEX && p.heads_tex) tex_tokens8(p.heads_tex, cand[q], hr[q]);
+                else ld_tokens8(reinterpret_cast<const uint32_t*>(p.heads + 2 * (size_t)cand[q]), hr[q]);
             } else {
 #pragma unroll
                 for (int u = 0; u < 8; ++u) hr[q][u] = 0;
@@ -798,7 +829,22 @@ __device__ __forceinline__ void load_slice(const KParams& p, RunState& r) {
 // unconditional lookups.
 //   kMap   : byte map in shared memory (map[d] = 1 iff lo + d is a probe token), R = range
 //   !kMap  : membership bitmap in global memory (word R/32 is zero), read through L1
-template <bool kMap>
+//   kOff   : (kMap) the map sits at this constant byte offset of the run kernel's dynamic
+//            shared memory, so a lookup is one LDS [d + kOff] (no base register to add);
+//            kNoOff: at `map`
+constexpr uint32_t kNoOff = 0xFFFFFFFFu;
+template <uint32_t kOff>
+__device__ __forceinline__ uint32_t smem_u8(uint32_t i) {
+    extern __shared__ __align__(16) uint32_t rsh[];
+    return reinterpret_cast<const uint8_t*>(rsh)[kOff + i];
+}
+template <uint32_t kOff>
+__device__ __forceinline__ uint32_t smem_u32(uint32_t i) {
+    extern __shared__ __align__(16) uint32_t rsh[];
+    return rsh[kOff / 4 + i];
+}
+
+template <bool kMap, uint32_t kOff = kNoOff>
 __device__ __forceinline__ uint32_t count8(const uint8_t* __restrict__ map,
                                            const uint32_t* __restrict__ bits, uint32_t lo,
                                            uint32_t R, const uint32_t t[8]) {
@@ -809,7 +855,8 @@ __device__ __forceinline__ uint32_t count8(const uint8_t* __restrict__ map,
 #if SSJB_RUN_MAP_BITS
         if (kMap) c += (reinterpret_cast<const uint32_t*>(map)[d >> 5] >> (d & 31)) & 1u;
 #else
-        if (kMap) c += map[d];
+        if (kMap && kOff != kNoOff) c += smem_u8<kOff>(d);
+        else if (kMap) c += map[d];
 #endif
         else c += (__ldg(bits + (d >> 5)) >> (d & 31)) & 1u;
     }
@@ -821,34 +868,41 @@ __device__ __forceinline__ uint32_t count8(const uint8_t* __restrict__ map,
 // consumed, i = probe tokens <= the step's last token, from the global bitmap's rank), so
 // the reference's bound (verify.hpp:58) is evaluated there; verdicts are bit-exact (see
 // ssj_device.cuh).
-template <bool kFull, bool kMap>
+// Probe tokens <= t (the merge position i on the probe side once s's tokens up to t are
+// consumed), from the probe bitmap's words and per-word ranks.
+template <bool kMap, uint32_t kOff = kNoOff>
+__device__ __forceinline__ uint32_t probe_rank(const uint32_t* __restrict__ bits,
+                                               const uint32_t* __restrict__ rank, uint32_t lo,
+                                               uint32_t nbits, uint32_t m, uint32_t t) {
+    const uint32_t d = t - lo;
+    if (t < lo) return 0;
+    if (d >= nbits) return m;
+    constexpr uint32_t kB = kOff + kRunMapBytes, kR = kB + 4 * kRunMapWords;
+    const uint32_t w = kOff != kNoOff ? smem_u32<kB>(d >> 5) : kMap ? bits[d >> 5] : __ldg(bits + (d >> 5));
+    const uint32_t rk = kOff != kNoOff ? smem_u32<kR>(d >> 5) : kMap ? rank[d >> 5] : __ldg(rank + (d >> 5));
+    return rk + __popc(w & ((2u << (d & 31)) - 1u));
+}
+
+template <bool kFull, bool kMap, uint32_t kOff = kNoOff>
 __device__ __forceinline__ bool bm_continue(const uint8_t* __restrict__ map,
                                             const uint32_t* __restrict__ bits,
                                             const uint32_t* __restrict__ rank, uint32_t lo,
                                             uint32_t nbits, uint32_t m,
                                             const uint32_t* __restrict__ s, uint32_t n,
-                                            uint32_t req, uint32_t ov, uint32_t* ov_out) {
+                                            uint32_t req, uint32_t ov, uint32_t* ov_out,
+                                            unsigned long long ttex, uint32_t spos8) {
     const uint32_t slack_r = m - req, slack_s = n - req;
     uint32_t j = 8;
     for (;;) {
         uint32_t t[8];
-        ld_tokens8(s + j, t);
-        ov += count8<kMap>(map, bits, lo, nbits, t);
+        if (SSJB_CONT_TEX && ttex) tex_tokens8(ttex, (uint64_t)spos8 + (j >> 3), t);
+        else ld_tokens8(s + j, t);
+        ov += count8<kMap, kOff>(map, bits, lo, nbits, t);
         j += 8;
         if (j >= n) break;  // s exhausted (padding never matches): the verdict is ov >= req
         if (!kFull && ov >= req) break;
         if (ov < req) {
-            const uint32_t d = t[7] - lo;
-            uint32_t i;
-            if (t[7] < lo) {
-                i = 0;
-            } else if (d >= nbits) {
-                i = m;
-            } else {
-                const uint32_t w = kMap ? bits[d >> 5] : __ldg(bits + (d >> 5));
-                const uint32_t rk = kMap ? rank[d >> 5] : __ldg(rank + (d >> 5));
-                i = rk + __popc(w & ((2u << (d & 31)) - 1u));
-            }
+            const uint32_t i = probe_rank<kMap, kOff>(bits, rank, lo, nbits, m, t[7]);
             if (i - ov > slack_r || j - ov > slack_s) {
                 if (kFull) *ov_out = 0;
                 return false;
@@ -857,6 +911,13 @@ __device__ __forceinline__ bool bm_continue(const uint8_t* __restrict__ map,
     }
     if (kFull) *ov_out = ov >= req ? ov : 0;
     return ov >= req;
+}
+
+// Required overlap of a run's pair: the engine's table by |r| + |s| (Jaccard / Dice; one
+// L1-resident load: a run's candidates span a few table lines) or the exact 32-bit formula.
+__device__ __forceinline__ uint32_t run_required(const KParams& p, uint32_t m, uint32_t n) {
+    if (SSJB_RUN_REQTAB && p.req_tab) return __ldg(p.req_tab + m + n);  // m, n <= max set size
+    return dev_required_fast(p.pred, m, n);
 }
 
 // Long pairs of a run are left to long_slice_kernel: one lane marks the run's slice (all 32
@@ -877,7 +938,7 @@ __device__ __forceinline__ bool warp_defer(const KParams& p, bool want, uint32_t
 //     lanes whose pairs need one block and lanes whose pairs need several).
 // pos8[q] / n[q]: the candidate's CSR position and size (pos8 = kNone: no candidate);
 // kPacked: the staged heads are packed records (tokens in the low 24 bits).
-template <int kOut, bool kStats, bool kMap, bool kPacked, bool kReg>
+template <int kOut, bool kStats, bool kMap, bool kPacked, bool kReg, uint32_t kOff = kNoOff>
 __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
                                            const uint32_t* pos8, const uint32_t* nn,
                                            const uint8_t* __restrict__ map,
@@ -896,7 +957,7 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
         const uint32_t slot = R.begin + q * T + tid;
         const bool valid = pos8[q] != kNone;
         const uint32_t n = nn[q];
-        const uint32_t rq = valid ? dev_required_fast(p.pred, m, n) : 0u;
+        const uint32_t rq = valid ? run_required(p, m, n) : 0u;
         const bool inrange = valid && rq >= 1 && rq <= min(m, n);
         const bool deferred = warp_defer(p, inrange && n > kLongPair, R.slice);
         bool met = valid && rq == 0, decided = true;
@@ -915,10 +976,14 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
 #pragma unroll
                 for (int u = 0; u < 8; ++u) t8[u] &= kHeadTokenMask;
             }
-            ov = count8<kMap>(map, bits, lo, nbits, t8);
+            ov = count8<kMap, kOff>(map, bits, lo, nbits, t8);
             if (n <= 8) met = ov >= rq;
             else if (!kFull && ov >= rq) met = true;
             else if (ov < rq && 8u - ov > n - rq) met = false;
+            // the probe-side bound at the same point (verify.hpp:58): i probe tokens <= the
+            // block's last token, ov of them matched
+            else if (SSJB_RUN_RSIDE1 && ov < rq &&
+                     probe_rank<kMap, kOff>(bits, rank, lo, nbits, m, t8[7]) - ov > m - rq) met = false;
             else decided = false;
         } else if (kFull && met) {
             ov = full_overlap_seq(p.tokens + (size_t)R.rpos8 * 8, m,
@@ -949,8 +1014,9 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
             const uint4 qe = hd[e];
             slot = qe.x;
             const uint32_t n = qe.z, rq = qe.w & 0xFFFFu;
-            met = bm_continue<kFull, kMap>(map, bits, rank, lo, nbits, m,
-                                           p.tokens + (size_t)qe.y * 8, n, rq, qe.w >> 16, &ov);
+            met = bm_continue<kFull, kMap, kOff>(map, bits, rank, lo, nbits, m,
+                                           p.tokens + (size_t)qe.y * 8, n, rq, qe.w >> 16, &ov,
+                                           p.tokens_tex, qe.y);
             if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
             if (kStats) {
                 ++verified;
@@ -979,7 +1045,7 @@ __device__ __forceinline__ void run_merge(const KParams& p, const RunState& R,
         const uint32_t slot = R.begin + q * T + tid;
         const bool valid = pos8[q] != kNone;
         const uint32_t n = nn[q];
-        const uint32_t rq = valid ? dev_required_fast(p.pred, m, n) : 0u;
+        const uint32_t rq = valid ? run_required(p, m, n) : 0u;
         const bool inrange = valid && rq >= 1 && rq <= min(m, n);
         const bool deferred = warp_defer(p, inrange && n > kLongPair, R.slice);
         bool met = valid && rq == 0;
@@ -1108,6 +1174,15 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
                 // run k's heads straight into registers (one 256-bit load per candidate)
 #pragma unroll
                 for (uint32_t q = 0; q < I; ++q) {
+                    if (kPacked && SSJB_RUN_TEX) {
+                        // packed heads are only handed to the kernels with their texture
+                        // (base_params), so no per-item pointer or texture checks here
+                        const bool ok = c[q] < p.n_sets;
+                        if (ok) tex_tokens8(p.heads_tex, c[q], hr[q]);
+                        else if (c[q] != kNone) flag_error(p.acc, kErrOutOfRange);
+                        vm1 |= (uint32_t)ok << q;
+                        continue;
+                    }
                     const uint32_t* src = nullptr;
                     if (kPacked) {
                         if (c[q] < p.n_sets) src = reinterpret_cast<const uint32_t*>(p.heads + 2 * (size_t)c[q]);
@@ -1206,9 +1281,17 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
             if (use_map) {
                 const uint8_t* mp = s_map + mb * kRunMapBuf;
                 const uint32_t* sb = reinterpret_cast<const uint32_t*>(mp + kRunMapBytes);
-                run_bitmap<kOut, kStats, true, kPacked, kReg>(p, R0, pos8, nn, mp, sb,
-                                                              sb + kRunMapWords, hd, hr, count,
-                                                              prunes, verified);
+                constexpr uint32_t kMap0 = T * I * 8 * NBS * 4;  // byte offset of map buffer 0
+                if (SSJB_RUN_MAPOFF && mb)
+                    run_bitmap<kOut, kStats, true, kPacked, kReg, kMap0 + kRunMapBuf>(
+                        p, R0, pos8, nn, mp, sb, sb + kRunMapWords, hd, hr, count, prunes, verified);
+                else if (SSJB_RUN_MAPOFF)
+                    run_bitmap<kOut, kStats, true, kPacked, kReg, kMap0>(
+                        p, R0, pos8, nn, mp, sb, sb + kRunMapWords, hd, hr, count, prunes, verified);
+                else
+                    run_bitmap<kOut, kStats, true, kPacked, kReg>(p, R0, pos8, nn, mp, sb,
+                                                                  sb + kRunMapWords, hd, hr, count,
+                                                                  prunes, verified);
             } else if (R0.bofs != kNone) {
                 run_bitmap<kOut, kStats, false, kPacked, kReg>(p, R0, pos8, nn, nullptr,
                                                                p.bm_bits + R0.bofs,

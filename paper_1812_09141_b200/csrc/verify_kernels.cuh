@@ -111,6 +111,8 @@ struct KParams {
     uint32_t n_tiles;
     PredDev pred;
     const uint4* heads;             // packed set heads, 2 x uint4 per set (nullable)
+    unsigned long long heads_tex;   // linear uint4 texture over heads (0: none)
+    unsigned long long tokens_tex;  // linear uint4 texture over tokens (0: none)
     const uint32_t* req_tab;        // Jaccard/Dice: required overlap by |r|+|s| (nullable)
     uint32_t req_tab_n;
     SliceDesc* slices;              // strategy A: per-slice descriptors (nullable otherwise)

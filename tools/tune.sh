@@ -11,7 +11,7 @@ for v in "${VARS[@]}"; do
   NAME=${v%%|*}; FLAGS=${v#*|}
   rm -rf build/obj
   make -s -j16 NVFLAGS_EXTRA="$FLAGS" paper_1812_09141_b200/libssjoin_b200.so > /dev/null 2>&1 || { echo "build $NAME failed"; continue; }
-  timeout 300 python bench.py --steps 10 --warmup 3 --e2e-steps 1 --cpu-sample 4e6 "$@" \
+  timeout 300 python bench.py --steps 10 --warmup 3 --e2e-steps 1 --no-cpu-baseline --join-workload none "$@" \
       > $OUT/tune_$NAME.json 2> $OUT/tune_$NAME.err
   python - "$NAME" <<'PY'
 import json, sys
@@ -19,7 +19,8 @@ v = sys.argv[1]
 try:
     d = json.load(open(f"gpurun_out/tune_{v}.json"))
     r = d["roofline"]
-    print(f"{v}: {d['value']/1e9:.2f} G pairs/s, kernel {r['kernel_ms_avg']:.3f} ms, frac {r['frac']:.3f}, e2e {d['e2e']['value']/1e9:.2f}, parity {d.get('parity_sample')}")
+    pa = d.get("parity", {})
+    print(f"{v}: {d['config'].get('name')} {d['value']/1e9:.2f} G pairs/s, kernel {r['kernel_ms_avg']:.3f} ms, frac {r['frac']:.3f} (hbm {r.get('hbm_frac', 0):.3f}), e2e {d['e2e']['value']/1e9:.2f}, golden {pa.get('golden_match')} e2e_identical {pa.get('e2e_flags_identical')}")
 except Exception as e:
     print(v, "failed", e, open(f"gpurun_out/tune_{v}.err").read()[-500:])
 PY
