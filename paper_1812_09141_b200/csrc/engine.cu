@@ -547,6 +547,10 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
     int ev = 0;
     int turn = 0;
     SSJ_CK(cudaMemsetAsync(s.dacc, 0, SSJ_RESULT_WORDS * sizeof(unsigned long long), e.s_comp));
+    // strategies B and C walk the slices only: slots past the last C_O end keep flag 0
+    // (strategy A's tiles write those flags themselves)
+    if (!tiles && out == ssjb::kOutFlags && nC)
+        SSJ_CK(cudaMemsetAsync(s.dflags, 0, nC, e.s_comp));
     if (tiles)
         SSJ_CK(cudaMemsetAsync(s.ddefer_n, 0, ctr_words * sizeof(unsigned long long), e.s_comp));
     if (out == ssjb::kOutResults)
@@ -1331,6 +1335,7 @@ int verify_device(ssj_engine* e, const uint32_t* d_C, uint64_t nC, const uint32_
         SSJ_CK(cudaEventRecord(k0, st));
     }
     SSJ_CK(cudaMemsetAsync(d_acc, 0, SSJ_RESULT_WORDS * sizeof(uint64_t), st));
+    if (!tiles && out == ssjb::kOutFlags && nC) SSJ_CK(cudaMemsetAsync(d_flags, 0, nC, st));
     if (tiles) SSJ_CK(cudaMemsetAsync(e->dev_defer_n, 0, ctr_words * sizeof(unsigned long long), st));
     SSJ_CK(ssjb::launch_prep(p, st));
     SSJ_CK(launch_strategy(*e, p, out, 0, n_tiles, st, stats));

@@ -45,8 +45,8 @@
 #ifndef SSJB_RUN_REQTAB
 #define SSJB_RUN_REQTAB 1  // run_kernel reads the required overlap from the engine's table
 #endif
-#ifndef SSJB_RUN_MAPOFF
-#define SSJB_RUN_MAPOFF 0  // 1: run_kernel byte-map lookups at constant shared offsets (neutral on cfg2)
+#ifndef SSJB_RUN_PIPE
+#define SSJB_RUN_PIPE 0  // 1: run_kernel gathers run k+1's heads in the middle of run k (2.58 vs 2.49 ms on cfg2)
 #endif
 #ifndef SSJB_TILE_DYN
 #define SSJB_TILE_DYN 1  // warp_tile_kernel takes short tiles from a per-launch counter
@@ -638,7 +638,8 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
             const uint32_t pe = __shfl_sync(0xffffffffu, my_end, (li - 1) & 31);
             s_beg = li ? pe : beg0;
         }
-        bool met = false, written = false;
+        // a tile without slices lies past the last C_O end: never verified, flag 0
+        bool met = false, written = ns == 0;
         uint32_t ov = 0;
         if (slot < slot1 && ns) {
             uint32_t e = e0 + li;
@@ -829,22 +830,7 @@ __device__ __forceinline__ void load_slice(const KParams& p, RunState& r) {
 // unconditional lookups.
 //   kMap   : byte map in shared memory (map[d] = 1 iff lo + d is a probe token), R = range
 //   !kMap  : membership bitmap in global memory (word R/32 is zero), read through L1
-//   kOff   : (kMap) the map sits at this constant byte offset of the run kernel's dynamic
-//            shared memory, so a lookup is one LDS [d + kOff] (no base register to add);
-//            kNoOff: at `map`
-constexpr uint32_t kNoOff = 0xFFFFFFFFu;
-template <uint32_t kOff>
-__device__ __forceinline__ uint32_t smem_u8(uint32_t i) {
-    extern __shared__ __align__(16) uint32_t rsh[];
-    return reinterpret_cast<const uint8_t*>(rsh)[kOff + i];
-}
-template <uint32_t kOff>
-__device__ __forceinline__ uint32_t smem_u32(uint32_t i) {
-    extern __shared__ __align__(16) uint32_t rsh[];
-    return rsh[kOff / 4 + i];
-}
-
-template <bool kMap, uint32_t kOff = kNoOff>
+template <bool kMap>
 __device__ __forceinline__ uint32_t count8(const uint8_t* __restrict__ map,
                                            const uint32_t* __restrict__ bits, uint32_t lo,
                                            uint32_t R, const uint32_t t[8]) {
@@ -855,8 +841,7 @@ __device__ __forceinline__ uint32_t count8(const uint8_t* __restrict__ map,
 #if SSJB_RUN_MAP_BITS
         if (kMap) c += (reinterpret_cast<const uint32_t*>(map)[d >> 5] >> (d & 31)) & 1u;
 #else
-        if (kMap && kOff != kNoOff) c += smem_u8<kOff>(d);
-        else if (kMap) c += map[d];
+        if (kMap) c += map[d];
 #endif
         else c += (__ldg(bits + (d >> 5)) >> (d & 31)) & 1u;
     }
@@ -870,20 +855,19 @@ __device__ __forceinline__ uint32_t count8(const uint8_t* __restrict__ map,
 // ssj_device.cuh).
 // Probe tokens <= t (the merge position i on the probe side once s's tokens up to t are
 // consumed), from the probe bitmap's words and per-word ranks.
-template <bool kMap, uint32_t kOff = kNoOff>
+template <bool kMap>
 __device__ __forceinline__ uint32_t probe_rank(const uint32_t* __restrict__ bits,
                                                const uint32_t* __restrict__ rank, uint32_t lo,
                                                uint32_t nbits, uint32_t m, uint32_t t) {
     const uint32_t d = t - lo;
     if (t < lo) return 0;
     if (d >= nbits) return m;
-    constexpr uint32_t kB = kOff + kRunMapBytes, kR = kB + 4 * kRunMapWords;
-    const uint32_t w = kOff != kNoOff ? smem_u32<kB>(d >> 5) : kMap ? bits[d >> 5] : __ldg(bits + (d >> 5));
-    const uint32_t rk = kOff != kNoOff ? smem_u32<kR>(d >> 5) : kMap ? rank[d >> 5] : __ldg(rank + (d >> 5));
+    const uint32_t w = kMap ? bits[d >> 5] : __ldg(bits + (d >> 5));
+    const uint32_t rk = kMap ? rank[d >> 5] : __ldg(rank + (d >> 5));
     return rk + __popc(w & ((2u << (d & 31)) - 1u));
 }
 
-template <bool kFull, bool kMap, uint32_t kOff = kNoOff>
+template <bool kFull, bool kMap>
 __device__ __forceinline__ bool bm_continue(const uint8_t* __restrict__ map,
                                             const uint32_t* __restrict__ bits,
                                             const uint32_t* __restrict__ rank, uint32_t lo,
@@ -897,12 +881,12 @@ __device__ __forceinline__ bool bm_continue(const uint8_t* __restrict__ map,
         uint32_t t[8];
         if (SSJB_CONT_TEX && ttex) tex_tokens8(ttex, (uint64_t)spos8 + (j >> 3), t);
         else ld_tokens8(s + j, t);
-        ov += count8<kMap, kOff>(map, bits, lo, nbits, t);
+        ov += count8<kMap>(map, bits, lo, nbits, t);
         j += 8;
         if (j >= n) break;  // s exhausted (padding never matches): the verdict is ov >= req
         if (!kFull && ov >= req) break;
         if (ov < req) {
-            const uint32_t i = probe_rank<kMap, kOff>(bits, rank, lo, nbits, m, t[7]);
+            const uint32_t i = probe_rank<kMap>(bits, rank, lo, nbits, m, t[7]);
             if (i - ov > slack_r || j - ov > slack_s) {
                 if (kFull) *ov_out = 0;
                 return false;
@@ -938,7 +922,9 @@ __device__ __forceinline__ bool warp_defer(const KParams& p, bool want, uint32_t
 //     lanes whose pairs need one block and lanes whose pairs need several).
 // pos8[q] / n[q]: the candidate's CSR position and size (pos8 = kNone: no candidate);
 // kPacked: the staged heads are packed records (tokens in the low 24 bits).
-template <int kOut, bool kStats, bool kMap, bool kPacked, bool kReg, uint32_t kOff = kNoOff>
+// mid(): called between the phases, once the heads in hr are consumed (run_kernel issues the
+// next run's head gathers there, so their latency hides behind the queue drain).
+template <int kOut, bool kStats, bool kMap, bool kPacked, bool kReg, typename Mid>
 __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
                                            const uint32_t* pos8, const uint32_t* nn,
                                            const uint8_t* __restrict__ map,
@@ -946,18 +932,21 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
                                            const uint32_t* __restrict__ rank, uint4* hd,
                                            const uint32_t (&hr)[kRunItems][8],
                                            unsigned& count, unsigned& prunes,
-                                           unsigned& verified) {
+                                           unsigned& verified, Mid&& mid) {
     constexpr bool kFull = kOut == kOutResults;
     constexpr uint32_t T = kRunThreads, I = kRunItems;
     const uint32_t lane = threadIdx.x & 31, tid = threadIdx.x;
     const uint32_t m = R.rsize, lo = R.lo, nbits = R.nw * 32u;
     uint32_t nq = 0;
+    uint32_t rqv[I];  // every item's required overlap first: the table loads overlap
+#pragma unroll
+    for (uint32_t q = 0; q < I; ++q) rqv[q] = pos8[q] != kNone ? run_required(p, m, nn[q]) : 0u;
 #pragma unroll
     for (uint32_t q = 0; q < I; ++q) {
         const uint32_t slot = R.begin + q * T + tid;
         const bool valid = pos8[q] != kNone;
         const uint32_t n = nn[q];
-        const uint32_t rq = valid ? run_required(p, m, n) : 0u;
+        const uint32_t rq = rqv[q];
         const bool inrange = valid && rq >= 1 && rq <= min(m, n);
         const bool deferred = warp_defer(p, inrange && n > kLongPair, R.slice);
         bool met = valid && rq == 0, decided = true;
@@ -976,14 +965,14 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
 #pragma unroll
                 for (int u = 0; u < 8; ++u) t8[u] &= kHeadTokenMask;
             }
-            ov = count8<kMap, kOff>(map, bits, lo, nbits, t8);
+            ov = count8<kMap>(map, bits, lo, nbits, t8);
             if (n <= 8) met = ov >= rq;
             else if (!kFull && ov >= rq) met = true;
             else if (ov < rq && 8u - ov > n - rq) met = false;
             // the probe-side bound at the same point (verify.hpp:58): i probe tokens <= the
             // block's last token, ov of them matched
             else if (SSJB_RUN_RSIDE1 && ov < rq &&
-                     probe_rank<kMap, kOff>(bits, rank, lo, nbits, m, t8[7]) - ov > m - rq) met = false;
+                     probe_rank<kMap>(bits, rank, lo, nbits, m, t8[7]) - ov > m - rq) met = false;
             else decided = false;
         } else if (kFull && met) {
             ov = full_overlap_seq(p.tokens + (size_t)R.rpos8 * 8, m,
@@ -1005,6 +994,7 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
         }
         if (kFull) warp_append(p, valid && decided && !deferred && met, slot, ov);
     }
+    mid();
     __syncwarp();
     for (uint32_t base = 0; base < nq; base += 32) {
         const uint32_t e = base + lane;
@@ -1014,7 +1004,7 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
             const uint4 qe = hd[e];
             slot = qe.x;
             const uint32_t n = qe.z, rq = qe.w & 0xFFFFu;
-            met = bm_continue<kFull, kMap, kOff>(map, bits, rank, lo, nbits, m,
+            met = bm_continue<kFull, kMap>(map, bits, rank, lo, nbits, m,
                                            p.tokens + (size_t)qe.y * 8, n, rq, qe.w >> 16, &ov,
                                            p.tokens_tex, qe.y);
             if (kOut == kOutFlags) p.flags[slot] = met ? 1 : 0;
@@ -1030,11 +1020,12 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
 }
 
 // A run whose probe has no bitmap: thread-sequential early-exit merge per candidate.
-template <int kOut, bool kStats, bool kPacked, bool kReg>
+template <int kOut, bool kStats, bool kPacked, bool kReg, typename Mid>
 __device__ __forceinline__ void run_merge(const KParams& p, const RunState& R,
                                           const uint32_t* pos8, const uint32_t* nn,
                                           const uint4* hd, unsigned& count, unsigned& prunes,
-                                          unsigned& verified) {
+                                          unsigned& verified, Mid&& mid) {
+    if (kReg) mid();  // the register heads are not read here (the merge reads the CSR)
     constexpr bool kFull = kOut == kOutResults;
     constexpr uint32_t T = kRunThreads, I = kRunItems;
     const uint32_t lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -1070,6 +1061,7 @@ __device__ __forceinline__ void run_merge(const KParams& p, const RunState& R,
         }
         if (kFull) warp_append(p, valid && !deferred && met, slot, ov);
     }
+    if (!kReg) mid();
     __syncwarp();
 }
 
@@ -1147,6 +1139,21 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
             }
         };
 
+        // kPipe: the heads of run k+1 are gathered (texture path) in the middle of run k, right
+        // after run k's first blocks consumed hr, with the C ids of run k+2 loaded behind them
+        constexpr bool kPipe = kReg && kPacked && SSJB_RUN_TEX && SSJB_RUN_PIPE;
+        uint32_t hr[I][8];  // kReg: first 8 tokens (packed records) of run k's candidates
+        auto tex_heads = [&](const uint32_t* cc) -> uint32_t {
+            uint32_t vm = 0;
+#pragma unroll
+            for (uint32_t q = 0; q < I; ++q) {
+                const bool ok = cc[q] < p.n_sets;
+                if (ok) tex_tokens8(p.heads_tex, cc[q], hr[q]);
+                else if (cc[q] != kNone) flag_error(p.acc, kErrOutOfRange);
+                vm |= (uint32_t)ok << q;
+            }
+            return vm;
+        };
         uint32_t run0 = first, run1 = next_run(first), run2 = next_run(run1);
         RunState R0, R1;
         load_run(p, run0, nr, R0);
@@ -1156,21 +1163,31 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
         uint2 d0[I];  // !kPacked: set descriptors of run k (then k+1)
         load_c(R0, c);
         uint32_t vm0 = 0;  // kPacked: items of run k with a candidate
-        if (kPacked) {
+        if (kPipe) {
+            vm0 = tex_heads(c);
+        } else if (kPacked) {
             if (NB == 2) vm0 = issue_heads(c, 0);
         } else {
             load_d(c, d0);
         }
-        if (!kPacked || NB == 2) load_c(R1, c);
-        uint32_t hr[I][8];  // kReg: first 8 tokens (packed records) of run k's candidates
-        uint32_t map_slice = kNone, mb = 1;  // slice whose map is in buffer mb
+        if (!kPacked || NB == 2 || kPipe) load_c(R1, c);
+        uint32_t map_slice = kNone, mb = kRunMapBufs - 1;  // slice whose map is in buffer mb
+        if (kRunMapBufs == 3) {
+            // every byte map starts zeroed; afterwards a buffer is re-zeroed two slice changes
+            // before its next use (see below)
+            for (uint32_t u = tid; u < 3 * kRunMapBuf / 16; u += T)
+                reinterpret_cast<uint4*>(s_map)[u] = make_uint4(0, 0, 0, 0);
+            __syncthreads();
+        }
 
         for (uint32_t k = 0; run0 < nr; ++k) {
             const uint32_t hb = NB == 2 ? (k & 1u) : 0u;
             uint4* const hd = hbase + hb * HB;
             uint2 d1[I];
             uint32_t vm1 = 0;
-            if (kReg) {
+            if (kPipe) {
+                // run k's heads were gathered during run k-1 (prologue for run 0)
+            } else if (kReg) {
                 // run k's heads straight into registers (one 256-bit load per candidate)
 #pragma unroll
                 for (uint32_t q = 0; q < I; ++q) {
@@ -1215,19 +1232,33 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
             load_slice(p, R1);
             RunState R2;
             load_run(p, run2, nr, R2);
-            load_c((!kPacked || NB == 2) ? R2 : R1, c);
+            if (!kPipe) load_c((!kPacked || NB == 2) ? R2 : R1, c);
+            // kPipe: run k+1's heads (from c), then run k+2's C ids into c
+            auto mid = [&]() {
+                if (kPipe) {
+                    vm1 = tex_heads(c);
+                    load_c(R2, c);
+                }
+            };
 
             // the probe's byte map (CTA-uniform condition)
             const bool use_map = map_ok(R0);
             if (use_map && R0.slice != map_slice) {
-                mb ^= 1u;
+                // Three buffers, one barrier per slice change c: the map goes into buffer
+                // c % 3 (zeroed after barrier c - 2), the barrier publishes it, then buffer
+                // (c + 2) % 3 -- slice c - 1's, whose readers all passed barrier c -- is
+                // zeroed for change c + 2 (every thread passes barrier c + 1 in between).
+                // Two buffers: zero-fill, barrier, scatter, barrier.
+                mb = mb + 1 == kRunMapBufs ? 0u : mb + 1;
                 map_slice = R0.slice;
                 uint8_t* mp = s_map + mb * kRunMapBuf;
                 const uint32_t range = R0.nw * 32u;
                 const uint32_t* r = p.tokens + (size_t)R0.rpos8 * 8;
-                for (uint32_t u = tid; u * 16 <= range; u += T)
-                    reinterpret_cast<uint4*>(mp)[u] = make_uint4(0, 0, 0, 0);
-                __syncthreads();
+                if (kRunMapBufs == 2) {
+                    for (uint32_t u = tid; u * 16 <= range; u += T)
+                        reinterpret_cast<uint4*>(mp)[u] = make_uint4(0, 0, 0, 0);
+                    __syncthreads();
+                }
 #if SSJB_RUN_MAP_BITS
                 for (uint32_t i = tid; i < R0.rsize; i += T) {
                     const uint32_t d = __ldg(r + i) - R0.lo;
@@ -1243,6 +1274,11 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
                     sb[kRunMapWords + w] = __ldg(p.bm_rank + R0.bofs + w);
                 }
                 __syncthreads();
+                if (kRunMapBufs == 3) {
+                    uint8_t* const old = s_map + (mb == 0 ? 2u : mb - 1) * kRunMapBuf;
+                    for (uint32_t u = tid; u < kRunMapBytes / 16; u += T)
+                        reinterpret_cast<uint4*>(old)[u] = make_uint4(0, 0, 0, 0);
+                }
             }
 
             uint32_t pos8[I], nn[I];
@@ -1281,24 +1317,17 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
             if (use_map) {
                 const uint8_t* mp = s_map + mb * kRunMapBuf;
                 const uint32_t* sb = reinterpret_cast<const uint32_t*>(mp + kRunMapBytes);
-                constexpr uint32_t kMap0 = T * I * 8 * NBS * 4;  // byte offset of map buffer 0
-                if (SSJB_RUN_MAPOFF && mb)
-                    run_bitmap<kOut, kStats, true, kPacked, kReg, kMap0 + kRunMapBuf>(
-                        p, R0, pos8, nn, mp, sb, sb + kRunMapWords, hd, hr, count, prunes, verified);
-                else if (SSJB_RUN_MAPOFF)
-                    run_bitmap<kOut, kStats, true, kPacked, kReg, kMap0>(
-                        p, R0, pos8, nn, mp, sb, sb + kRunMapWords, hd, hr, count, prunes, verified);
-                else
-                    run_bitmap<kOut, kStats, true, kPacked, kReg>(p, R0, pos8, nn, mp, sb,
-                                                                  sb + kRunMapWords, hd, hr, count,
-                                                                  prunes, verified);
+                run_bitmap<kOut, kStats, true, kPacked, kReg>(p, R0, pos8, nn, mp, sb,
+                                                              sb + kRunMapWords, hd, hr, count,
+                                                              prunes, verified, mid);
             } else if (R0.bofs != kNone) {
                 run_bitmap<kOut, kStats, false, kPacked, kReg>(p, R0, pos8, nn, nullptr,
                                                                p.bm_bits + R0.bofs,
                                                                p.bm_rank + R0.bofs, hd, hr,
-                                                               count, prunes, verified);
+                                                               count, prunes, verified, mid);
             } else {
-                run_merge<kOut, kStats, kPacked, kReg>(p, R0, pos8, nn, hd, count, prunes, verified);
+                run_merge<kOut, kStats, kPacked, kReg>(p, R0, pos8, nn, hd, count, prunes,
+                                                       verified, mid);
             }
 
             R0 = R1;

@@ -67,13 +67,18 @@ constexpr uint32_t kRunMapBuf = kRunMapBytes + 2 * ((kRunMapWords + 3) & ~3u) * 
 constexpr int kRunMinBlocks = SSJB_RUN_MIN_BLOCKS;
 constexpr uint32_t kRunBlock = SSJB_RUN_BLOCK;          // consecutive runs per CTA turn
 // shared memory: two candidate-head buffers per warp [buf][item][lane] 32 bytes (the
-// current one doubles as the warp's continuation queue), two probe byte maps
+// current one doubles as the warp's continuation queue), two or three probe byte maps
 #ifndef SSJB_RUN_HEAD_BUFS
 #define SSJB_RUN_HEAD_BUFS 0
 #endif
 constexpr uint32_t kRunHeadBufs = SSJB_RUN_HEAD_BUFS;  // 2: heads of run k+1 fetched during run k
+#ifndef SSJB_RUN_MAP_BUFS
+#define SSJB_RUN_MAP_BUFS 2  // 3: one barrier per slice change, but spills at 64 registers (3.0 vs 2.49 ms)
+#endif
+constexpr uint32_t kRunMapBufs = SSJB_RUN_MAP_BUFS;  // probe byte-map buffers (2 or 3)
 constexpr size_t kRunSmemBytes =
-    (size_t)kRunThreads * kRunItems * 32 * (kRunHeadBufs ? kRunHeadBufs : 1) + 2 * kRunMapBuf;
+    (size_t)kRunThreads * kRunItems * 32 * (kRunHeadBufs ? kRunHeadBufs : 1) +
+    kRunMapBufs * kRunMapBuf;
 
 struct RunDesc {
     uint32_t slice;  // slice index

@@ -250,8 +250,20 @@ def test_trailing_uncovered_slots(ssj, gpu, oracle):
     chunk = random_chunk(ssj, rng, coll, 10_000, 300, trailing=5000)
     ref = oracle.verify_chunk(coll.tokens, coll.offsets, chunk.C, chunk.C_O,
                               oracle.pred(J, 1, 2))
+    # the same slots all covered first, so the engine's reused flag buffer holds verdicts
+    # of the trailing slots (compute-sanitizer initcheck found strategies B / C copying
+    # never-written flag bytes back)
+    CO_full = chunk.C_O.copy()
+    CO_full[-1] = chunk.C.size
+    full = ssj.CandidateChunk(chunk.C, CO_full)
+    ref_full = oracle.verify_chunk(coll.tokens, coll.offsets, full.C, full.C_O,
+                                   oracle.pred(J, 1, 2))
+    assert ref_full["flags"][10_000:].any()
     for kind, group in (("A", 1), ("B", 32), ("C", 8)):
         with engine(ssj, coll, ssj.jaccard(1, 2), kind, group) as eng:
+            out = eng.verify_chunk(full)
+            bad = np.flatnonzero(out.flags != ref_full["flags"])
+            assert bad.size == 0 and out.count == ref_full["count"], (kind, bad[:10], bad.size)
             out = eng.verify_chunk(chunk)
             assert np.array_equal(out.flags, ref["flags"]) and out.count == ref["count"]
             assert not out.flags[10_000:].any()
@@ -371,6 +383,37 @@ def test_device_api_and_algorithmic_bytes(ssj, gpu, oracle):
                                                chunk.C_O.size, dB.data_ptr(), stream)
             torch.cuda.synchronize()
             assert int(dB.item()) == ref_bytes
+
+
+def test_every_flag_written(ssj, gpu, oracle):
+    """Every slot's flag is stored by the kernels, covered or not: the device flag buffer is
+    filled with 0xAB first, so a flag some kernel leaves unwritten cannot pass as a stale 0
+    (long slices cut into runs, pairs longer than kLongPair, zero-width and trailing slices)."""
+    import torch
+    rng = np.random.default_rng(47)
+    coll = random_collection(ssj, rng, 900, 300, 1200)
+    dev = torch.device("cuda:0")
+    stream = torch.cuda.current_stream().cuda_stream
+    shapes = [dict(n_cands=10_000, n_slices=300, trailing=5000),
+              dict(n_cands=60_000, n_slices=40, zero_width=0.2),
+              dict(n_cands=3_000, n_slices=2000, trailing=700)]
+    for kw in shapes:
+        chunk = random_chunk(ssj, rng, coll, **kw)
+        ref = oracle.verify_chunk(coll.tokens, coll.offsets, chunk.C, chunk.C_O,
+                                  oracle.pred(J, 1, 2))
+        dC = torch.from_numpy(chunk.C.view(np.int32)).to(dev)
+        dCO = torch.from_numpy(chunk.C_O.view(np.int32)).to(dev)
+        dR = torch.zeros(8, dtype=torch.int64, device=dev)
+        for kind, group in (("A", 1), ("Auto", 32), ("B", 64), ("C", 8)):
+            dF = torch.full((chunk.C.size,), 0xAB, dtype=torch.uint8, device=dev)
+            with engine(ssj, coll, ssj.jaccard(1, 2), kind, group) as eng:
+                eng.verify_chunk_device(dC.data_ptr(), chunk.C.size, dCO.data_ptr(),
+                                        chunk.C_O.size, dF.data_ptr(), dR.data_ptr(), stream)
+                torch.cuda.synchronize()
+            got = dF.cpu().numpy()
+            bad = np.flatnonzero(got != ref["flags"])
+            assert bad.size == 0, (kw, kind, bad[:8], got[bad[:8]])
+            assert int(dR[0].item()) == ref["count"]
 
 
 def test_c4_golden_on_gpu(ssj, gpu):
