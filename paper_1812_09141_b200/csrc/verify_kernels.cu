@@ -45,8 +45,11 @@
 #ifndef SSJB_RUN_REQTAB
 #define SSJB_RUN_REQTAB 1  // run_kernel reads the required overlap from the engine's table
 #endif
-#ifndef SSJB_RUN_PIPE
-#define SSJB_RUN_PIPE 0  // 1: run_kernel gathers run k+1's heads in the middle of run k (2.58 vs 2.49 ms on cfg2)
+#ifndef SSJB_RUN_OWN_BITMAP
+#define SSJB_RUN_OWN_BITMAP 1  // run slices' probe bitmaps built by run_kernel
+#endif
+#ifndef SSJB_RUN_AHEAD
+#define SSJB_RUN_AHEAD 1  // run_kernel: a warp free at a slice change builds the next map too
 #endif
 #ifndef SSJB_TILE_DYN
 #define SSJB_TILE_DYN 1  // warp_tile_kernel takes short tiles from a per-launch counter
@@ -344,9 +347,13 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const KParams p) {
                 // range land there), rounded to 16 bytes for cp.async; no bitmap when the
                 // probe holds token 0xFFFFFFFF (the padding value)
                 if (nw <= kMaxBitmapWords && hi != 0xFFFFFFFFu) {
-                    na = bitmap_alloc_words(nw);
                     d1.x = lo;
                     d1.y = nw;
+                    // run_kernel builds the bitmap of a run slice whose range fits its byte
+                    // map itself (in shared memory): no global words for those
+                    const bool own = SSJB_RUN_OWN_BITMAP && end - begin >= kRunMinSlice &&
+                                     nw * 32u <= kRunMapRange;
+                    if (!own) na = bitmap_alloc_words(nw);
                 }
             }
         }
@@ -354,7 +361,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const KParams p) {
             warp_alloc(0, na, [&](uint64_t) { return p.acc + kAccBitmapWords; });
         const bool got = na && off + na <= p.bm_cap;
         if (got) d0.w = (uint32_t)off;
-        else d1 = make_uint4(0, 0, 0, 0);
+        else if (na) d1 = make_uint4(0, 0, 0, 0);  // wanted global words, none left: merge path
         if (p.bm_list) {
             const unsigned long long li =
                 warp_alloc(0, got ? 1u : 0u, [&](uint64_t) { return p.acc + kAccBitmapSlices; });
@@ -789,6 +796,83 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 
+// mbarrier helpers (shared::cta); try_wait has acquire, arrive release semantics (CTA scope).
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(b)),
+                 "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred P;\n"
+        "W%=: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        " @!P bra W%=;\n}\n" ::"r"((uint32_t)__cvta_generic_to_shared(b)),
+        "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred P;\n"
+        " mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, P;\n}\n"
+        : "=r"(ok) : "r"((uint32_t)__cvta_generic_to_shared(b)), "r"(parity) : "memory");
+    return ok != 0;
+}
+
+// One warp builds a probe's map in shared memory (byte map over [lo, lo + 32 nw) with entry
+// 32 nw empty, then the bitmap words and the per-word ranks for the exact bound) and
+// publishes it on `full`. Out of line: it runs once per slice change, and inlined its
+// registers would weigh on the verification loop.
+__device__ __noinline__ void build_probe_map(const KParams& p, uint8_t* mp, uint32_t rpos8,
+                                             uint32_t rsize, uint32_t lo, uint32_t nw,
+                                             uint32_t bofs, uint64_t* full) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t range = nw * 32u;
+    const uint32_t* r = p.tokens + (size_t)rpos8 * 8;
+    uint32_t* sb = reinterpret_cast<uint32_t*>(mp + kRunMapBytes);
+    for (uint32_t u = lane; u * 16 <= range; u += 32)
+        reinterpret_cast<uint4*>(mp)[u] = make_uint4(0, 0, 0, 0);
+    if (SSJB_RUN_OWN_BITMAP) {
+        for (uint32_t w = lane; w < nw; w += 32) sb[w] = 0;
+        __syncwarp();
+        for (uint32_t i = lane; i < rsize; i += 32) {
+            const uint32_t d = __ldg(r + i) - lo;
+            mp[d] = 1;
+            atomicOr(sb + (d >> 5), 1u << (d & 31));
+        }
+        __syncwarp();
+        // lane l: words [l*per, l*per + per) (per <= 8), exclusive warp scan of their counts
+        const uint32_t per = (nw + 31) / 32;
+        uint32_t tot = 0;
+        for (uint32_t q = 0, w = lane * per; q < per && w < nw; ++q, ++w) tot += __popc(sb[w]);
+        uint32_t incl = tot;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= (uint32_t)off) incl += v;
+        }
+        uint32_t x = incl - tot;
+        for (uint32_t q = 0, w = lane * per; q < per && w < nw; ++q, ++w) {
+            sb[kRunMapWords + w] = x;
+            x += __popc(sb[w]);
+        }
+    } else {  // copied from the prep pass's global bitmap
+        for (uint32_t w = lane; w < nw; w += 32) {
+            sb[w] = __ldg(p.bm_bits + bofs + w);
+            sb[kRunMapWords + w] = __ldg(p.bm_rank + bofs + w);
+        }
+        __syncwarp();
+        for (uint32_t i = lane; i < rsize; i += 32) mp[__ldg(r + i) - lo] = 1;
+    }
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(full);
+}
+
 // Per-run uniform state (every thread holds the same values).
 struct RunState {
     uint32_t begin, end;      // slots
@@ -838,11 +922,7 @@ __device__ __forceinline__ uint32_t count8(const uint8_t* __restrict__ map,
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const uint32_t d = min(t[q] - lo, R);
-#if SSJB_RUN_MAP_BITS
-        if (kMap) c += (reinterpret_cast<const uint32_t*>(map)[d >> 5] >> (d & 31)) & 1u;
-#else
         if (kMap) c += map[d];
-#endif
         else c += (__ldg(bits + (d >> 5)) >> (d & 31)) & 1u;
     }
     return c;
@@ -922,9 +1002,7 @@ __device__ __forceinline__ bool warp_defer(const KParams& p, bool want, uint32_t
 //     lanes whose pairs need one block and lanes whose pairs need several).
 // pos8[q] / n[q]: the candidate's CSR position and size (pos8 = kNone: no candidate);
 // kPacked: the staged heads are packed records (tokens in the low 24 bits).
-// mid(): called between the phases, once the heads in hr are consumed (run_kernel issues the
-// next run's head gathers there, so their latency hides behind the queue drain).
-template <int kOut, bool kStats, bool kMap, bool kPacked, bool kReg, typename Mid>
+template <int kOut, bool kStats, bool kMap, bool kPacked, bool kReg>
 __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
                                            const uint32_t* pos8, const uint32_t* nn,
                                            const uint8_t* __restrict__ map,
@@ -932,7 +1010,7 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
                                            const uint32_t* __restrict__ rank, uint4* hd,
                                            const uint32_t (&hr)[kRunItems][8],
                                            unsigned& count, unsigned& prunes,
-                                           unsigned& verified, Mid&& mid) {
+                                           unsigned& verified) {
     constexpr bool kFull = kOut == kOutResults;
     constexpr uint32_t T = kRunThreads, I = kRunItems;
     const uint32_t lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -994,7 +1072,6 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
         }
         if (kFull) warp_append(p, valid && decided && !deferred && met, slot, ov);
     }
-    mid();
     __syncwarp();
     for (uint32_t base = 0; base < nq; base += 32) {
         const uint32_t e = base + lane;
@@ -1020,12 +1097,11 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
 }
 
 // A run whose probe has no bitmap: thread-sequential early-exit merge per candidate.
-template <int kOut, bool kStats, bool kPacked, bool kReg, typename Mid>
+template <int kOut, bool kStats, bool kPacked, bool kReg>
 __device__ __forceinline__ void run_merge(const KParams& p, const RunState& R,
                                           const uint32_t* pos8, const uint32_t* nn,
                                           const uint4* hd, unsigned& count, unsigned& prunes,
-                                          unsigned& verified, Mid&& mid) {
-    if (kReg) mid();  // the register heads are not read here (the merge reads the CSR)
+                                          unsigned& verified) {
     constexpr bool kFull = kOut == kOutResults;
     constexpr uint32_t T = kRunThreads, I = kRunItems;
     const uint32_t lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -1061,7 +1137,6 @@ __device__ __forceinline__ void run_merge(const KParams& p, const RunState& R,
         }
         if (kFull) warp_append(p, valid && !deferred && met, slot, ov);
     }
-    if (!kReg) mid();
     __syncwarp();
 }
 
@@ -1071,17 +1146,17 @@ __device__ __forceinline__ void run_merge(const KParams& p, const RunState& R,
 // candidates of nearby probes share L2 -- and consecutive runs of a block usually share
 // their slice.
 //
-// Thread t owns slots begin + q*kRunThreads + t (q < kRunItems) of every run. The first
-// 32-byte sector of each of its candidates is fetched by cp.async into the warp's head
-// buffer (the thread's own slots: no barrier): kPacked (the collection has packed head
-// records) one run ahead into the other of two buffers, with the C ids prefetched one run
-// further -- one 32-byte fetch gives the first 8 tokens, |s| and the CSR position; else set
-// descriptors are prefetched one run ahead and the CSR sector is fetched at the run's start.
-// When a run starts a new slice whose probe spans <= kRunMapRange tokens, the CTA builds the
-// probe's byte map in one of two shared buffers (zero-fill, barrier, scatter of the probe's
-// tokens, barrier); a buffer is rebuilt only after the barriers of the next slice change, so
-// nobody still reads it.
-template <int kOut, bool kStats, bool kPacked>
+// Thread t owns slots begin + q*kRunThreads + t (q < kRunItems) of every run. By default
+// (kRunHeadBufs = 0, packed heads) the C ids are prefetched one run ahead and each
+// candidate's 32-byte head record -- first 8 tokens, |s|, CSR position -- is gathered
+// through the texture path straight into registers at the run's start (the variants with
+// cp.async head buffers in shared memory remain for collections without packed heads).
+// When a run starts a new slice whose probe spans <= kRunMapRange tokens, the probe's byte
+// map, bitmap words and ranks are built in one of kMB shared buffers by ONE warp -- the
+// first to get there -- and published with an mbarrier; the others wait for that
+// publication only, never for each other (no CTA barrier). That warp also builds the next
+// run's map ahead when its buffer is already free (kMB = 3 for short slices).
+template <int kOut, bool kStats, bool kPacked, uint32_t kMB>
 __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const KParams p) {
     extern __shared__ __align__(16) uint32_t rsh[];
     constexpr uint32_t T = kRunThreads, I = kRunItems;
@@ -1103,7 +1178,7 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
     const uint32_t first = blockIdx.x * kRunBlock;
     if (first < nr) {
         auto map_ok = [](const RunState& r) {
-            return r.bofs != kNone && r.nw * 32u <= kRunMapRange;
+            return (SSJB_RUN_OWN_BITMAP || r.bofs != kNone) && r.nw && r.nw * 32u <= kRunMapRange;
         };
         auto load_c = [&](const RunState& r, uint32_t* c) {
 #pragma unroll
@@ -1139,21 +1214,7 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
             }
         };
 
-        // kPipe: the heads of run k+1 are gathered (texture path) in the middle of run k, right
-        // after run k's first blocks consumed hr, with the C ids of run k+2 loaded behind them
-        constexpr bool kPipe = kReg && kPacked && SSJB_RUN_TEX && SSJB_RUN_PIPE;
         uint32_t hr[I][8];  // kReg: first 8 tokens (packed records) of run k's candidates
-        auto tex_heads = [&](const uint32_t* cc) -> uint32_t {
-            uint32_t vm = 0;
-#pragma unroll
-            for (uint32_t q = 0; q < I; ++q) {
-                const bool ok = cc[q] < p.n_sets;
-                if (ok) tex_tokens8(p.heads_tex, cc[q], hr[q]);
-                else if (cc[q] != kNone) flag_error(p.acc, kErrOutOfRange);
-                vm |= (uint32_t)ok << q;
-            }
-            return vm;
-        };
         uint32_t run0 = first, run1 = next_run(first), run2 = next_run(run1);
         RunState R0, R1;
         load_run(p, run0, nr, R0);
@@ -1163,31 +1224,37 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
         uint2 d0[I];  // !kPacked: set descriptors of run k (then k+1)
         load_c(R0, c);
         uint32_t vm0 = 0;  // kPacked: items of run k with a candidate
-        if (kPipe) {
-            vm0 = tex_heads(c);
-        } else if (kPacked) {
+        if (kPacked) {
             if (NB == 2) vm0 = issue_heads(c, 0);
         } else {
             load_d(c, d0);
         }
-        if (!kPacked || NB == 2 || kPipe) load_c(R1, c);
-        uint32_t map_slice = kNone, mb = kRunMapBufs - 1;  // slice whose map is in buffer mb
-        if (kRunMapBufs == 3) {
-            // every byte map starts zeroed; afterwards a buffer is re-zeroed two slice changes
-            // before its next use (see below)
-            for (uint32_t u = tid; u < 3 * kRunMapBuf / 16; u += T)
-                reinterpret_cast<uint4*>(s_map)[u] = make_uint4(0, 0, 0, 0);
-            __syncthreads();
+        if (!kPacked || NB == 2) load_c(R1, c);
+        uint32_t map_slice = kNone, mb = 0;  // slice whose map is in buffer mb
+        // Probe maps without CTA barriers: every warp sees the same sequence of maps (k =
+        // 0, 1, ...; map k in buffer k % NB). The first warp to reach map k claims its build
+        // (s_claim), waits until every warp has left map k - NB (empty[k % NB]: one arrival
+        // per warp), builds it alone and publishes it (full[k % NB]: one arrival). The other
+        // warps only wait for the publication -- never for each other.
+        __shared__ uint64_t s_full[kMB], s_empty[kMB];
+        __shared__ uint32_t s_claim;
+        uint32_t map_seq = 0;
+        if (tid == 0) {
+            for (uint32_t b = 0; b < kMB; ++b) {
+                mbar_init(&s_full[b], 1);
+                mbar_init(&s_empty[b], T / 32);
+            }
+            s_claim = 0;
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
+        __syncthreads();
 
         for (uint32_t k = 0; run0 < nr; ++k) {
             const uint32_t hb = NB == 2 ? (k & 1u) : 0u;
             uint4* const hd = hbase + hb * HB;
             uint2 d1[I];
             uint32_t vm1 = 0;
-            if (kPipe) {
-                // run k's heads were gathered during run k-1 (prologue for run 0)
-            } else if (kReg) {
+            if (kReg) {
                 // run k's heads straight into registers (one 256-bit load per candidate)
 #pragma unroll
                 for (uint32_t q = 0; q < I; ++q) {
@@ -1232,53 +1299,36 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
             load_slice(p, R1);
             RunState R2;
             load_run(p, run2, nr, R2);
-            if (!kPipe) load_c((!kPacked || NB == 2) ? R2 : R1, c);
-            // kPipe: run k+1's heads (from c), then run k+2's C ids into c
-            auto mid = [&]() {
-                if (kPipe) {
-                    vm1 = tex_heads(c);
-                    load_c(R2, c);
-                }
-            };
+            load_c((!kPacked || NB == 2) ? R2 : R1, c);
 
             // the probe's byte map (CTA-uniform condition)
             const bool use_map = map_ok(R0);
             if (use_map && R0.slice != map_slice) {
-                // Three buffers, one barrier per slice change c: the map goes into buffer
-                // c % 3 (zeroed after barrier c - 2), the barrier publishes it, then buffer
-                // (c + 2) % 3 -- slice c - 1's, whose readers all passed barrier c -- is
-                // zeroed for change c + 2 (every thread passes barrier c + 1 in between).
-                // Two buffers: zero-fill, barrier, scatter, barrier.
-                mb = mb + 1 == kRunMapBufs ? 0u : mb + 1;
                 map_slice = R0.slice;
-                uint8_t* mp = s_map + mb * kRunMapBuf;
-                const uint32_t range = R0.nw * 32u;
-                const uint32_t* r = p.tokens + (size_t)R0.rpos8 * 8;
-                if (kRunMapBufs == 2) {
-                    for (uint32_t u = tid; u * 16 <= range; u += T)
-                        reinterpret_cast<uint4*>(mp)[u] = make_uint4(0, 0, 0, 0);
-                    __syncthreads();
+                const uint32_t k = map_seq++;
+                mb = k % kMB;
+                __syncwarp();
+                if (k > 0 && lane == 0) mbar_arrive(&s_empty[(k - 1) % kMB]);
+                uint32_t won = 0;
+                if (lane == 0) won = atomicCAS(&s_claim, k, k + 1) == k;
+                if (__shfl_sync(0xffffffffu, won, 0)) {
+                    if (k >= kMB) mbar_wait(&s_empty[mb], ((k / kMB) - 1) & 1u);
+                    build_probe_map(p, s_map + mb * kRunMapBuf, R0.rpos8, R0.rsize, R0.lo, R0.nw,
+                                    R0.bofs, &s_full[mb]);
                 }
-#if SSJB_RUN_MAP_BITS
-                for (uint32_t i = tid; i < R0.rsize; i += T) {
-                    const uint32_t d = __ldg(r + i) - R0.lo;
-                    atomicOr(reinterpret_cast<uint32_t*>(mp) + (d >> 5), 1u << (d & 31));
+                // build ahead: the next run opens a new mapped slice (map k + 1) and its buffer
+                // is already free -- build it now instead of waiting for map k
+                if (SSJB_RUN_AHEAD && R1.slice != R0.slice && map_ok(R1)) {
+                    const uint32_t k1 = k + 1, b1 = k1 % kMB;
+                    uint32_t won1 = 0;
+                    if (lane == 0 && *(volatile uint32_t*)&s_claim == k1 &&
+                        (k1 < kMB || mbar_test(&s_empty[b1], ((k1 / kMB) - 1) & 1u)))
+                        won1 = atomicCAS(&s_claim, k1, k1 + 1) == k1;
+                    if (__shfl_sync(0xffffffffu, won1, 0))
+                        build_probe_map(p, s_map + b1 * kRunMapBuf, R1.rpos8, R1.rsize, R1.lo,
+                                        R1.nw, R1.bofs, &s_full[b1]);
                 }
-#else
-                for (uint32_t i = tid; i < R0.rsize; i += T) mp[__ldg(r + i) - R0.lo] = 1;
-#endif
-                // the probe's bitmap words and ranks (built by bitmap_kernel) for the bound
-                uint32_t* sb = reinterpret_cast<uint32_t*>(mp + kRunMapBytes);
-                for (uint32_t w = tid; w < R0.nw; w += T) {
-                    sb[w] = __ldg(p.bm_bits + R0.bofs + w);
-                    sb[kRunMapWords + w] = __ldg(p.bm_rank + R0.bofs + w);
-                }
-                __syncthreads();
-                if (kRunMapBufs == 3) {
-                    uint8_t* const old = s_map + (mb == 0 ? 2u : mb - 1) * kRunMapBuf;
-                    for (uint32_t u = tid; u < kRunMapBytes / 16; u += T)
-                        reinterpret_cast<uint4*>(old)[u] = make_uint4(0, 0, 0, 0);
-                }
+                mbar_wait(&s_full[mb], (k / kMB) & 1u);
             }
 
             uint32_t pos8[I], nn[I];
@@ -1319,15 +1369,14 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
                 const uint32_t* sb = reinterpret_cast<const uint32_t*>(mp + kRunMapBytes);
                 run_bitmap<kOut, kStats, true, kPacked, kReg>(p, R0, pos8, nn, mp, sb,
                                                               sb + kRunMapWords, hd, hr, count,
-                                                              prunes, verified, mid);
+                                                              prunes, verified);
             } else if (R0.bofs != kNone) {
                 run_bitmap<kOut, kStats, false, kPacked, kReg>(p, R0, pos8, nn, nullptr,
                                                                p.bm_bits + R0.bofs,
                                                                p.bm_rank + R0.bofs, hd, hr,
-                                                               count, prunes, verified, mid);
+                                                               count, prunes, verified);
             } else {
-                run_merge<kOut, kStats, kPacked, kReg>(p, R0, pos8, nn, hd, count, prunes,
-                                                       verified, mid);
+                run_merge<kOut, kStats, kPacked, kReg>(p, R0, pos8, nn, hd, count, prunes, verified);
             }
 
             R0 = R1;
@@ -1987,11 +2036,16 @@ cudaError_t launch_tiles_t(const KParams& p, uint32_t tile_begin, uint32_t tile_
     (void)tile_begin;
     (void)tile_end;
     const int sms = sm_count();
-    auto rk = p.heads ? run_kernel<kOut, kStats, true> : run_kernel<kOut, kStats, false>;
-    static std::atomic<uint64_t> attr[2];  // per instantiation and device
-    cudaError_t err = ensure_smem_attr(rk, (int)kRunSmemBytes, attr[p.heads ? 1 : 0]);
+    // short slices (a map per run or two): three map buffers, so the next map is built while
+    // the current one is in use
+    const bool mb3 = (double)p.nC < (double)SSJB_RUN_MB3_BELOW * (double)max(p.n_slices, 1u);
+    auto rk = p.heads ? (mb3 ? run_kernel<kOut, kStats, true, 3> : run_kernel<kOut, kStats, true, 2>)
+                      : (mb3 ? run_kernel<kOut, kStats, false, 3> : run_kernel<kOut, kStats, false, 2>);
+    const size_t smem = run_smem_bytes(mb3 ? 3 : 2);
+    static std::atomic<uint64_t> attr[4];  // per instantiation and device
+    cudaError_t err = ensure_smem_attr(rk, (int)smem, attr[(p.heads ? 1 : 0) + (mb3 ? 2 : 0)]);
     if (err != cudaSuccess) return err;
-    rk<<<sms * kRunMinBlocks, kRunThreads, kRunSmemBytes, st>>>(p);
+    rk<<<sms * kRunMinBlocks, kRunThreads, smem, st>>>(p);
     if (p.heads)
         warp_tile_kernel<kOut, kStats, true><<<sms * kTileMinBlocks, kThreadsA, 0, st>>>(p);
     else

@@ -72,13 +72,15 @@ constexpr uint32_t kRunBlock = SSJB_RUN_BLOCK;          // consecutive runs per 
 #define SSJB_RUN_HEAD_BUFS 0
 #endif
 constexpr uint32_t kRunHeadBufs = SSJB_RUN_HEAD_BUFS;  // 2: heads of run k+1 fetched during run k
-#ifndef SSJB_RUN_MAP_BUFS
-#define SSJB_RUN_MAP_BUFS 2  // 3: one barrier per slice change, but spills at 64 registers (3.0 vs 2.49 ms)
+// probe-map buffers: 2, or 3 when slices are short (maps change every run or two, and one
+// warp builds the next map while the others still verify: run_kernel's build-ahead)
+#ifndef SSJB_RUN_MB3_BELOW
+#define SSJB_RUN_MB3_BELOW 2048  // average candidates per slice below which 3 buffers are used
 #endif
-constexpr uint32_t kRunMapBufs = SSJB_RUN_MAP_BUFS;  // probe byte-map buffers (2 or 3)
-constexpr size_t kRunSmemBytes =
-    (size_t)kRunThreads * kRunItems * 32 * (kRunHeadBufs ? kRunHeadBufs : 1) +
-    kRunMapBufs * kRunMapBuf;
+constexpr size_t run_smem_bytes(uint32_t map_bufs) {
+    return (size_t)kRunThreads * kRunItems * 32 * (kRunHeadBufs ? kRunHeadBufs : 1) +
+           map_bufs * kRunMapBuf;
+}
 
 struct RunDesc {
     uint32_t slice;  // slice index
