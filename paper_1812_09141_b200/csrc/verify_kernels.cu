@@ -651,7 +651,9 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
         if (slot < slot1 && ns) {
             uint32_t e = e0 + li;
             if (!small) {
-                e = upper_bound_ends(p.C_O, e0, p.n_slices, slot);
+                // the slot's slice is among the tile's ns slices (tile_first[t + 1] bounds
+                // them): a short search whose C_O loads hit the lines my_end just read
+                e = upper_bound_ends(p.C_O, e0, min(e0 + ns, p.n_slices), slot);
                 if (e < p.n_slices) {
                     s_end = __ldg(p.C_O + 2 * (size_t)e + 1);
                     s_beg = e ? __ldg(p.C_O + 2 * (size_t)e - 1) : 0u;
