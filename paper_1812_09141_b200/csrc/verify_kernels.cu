@@ -454,17 +454,28 @@ __global__ void bitmap_kernel(const KParams p) {
         }
         __threadfence_block();
         __syncwarp();
+        // ranks, 128 words per round: lane l takes words 4l..4l+3 in one 16-byte load (the
+        // allocation is a multiple of 4 words and zero past nw), so a 1,300-word probe takes
+        // 11 round trips to L2 instead of 41
+        const uint32_t alloc = bitmap_alloc_words(nw);
         uint32_t carry = 0;
-        for (uint32_t base = 0; base < nw; base += 32) {
-            const uint32_t w = base + lane;
-            const uint32_t c = w < nw ? __popc(__ldcg(bits + w)) : 0u;
-            uint32_t incl = c;
+        for (uint32_t base = 0; base < nw; base += 128) {
+            const uint32_t w = base + 4 * lane;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (w < alloc) v = __ldcg(reinterpret_cast<const uint4*>(bits + w));
+            const uint32_t c0 = __popc(v.x), c1 = __popc(v.y), c2 = __popc(v.z), c3 = __popc(v.w);
+            const uint32_t tot = c0 + c1 + c2 + c3;
+            uint32_t incl = tot;
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= (uint32_t)off) incl += v;
+                const uint32_t u = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= (uint32_t)off) incl += u;
             }
-            if (w < nw) rank[w] = carry + incl - c;
+            const uint32_t x = carry + incl - tot;
+            if (w < nw) rank[w] = x;
+            if (w + 1 < nw) rank[w + 1] = x + c0;
+            if (w + 2 < nw) rank[w + 2] = x + c0 + c1;
+            if (w + 3 < nw) rank[w + 3] = x + c0 + c1 + c2;
             carry += __shfl_sync(0xffffffffu, incl, 31);
         }
     }
