@@ -200,6 +200,10 @@ struct ssj_engine {
     GenState* gen_g = nullptr;          // GroupJoin: bounds over groups and block buffers
     uint32_t req_tab_n = 0;
     cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+    // strategy A: warp_tile_kernel runs on s_aux beside run_kernel (forked and joined with
+    // two events), so the two passes' tails overlap
+    cudaStream_t s_aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     ChunkSlot slot[2];
     uint64_t next_ticket = 0;
     // pageable-input staging
@@ -433,15 +437,20 @@ int ensure_tile_scratch(ssjb::SliceDesc** slices, size_t* capS, uint32_t** bits,
 }
 
 // want_stats = false: the caller reports no VerifyStats (the all-GPU join), so the kernels
-// skip their per-pair stats accumulation.
+// skip their per-pair stats accumulation. fork: warp_tile_kernel beside run_kernel on the
+// engine's aux stream (device-resident chunks; the host path's pieces already overlap their
+// copies with the kernels, and measured slower with the fork: cfg2 e2e 12.6 vs 13.3 G/s)
 cudaError_t launch_strategy(const ssj_engine& e, const KParams& p, int out, uint32_t tile_begin,
-                            uint32_t tile_end, cudaStream_t st, bool want_stats = true) {
+                            uint32_t tile_end, cudaStream_t st, bool want_stats = true,
+                            bool fork = true) {
     const bool stats = want_stats && e.strategy.kind != SSJ_STRATEGY_C;
     switch (e.exec.kind) {
         case SSJ_STRATEGY_B: return ssjb::launch_block(p, out, stats, e.exec.group_size, st);
         case SSJ_STRATEGY_C: return ssjb::launch_path(p, out, e.exec.group_size, st);
         default: {
-            cudaError_t err = ssjb::launch_tiles(p, out, stats, tile_begin, tile_end, st);
+            cudaError_t err = ssjb::launch_tiles(p, out, stats, tile_begin, tile_end, st,
+                                                 SSJB_TILES_FORK && fork ? e.s_aux : nullptr, e.ev_fork,
+                                                 e.ev_join);
             if (err != cudaSuccess) return err;
             return ssjb::launch_long(p, out, stats, tile_begin, tile_end, st);
         }
@@ -585,7 +594,7 @@ int enqueue_chunk(ssj_engine& e, ChunkSlot& s, const uint32_t* C, uint64_t nC,
             p.short_n = s.ddefer_n + kCounters * pc + 2;
             p.short_cap = t1 - t0;
         }
-        SSJ_CK(launch_strategy(e, p, out, t0, t1, e.s_comp));
+        SSJ_CK(launch_strategy(e, p, out, t0, t1, e.s_comp, true, false));
         if (out == ssjb::kOutFlags && hi > lo) {
             SSJ_CK(cudaEventRecord(s.ev[ev], e.s_comp));
             SSJ_CK(cudaStreamWaitEvent(e.s_d2h, s.ev[ev], 0));
@@ -644,6 +653,9 @@ int init_engine_runtime(ssj_engine& e) {
     SSJ_CK(cudaStreamCreateWithFlags(&e.s_comp, cudaStreamNonBlocking));
     SSJ_CK(cudaStreamCreateWithFlags(&e.s_h2d, cudaStreamNonBlocking));
     SSJ_CK(cudaStreamCreateWithFlags(&e.s_d2h, cudaStreamNonBlocking));
+    SSJ_CK(cudaStreamCreateWithFlags(&e.s_aux, cudaStreamNonBlocking));
+    SSJ_CK(cudaEventCreateWithFlags(&e.ev_fork, cudaEventDisableTiming));
+    SSJ_CK(cudaEventCreateWithFlags(&e.ev_join, cudaEventDisableTiming));
     for (auto& s : e.slot) {
         for (auto& ev : s.ev) SSJ_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         SSJ_CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
@@ -1048,6 +1060,9 @@ void ssj_engine_destroy(ssj_engine* e) {
     if (e->s_comp) cudaStreamDestroy(e->s_comp);
     if (e->s_h2d) cudaStreamDestroy(e->s_h2d);
     if (e->s_d2h) cudaStreamDestroy(e->s_d2h);
+    if (e->s_aux) cudaStreamDestroy(e->s_aux);
+    if (e->ev_fork) cudaEventDestroy(e->ev_fork);
+    if (e->ev_join) cudaEventDestroy(e->ev_join);
     delete e;
 }
 

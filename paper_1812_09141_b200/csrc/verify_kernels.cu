@@ -2045,7 +2045,7 @@ cudaError_t ensure_smem_attr(K kernel, int bytes, std::atomic<uint64_t>& done) {
 
 template <int kOut, bool kStats>
 cudaError_t launch_tiles_t(const KParams& p, uint32_t tile_begin, uint32_t tile_end,
-                           cudaStream_t st) {
+                           cudaStream_t st, cudaStream_t aux, cudaEvent_t fork, cudaEvent_t join) {
     (void)tile_begin;
     (void)tile_end;
     const int sms = sm_count();
@@ -2058,24 +2058,35 @@ cudaError_t launch_tiles_t(const KParams& p, uint32_t tile_begin, uint32_t tile_
     static std::atomic<uint64_t> attr[4];  // per instantiation and device
     cudaError_t err = ensure_smem_attr(rk, (int)smem, attr[(p.heads ? 1 : 0) + (mb3 ? 2 : 0)]);
     if (err != cudaSuccess) return err;
-    rk<<<sms * kRunMinBlocks, kRunThreads, smem, st>>>(p);
+    cudaStream_t ts = st;
+    if (aux && fork && join) {
+        if ((err = cudaEventRecord(fork, st)) != cudaSuccess) return err;
+        if ((err = cudaStreamWaitEvent(aux, fork, 0)) != cudaSuccess) return err;
+        ts = aux;
+    }
     if (p.heads)
-        warp_tile_kernel<kOut, kStats, true><<<sms * kTileMinBlocks, kThreadsA, 0, st>>>(p);
+        warp_tile_kernel<kOut, kStats, true><<<sms * kTileMinBlocks, kThreadsA, 0, ts>>>(p);
     else
-        warp_tile_kernel<kOut, kStats, false><<<sms * kTileMinBlocks, kThreadsA, 0, st>>>(p);
+        warp_tile_kernel<kOut, kStats, false><<<sms * kTileMinBlocks, kThreadsA, 0, ts>>>(p);
+    rk<<<sms * kRunMinBlocks, kRunThreads, smem, st>>>(p);
+    if (ts != st) {
+        if ((err = cudaEventRecord(join, ts)) != cudaSuccess) return err;
+        if ((err = cudaStreamWaitEvent(st, join, 0)) != cudaSuccess) return err;
+    }
     return cudaGetLastError();
 }
 
 cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_begin,
-                         uint32_t tile_end, cudaStream_t st) {
+                         uint32_t tile_end, cudaStream_t st, cudaStream_t aux, cudaEvent_t fork,
+                         cudaEvent_t join) {
     if (tile_end <= tile_begin) return cudaSuccess;
     switch (out * 2 + (stats ? 1 : 0)) {
-        case 0: return launch_tiles_t<kOutCount, false>(p, tile_begin, tile_end, st);
-        case 1: return launch_tiles_t<kOutCount, true>(p, tile_begin, tile_end, st);
-        case 2: return launch_tiles_t<kOutFlags, false>(p, tile_begin, tile_end, st);
-        case 3: return launch_tiles_t<kOutFlags, true>(p, tile_begin, tile_end, st);
-        case 4: return launch_tiles_t<kOutResults, false>(p, tile_begin, tile_end, st);
-        default: return launch_tiles_t<kOutResults, true>(p, tile_begin, tile_end, st);
+        case 0: return launch_tiles_t<kOutCount, false>(p, tile_begin, tile_end, st, aux, fork, join);
+        case 1: return launch_tiles_t<kOutCount, true>(p, tile_begin, tile_end, st, aux, fork, join);
+        case 2: return launch_tiles_t<kOutFlags, false>(p, tile_begin, tile_end, st, aux, fork, join);
+        case 3: return launch_tiles_t<kOutFlags, true>(p, tile_begin, tile_end, st, aux, fork, join);
+        case 4: return launch_tiles_t<kOutResults, false>(p, tile_begin, tile_end, st, aux, fork, join);
+        default: return launch_tiles_t<kOutResults, true>(p, tile_begin, tile_end, st, aux, fork, join);
     }
 }
 

@@ -178,8 +178,14 @@ cudaError_t launch_build_heads(const uint32_t* tokens, const uint2* sets, uint32
 cudaError_t launch_prep(const KParams& p, cudaStream_t st, int* launches = nullptr);
 // Strategy A, first pass over the segment holding tiles [tile_begin, tile_end): run_kernel
 // (long slices), warp_tile_kernel (short slices)
+// (aux, fork, join: when aux is set, warp_tile_kernel runs on aux concurrently with
+// run_kernel on st -- they verify disjoint slots -- and st waits for it)
+#ifndef SSJB_TILES_FORK
+#define SSJB_TILES_FORK 1
+#endif
 cudaError_t launch_tiles(const KParams& p, int out, bool stats, uint32_t tile_begin,
-                         uint32_t tile_end, cudaStream_t st);
+                         uint32_t tile_end, cudaStream_t st, cudaStream_t aux = nullptr,
+                         cudaEvent_t fork = nullptr, cudaEvent_t join = nullptr);
 // Strategy A, second pass: slices the first pass marked for long pairs, slots of tiles
 // [tile_begin, tile_end) (CTA per slice, bitmap in shared memory, one warp per pair)
 cudaError_t launch_long(const KParams& p, int out, bool stats, uint32_t tile_begin,
