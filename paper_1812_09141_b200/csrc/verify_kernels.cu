@@ -1173,14 +1173,15 @@ template <int kOut, bool kStats, bool kPacked, uint32_t kMB>
 __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const KParams p) {
     extern __shared__ __align__(16) uint32_t rsh[];
     constexpr uint32_t T = kRunThreads, I = kRunItems;
-    constexpr uint32_t HB = I * 2 * 32;  // uint4 per warp head buffer
+    // uint4 per warp head buffer; with register heads only the continuation queue (I*32)
+    constexpr uint32_t HB = kRunHeadBufs == 0 ? I * 32 : I * 2 * 32;
     constexpr uint32_t NB = kRunHeadBufs;  // 0: heads in registers (LDG.256), queue-only buffer
     constexpr bool kReg = NB == 0;
     constexpr uint32_t NBS = kReg ? 1 : NB;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint4* const hbase = reinterpret_cast<uint4*>(rsh) + warp * (NBS * HB);  // [bufs][item][lane][half]
     // [2][kRunMapBuf]: probe byte map, then its bitmap words and ranks (for the exact bound)
-    uint8_t* const s_map = reinterpret_cast<uint8_t*>(rsh + T * I * 8 * NBS);
+    uint8_t* const s_map = reinterpret_cast<uint8_t*>(rsh + (T / 32) * NBS * HB * 4);
     const uint32_t nr = (uint32_t)min((uint64_t)*p.runs_n, p.runs_cap);
     // this CTA's runs: blocks blockIdx.x, blockIdx.x + G, ... of kRunBlock consecutive runs
     const uint32_t stride = (gridDim.x - 1) * kRunBlock;
@@ -1330,16 +1331,23 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
                                     R0.bofs, &s_full[mb]);
                 }
                 // build ahead: the next run opens a new mapped slice (map k + 1) and its buffer
-                // is already free -- build it now instead of waiting for map k
-                if (SSJB_RUN_AHEAD && R1.slice != R0.slice && map_ok(R1)) {
-                    const uint32_t k1 = k + 1, b1 = k1 % kMB;
+                // is already free -- build it now instead of waiting for map k (a second map
+                // ahead from run k+2, with a fourth buffer, measured slower: J 0.90 3.50 vs
+                // 2.49 ms)
+                auto try_ahead = [&](uint32_t kk, uint32_t rpos8, uint32_t rsize, uint32_t lo,
+                                     uint32_t nw, uint32_t bofs) {
+                    const uint32_t bb = kk % kMB;
                     uint32_t won1 = 0;
-                    if (lane == 0 && *(volatile uint32_t*)&s_claim == k1 &&
-                        (k1 < kMB || mbar_test(&s_empty[b1], ((k1 / kMB) - 1) & 1u)))
-                        won1 = atomicCAS(&s_claim, k1, k1 + 1) == k1;
+                    if (lane == 0 && *(volatile uint32_t*)&s_claim == kk &&
+                        (kk < kMB || mbar_test(&s_empty[bb], ((kk / kMB) - 1) & 1u)))
+                        won1 = atomicCAS(&s_claim, kk, kk + 1) == kk;
                     if (__shfl_sync(0xffffffffu, won1, 0))
-                        build_probe_map(p, s_map + b1 * kRunMapBuf, R1.rpos8, R1.rsize, R1.lo,
-                                        R1.nw, R1.bofs, &s_full[b1]);
+                        build_probe_map(p, s_map + bb * kRunMapBuf, rpos8, rsize, lo, nw, bofs,
+                                        &s_full[bb]);
+                };
+                if (SSJB_RUN_AHEAD) {
+                    const bool new1 = R1.slice != R0.slice && map_ok(R1);
+                    if (new1) try_ahead(k + 1, R1.rpos8, R1.rsize, R1.lo, R1.nw, R1.bofs);
                 }
                 mbar_wait(&s_full[mb], (k / kMB) & 1u);
             }
@@ -2051,12 +2059,13 @@ cudaError_t launch_tiles_t(const KParams& p, uint32_t tile_begin, uint32_t tile_
     const int sms = sm_count();
     // short slices (a map per run or two): three map buffers, so the next map is built while
     // the current one is in use
-    const bool mb3 = (double)p.nC < (double)SSJB_RUN_MB3_BELOW * (double)max(p.n_slices, 1u);
-    auto rk = p.heads ? (mb3 ? run_kernel<kOut, kStats, true, 3> : run_kernel<kOut, kStats, true, 2>)
-                      : (mb3 ? run_kernel<kOut, kStats, false, 3> : run_kernel<kOut, kStats, false, 2>);
-    const size_t smem = run_smem_bytes(mb3 ? 3 : 2);
+    const double avg = (double)p.nC / (double)max(p.n_slices, 1u);
+    const uint32_t mb = avg < SSJB_RUN_MB3_BELOW ? 3u : 2u;
+    auto rk = p.heads ? (mb == 3 ? run_kernel<kOut, kStats, true, 3> : run_kernel<kOut, kStats, true, 2>)
+                      : (mb == 3 ? run_kernel<kOut, kStats, false, 3> : run_kernel<kOut, kStats, false, 2>);
+    const size_t smem = run_smem_bytes(mb);
     static std::atomic<uint64_t> attr[4];  // per instantiation and device
-    cudaError_t err = ensure_smem_attr(rk, (int)smem, attr[(p.heads ? 1 : 0) + (mb3 ? 2 : 0)]);
+    cudaError_t err = ensure_smem_attr(rk, (int)smem, attr[(p.heads ? 1 : 0) + 2 * (mb - 2)]);
     if (err != cudaSuccess) return err;
     cudaStream_t ts = st;
     if (aux && fork && join) {

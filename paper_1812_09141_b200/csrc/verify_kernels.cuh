@@ -78,7 +78,10 @@ constexpr uint32_t kRunHeadBufs = SSJB_RUN_HEAD_BUFS;  // 2: heads of run k+1 fe
 #define SSJB_RUN_MB3_BELOW 2048  // average candidates per slice below which 3 buffers are used
 #endif
 constexpr size_t run_smem_bytes(uint32_t map_bufs) {
-    return (size_t)kRunThreads * kRunItems * 32 * (kRunHeadBufs ? kRunHeadBufs : 1) +
+    // per warp: the continuation queue (I*32 entries of 16 bytes), or with cp.async head
+    // buffers (kRunHeadBufs > 0) that many buffers of I*64 uint4
+    return (size_t)(kRunThreads / 32) * 16 *
+               (kRunHeadBufs ? (size_t)kRunHeadBufs * kRunItems * 64 : (size_t)kRunItems * 32) +
            map_bufs * kRunMapBuf;
 }
 
