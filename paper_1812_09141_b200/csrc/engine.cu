@@ -192,6 +192,7 @@ struct ssj_engine {
     bool owns_collection = true;
     uint32_t* d_req_tab = nullptr;  // Jaccard/Dice required overlap by |r|+|s|
     uint4* d_heads = nullptr;       // packed set heads (null: tokens too large to pack)
+    uint32_t long_words = 0;            // long pass: bitmap words a probe range can need (0: cap)
     unsigned long long heads_tex = 0;   // linear uint4 textures over d_heads / d_tokens for
     unsigned long long tokens_tex = 0;  // the run kernel's gathers (0: not created)
     ssjb::FilterIndex* fidx = nullptr;  // GPU candidate generation index (built on first use)
@@ -313,6 +314,7 @@ KParams base_params(const ssj_engine& e) {
     // through it); without one the kernels read descriptors and the CSR
     p.heads = e.heads_tex ? e.d_heads : nullptr;
     p.heads_tex = e.heads_tex;
+    p.long_words = e.long_words;
     p.tokens_tex = e.tokens_tex;
     return p;
 }
@@ -352,6 +354,12 @@ int build_heads(ssj_engine& e) {
     unsigned mx = 0;
     SSJ_CK(cudaMemcpy(&mx, d_max, sizeof(unsigned), cudaMemcpyDeviceToHost));
     cudaFree(d_max);
+    // the widest probe range (tokens <= mx) bounds the long pass's shared bitmap: bits and
+    // ranks of (mx >> 5) + 1 words plus the guard word, rounded to 16 bytes
+    if (mx < 0xFFFFFFE0u) {
+        const uint64_t w = (((uint64_t)(mx >> 5) + 2) + 3) & ~3ull;
+        e.long_words = (uint32_t)std::min<uint64_t>(w, ssjb::kMaxBitmapWords);
+    }
     if (mx >= ssjb::kHeadTokenLimit) {
         cudaFree(e.d_heads);
         e.d_heads = nullptr;

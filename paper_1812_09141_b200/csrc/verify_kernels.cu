@@ -1632,9 +1632,12 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
                                                                   const uint64_t seg_lo,
                                                                   const uint64_t seg_hi) {
     extern __shared__ __align__(16) uint32_t lsh[];
-    uint32_t* const bits = lsh;                          // [kMaxBitmapWords + 1]
-    uint32_t* const rank = lsh + kMaxBitmapWords + 4;    // [kMaxBitmapWords + 1]
-    uint4* const llist = reinterpret_cast<uint4*>(rank + kMaxBitmapWords + 4);  // [kLongThreads]
+    // bitmap capacity BW words: the collection's widest possible probe range (long_words, a
+    // multiple of 4), so narrow-universe collections fit more CTAs per SM
+    const uint32_t BW = p.long_words ? p.long_words : kMaxBitmapWords;
+    uint32_t* const bits = lsh;                          // [BW + 4]
+    uint32_t* const rank = lsh + BW + 4;                 // [BW + 4]
+    uint4* const llist = reinterpret_cast<uint4*>(rank + BW + 4);  // [kLongThreads]
     uint32_t* const lcount = reinterpret_cast<uint32_t*>(llist + kLongThreads);
     const uint32_t bits_s = (uint32_t)__cvta_generic_to_shared(bits);
     const uint32_t rank_s = (uint32_t)__cvta_generic_to_shared(rank);
@@ -1665,7 +1668,7 @@ __global__ void __launch_bounds__(kLongThreads) long_slice_kernel(const KParams 
         const uint32_t lo = m ? (__ldg(r) & ~31u) : 0u;
         const uint32_t hi = m ? __ldg(r + m - 1) : 0u;
         const uint32_t nw = m ? ((hi - lo) >> 5) + 1 : 0u;
-        const bool use_bm = m && nw <= kMaxBitmapWords && hi != 0xFFFFFFFFu;  // CTA-uniform
+        const bool use_bm = m && nw <= BW && hi != 0xFFFFFFFFu;  // CTA-uniform
         const uint32_t nbits = nw * 32u;
         __syncthreads();  // previous slice's readers are done with the bitmap
         if (use_bm) {
@@ -2105,7 +2108,9 @@ cudaError_t launch_long_t(const KParams& p, uint64_t seg_lo, uint64_t seg_hi, cu
     static std::atomic<uint64_t> attr;  // per device
     cudaError_t err = ensure_smem_attr(k, (int)kLongSmemBytes, attr);
     if (err != cudaSuccess) return err;
-    k<<<sm_count() * (1024 / kLongThreads) * 2, kLongThreads, kLongSmemBytes, st>>>(p, seg_lo, seg_hi);
+    const uint32_t W = p.long_words ? p.long_words : kMaxBitmapWords;
+    const size_t smem = (size_t)(2 * W + 8) * 4 + kLongThreads * 16 + 16;
+    k<<<sm_count() * (1024 / kLongThreads) * 2, kLongThreads, smem, st>>>(p, seg_lo, seg_hi);
     return cudaGetLastError();
 }
 

@@ -123,6 +123,7 @@ struct KParams {
     const uint4* heads;             // packed set heads, 2 x uint4 per set (nullable)
     unsigned long long heads_tex;   // linear uint4 texture over heads (0: none)
     unsigned long long tokens_tex;  // linear uint4 texture over tokens (0: none)
+    uint32_t long_words;            // long pass: shared bitmap words per CTA (0: kMaxBitmapWords)
     const uint32_t* req_tab;        // Jaccard/Dice: required overlap by |r|+|s| (nullable)
     uint32_t req_tab_n;
     SliceDesc* slices;              // strategy A: per-slice descriptors (nullable otherwise)
