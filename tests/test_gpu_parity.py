@@ -416,6 +416,40 @@ def test_every_flag_written(ssj, gpu, oracle):
             assert int(dR[0].item()) == ref["count"]
 
 
+def test_probe_map_protocol_stress(ssj, gpu, oracle):
+    """run_kernel's probe maps are built by one warp and published through mbarriers (no CTA
+    barrier): chunks whose runs change probe every run (3-buffer path, build-ahead) or every
+    few runs (2-buffer path), re-verified several times into a 0xAB-filled buffer -- a reader
+    that saw a half-built or recycled map would flip flags."""
+    import torch
+    rng = np.random.default_rng(2024)
+    coll = random_collection(ssj, rng, 4000, 70, 3000, zipf=True)
+    dev = torch.device("cuda:0")
+    stream = torch.cuda.current_stream().cuda_stream
+    n = coll.size()
+    for per_slice, n_slices in ((200, 2500), (3000, 120)):
+        lens = rng.integers(per_slice // 2, per_slice * 3 // 2, size=n_slices)
+        ends = np.cumsum(lens)
+        probes = rng.integers(64, n, size=n_slices)
+        C_ = np.concatenate([rng.integers(max(0, int(p) - 300), int(p) + 1, size=int(k))
+                             for p, k in zip(probes, lens)]).astype(np.uint32)
+        CO = np.stack([probes.astype(np.uint32), ends.astype(np.uint32)], 1).reshape(-1)
+        ref = oracle.verify_chunk(coll.tokens, coll.offsets, C_, CO, oracle.pred(J, 1, 2))
+        dC = torch.from_numpy(C_.view(np.int32)).to(dev)
+        dCO = torch.from_numpy(CO.view(np.int32)).to(dev)
+        dR = torch.zeros(8, dtype=torch.int64, device=dev)
+        with engine(ssj, coll, ssj.jaccard(1, 2), "A", 32) as eng:
+            for rep in range(5):
+                dF = torch.full((C_.size,), 0xAB, dtype=torch.uint8, device=dev)
+                eng.verify_chunk_device(dC.data_ptr(), C_.size, dCO.data_ptr(), CO.size,
+                                        dF.data_ptr(), dR.data_ptr(), stream)
+                torch.cuda.synchronize()
+                got = dF.cpu().numpy()
+                bad = np.flatnonzero(got != ref["flags"])
+                assert bad.size == 0, (per_slice, rep, bad[:8])
+                assert int(dR[0].item()) == ref["count"]
+
+
 def test_c4_golden_on_gpu(ssj, gpu):
     """acceptance.cpp:230-264: the all-pairs chunk of seed 777 (12.5 M candidates) verified
     on the GPU reproduces the reference's 30,092-byte pairs output exactly."""
