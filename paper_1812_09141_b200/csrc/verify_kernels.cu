@@ -36,12 +36,6 @@
 #ifndef SSJB_CONT_TEX
 #define SSJB_CONT_TEX 1  // run_kernel's continuation blocks read the CSR through the texture path
 #endif
-#ifndef SSJB_TILE_TEX
-#define SSJB_TILE_TEX 0  // 1: warp_tile_kernel gathers candidate heads through the texture path
-#endif
-#ifndef SSJB_RUN_RSIDE1
-#define SSJB_RUN_RSIDE1 0  // 1: run_kernel also applies the probe-side bound after the first block (slower: 2.82 vs 2.71 ms on cfg2)
-#endif
 #ifndef SSJB_RUN_REQTAB
 #define SSJB_RUN_REQTAB 1  // run_kernel reads the required overlap from the engine's table
 #endif
@@ -588,8 +582,7 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
 #pragma unroll
         for (int q = 0; q < kItems; ++q) {
             if (cand[q] < p.n_sets) {
-                if (SSJB_TILE_TEX && p.heads_tex) tex_tokens8(p.heads_tex, cand[q], hr[q]);
-                else ld_tokens8(reinterpret_cast<const uint32_t*>(p.heads + 2 * (size_t)cand[q]), hr[q]);
+                ld_tokens8(reinterpret_cast<const uint32_t*>(p.heads + 2 * (size_t)cand[q]), hr[q]);
             } else {
 #pragma unroll
                 for (int u = 0; u < 8; ++u) hr[q][u] = 0;
@@ -1060,10 +1053,6 @@ __device__ __forceinline__ void run_bitmap(const KParams& p, const RunState& R,
             if (n <= 8) met = ov >= rq;
             else if (!kFull && ov >= rq) met = true;
             else if (ov < rq && 8u - ov > n - rq) met = false;
-            // the probe-side bound at the same point (verify.hpp:58): i probe tokens <= the
-            // block's last token, ov of them matched
-            else if (SSJB_RUN_RSIDE1 && ov < rq &&
-                     probe_rank<kMap>(bits, rank, lo, nbits, m, t8[7]) - ov > m - rq) met = false;
             else decided = false;
         } else if (kFull && met) {
             ov = full_overlap_seq(p.tokens + (size_t)R.rpos8 * 8, m,

@@ -1,4 +1,2 @@
-timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_filter.py -x -q > gpurun_out/t1_pytest.log 2>&1; tail -2 gpurun_out/t1_pytest.log
-for W in cfg3 cfg4; do
-bash tools/tune.sh "dp_$W|" "nodp_$W|-DSSJB_LONG_DYN_PAIRS=0" -- --workload $W
-done
+timeout 1500 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/t1_pytest.log 2>&1; tail -2 gpurun_out/t1_pytest.log
+bash tools/tune.sh "cl_cfg2|" -- --workload cfg2
