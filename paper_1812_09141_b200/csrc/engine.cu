@@ -193,6 +193,8 @@ struct ssj_engine {
     uint32_t* d_req_tab = nullptr;  // Jaccard/Dice required overlap by |r|+|s|
     uint4* d_heads = nullptr;       // packed set heads (null: tokens too large to pack)
     uint32_t long_words = 0;            // long pass: bitmap words a probe range can need (0: cap)
+    uint32_t max_set_size = 0xFFFFFFFFu;  // largest |s| (unknown: all ones); no set longer
+                                          // than kLongPair -> no long pairs, no long pass
     unsigned long long heads_tex = 0;   // linear uint4 textures over d_heads / d_tokens for
     unsigned long long tokens_tex = 0;  // the run kernel's gathers (0: not created)
     ssjb::FilterIndex* fidx = nullptr;  // GPU candidate generation index (built on first use)
@@ -460,6 +462,8 @@ cudaError_t launch_strategy(const ssj_engine& e, const KParams& p, int out, uint
                                                  SSJB_TILES_FORK && fork ? e.s_aux : nullptr, e.ev_fork,
                                                  e.ev_join);
             if (err != cudaSuccess) return err;
+            // no set longer than kLongPair: no pair is deferred, nothing for the long pass
+            if (e.max_set_size <= ssjb::kLongPair) return cudaSuccess;
             return ssjb::launch_long(p, out, stats, tile_begin, tile_end, st);
         }
     }
@@ -868,6 +872,7 @@ int ssj_engine_create(ssj_engine** out, int device, const uint32_t* tokens, cons
         return cleanup(fail(SSJ_ERR_CUDA, "collection upload failed"));
     uint32_t max_size = 0;
     for (uint32_t i = 0; i < n_sets; ++i) max_size = std::max(max_size, offsets[i + 1] - offsets[i]);
+    e->max_set_size = max_size;
     if ((rc = check_cosine_range(*pred, max_size))) return cleanup(rc);
     if ((rc = build_req_table(*e, max_size))) return cleanup(rc);
     if ((rc = build_heads(*e))) return cleanup(rc);
@@ -925,6 +930,7 @@ int ssj_engine_create_from_device(ssj_engine** out, int device, const uint32_t* 
         }
         uint32_t max_size = 0;
         for (const auto& sd : sets) max_size = std::max(max_size, sd.y);
+        e->max_set_size = max_size;
         if ((rc = check_cosine_range(*pred, max_size)) || (rc = build_req_table(*e, max_size))) {
             ssj_engine_destroy(e);
             return rc;
@@ -966,6 +972,7 @@ int ssj_engine_create_multi(ssj_engine** out, const int32_t* devices, uint32_t n
     e->n_sets = n_sets;
     e->n_tokens = e0->n_tokens;
     e->n_padded = e0->n_padded;
+    e->max_set_size = e0->max_set_size;
     e->owns_collection = false;
     *out = e;
     return SSJ_OK;
@@ -1936,9 +1943,10 @@ int ssj_launches_per_chunk(const ssj_engine* e, uint64_t nC, uint64_t nCO) {
     // prep + one verification kernel (B, C); the memsets of the result block are not ours.
     // Strategy A: prep (validation, descriptors, tile index, run and short-tile lists), probe
     // bitmaps (when there are slices), run_kernel and warp_tile_kernel (when there are
-    // slots), and the long-pair pass.
+    // slots), and the long-pair pass (when some set is longer than kLongPair).
     const int per = (e && e->exec.kind == SSJ_STRATEGY_A)
-                        ? (nCO >= 2 ? 2 : 1) + (nC ? 2 : 0) + 1
+                        ? (nCO >= 2 ? 2 : 1) + (nC ? 2 : 0) +
+                              (e->max_set_size > ssjb::kLongPair ? 1 : 0)
                         : 2;
     return e && e->group ? per * (int)ssjm::size(*e->group) : per;
 }
