@@ -45,6 +45,9 @@
 #ifndef SSJB_RUN_AHEAD
 #define SSJB_RUN_AHEAD 1  // run_kernel: a warp free at a slice change builds the next map too
 #endif
+#ifndef SSJB_ORDERED_MIN_SLOTS
+#define SSJB_ORDERED_MIN_SLOTS (1u << 24)  // device path: run list in slot order from 16M candidates
+#endif
 #ifndef SSJB_TILE_DYN
 #define SSJB_TILE_DYN 1  // warp_tile_kernel takes short tiles from a per-launch counter
 #endif
@@ -306,7 +309,9 @@ __device__ __forceinline__ unsigned long long ordered_run_base(const KParams& p,
 __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const KParams p) {
     // slices in ticket order (ordered run list) or by block index
     __shared__ uint32_t s_ticket;
-    const bool ordered = p.ctr_all && p.lb_status && p.seg_slots >= p.nC;
+    // (small chunks: the run list's order buys no L2 locality, skip the look-back)
+    const bool ordered = p.ctr_all && p.lb_status && p.seg_slots >= p.nC &&
+                         p.nC >= (uint64_t)SSJB_ORDERED_MIN_SLOTS;
     if (ordered) {
         if (threadIdx.x == 0) s_ticket = (uint32_t)atomicAdd(p.lb_status + kLbTicket, 1ull);
         __syncthreads();
