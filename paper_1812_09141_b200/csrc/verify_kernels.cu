@@ -6,11 +6,16 @@
 //   A  (= Auto) thread per pair, load-balanced independently of slice lengths:
 //      prep_kernel       : thread per slice: validation, slice descriptor, tile index, the
 //                          runs of long slices (>= kRunMinSlice) and the short-tile lists
-//      bitmap_kernel     : probe bitmaps of slices with >= kSliceBitmapMinCands candidates
-//      run_kernel        : runs; candidate head records by 256-bit loads, the probe as a
-//                          byte map in shared memory, first 8 tokens per thread and a
+//      bitmap_kernel     : global probe bitmaps of the slices that read one (warp-tile
+//                          slices with >= kSliceBitmapMinCands candidates, run slices whose
+//                          probe range exceeds the byte map)
+//      run_kernel        : runs; candidate head records through the texture path, the probe
+//                          as a byte map + bitmap + ranks in shared memory (built by one
+//                          warp, published with mbarriers), first 8 tokens per thread and a
 //                          per-warp continuation queue (the headline kernel)
-//      warp_tile_kernel  : 64-slot warp tiles of short slices (shuffle slot -> slice search)
+//      warp_tile_kernel  : 64-slot warp tiles of short slices (shuffle slot -> slice search);
+//                          on device-resident chunks it runs beside run_kernel on a second
+//                          stream
 //      long_slice_kernel : pairs longer than kLongPair, CTA per slice with the probe bitmap
 //                          and rank in shared memory, 128 tokens per warp step
 //   B  block_kernel : one CTA per probe slice (paper Alt B): the probe set is staged in
