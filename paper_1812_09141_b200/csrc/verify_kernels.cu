@@ -1323,7 +1323,8 @@ __global__ void __launch_bounds__(kRunThreads, kRunMinBlocks) run_kernel(const K
                 __syncwarp();
                 if (k > 0 && lane == 0) mbar_arrive(&s_empty[(k - 1) % kMB]);
                 uint32_t won = 0;
-                if (lane == 0) won = atomicCAS(&s_claim, k, k + 1) == k;
+                if (lane == 0)  // (a map built ahead is usually claimed already: no CAS)
+                    won = *(volatile uint32_t*)&s_claim == k && atomicCAS(&s_claim, k, k + 1) == k;
                 if (__shfl_sync(0xffffffffu, won, 0)) {
                     if (k >= kMB) mbar_wait(&s_empty[mb], ((k / kMB) - 1) & 1u);
                     build_probe_map(p, s_map + mb * kRunMapBuf, R0.rpos8, R0.rsize, R0.lo, R0.nw,
