@@ -53,6 +53,9 @@
 #ifndef SSJB_ORDERED_MIN_SLOTS
 #define SSJB_ORDERED_MIN_SLOTS (1u << 24)  // device path: run list in slot order from 16M candidates
 #endif
+#ifndef SSJB_TILE_DESC_SHFL
+#define SSJB_TILE_DESC_SHFL 1
+#endif
 #ifndef SSJB_TILE_DYN
 #define SSJB_TILE_DYN 1  // warp_tile_kernel takes short tiles from a per-launch counter
 #endif
@@ -614,6 +617,11 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
     const bool small = ns <= 32;  // warp-uniform
     const uint32_t my_end = lane < ns ? __ldg(p.C_O + 2 * ((size_t)e0 + lane) + 1) : 0xFFFFFFFFu;
     const uint32_t beg0 = (e0 && e0 < p.n_slices) ? __ldg(p.C_O + 2 * (size_t)e0 - 1) : 0u;
+    // small tiles: lane l also holds slice e0 + l's descriptor (loaded beside its end), and a
+    // slot takes its slice's descriptor by shuffles -- no dependent load after the search
+    uint4 my_d0 = make_uint4(0, 0, 0, kNone);
+    if (SSJB_TILE_DESC_SHFL && small && lane < ns)
+        my_d0 = __ldg(reinterpret_cast<const uint4*>(p.slices + e0 + lane));
 
     uint4 nw0, nw1;
     if (!kPacked) {
@@ -659,6 +667,13 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
             const uint32_t pe = __shfl_sync(0xffffffffu, my_end, (li - 1) & 31);
             s_beg = li ? pe : beg0;
         }
+        uint4 d0s = make_uint4(0, 0, 0, kNone);
+        if (SSJB_TILE_DESC_SHFL && small) {
+            d0s.x = __shfl_sync(0xffffffffu, my_d0.x, li & 31);
+            d0s.y = __shfl_sync(0xffffffffu, my_d0.y, li & 31);
+            d0s.z = __shfl_sync(0xffffffffu, my_d0.z, li & 31);
+            d0s.w = __shfl_sync(0xffffffffu, my_d0.w, li & 31);
+        }
         // a tile without slices lies past the last C_O end: never verified, flag 0
         bool met = false, written = ns == 0;
         uint32_t ov = 0;
@@ -680,7 +695,9 @@ __device__ __forceinline__ void warp_tile(const KParams& p, const uint32_t tile,
                 // flag written by run_kernel
             } else if (e < p.n_slices && (!small || li < ns)) {
                 written = true;
-                const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(p.slices + e));
+                const uint4 d0 = (SSJB_TILE_DESC_SHFL && small)
+                                     ? d0s
+                                     : __ldg(reinterpret_cast<const uint4*>(p.slices + e));
                 const uint32_t m = d0.z;
                 const uint32_t* r = p.tokens + (size_t)d0.y * 8;
                 if (cand[q] >= p.n_sets) {
