@@ -1,2 +1,1 @@
-tail -2 gpurun_out/t1_pytest.log
-for i in 1 2; do bash tools/tune.sh "ds${i}_cfg3|" "nods${i}_cfg3|-DSSJB_TILE_DESC_SHFL=0" -- --workload cfg3; done
+for W in cfg3 cfg1; do bash tools/tune.sh "mb8_$W|" "mb6_$W|-DSSJB_TILE_MIN_BLOCKS=6" "mb7_$W|-DSSJB_TILE_MIN_BLOCKS=7" -- --workload $W; done
