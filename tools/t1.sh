@@ -1,1 +1,2 @@
-for W in cfg3 cfg1; do bash tools/tune.sh "mb8_$W|" "mb6_$W|-DSSJB_TILE_MIN_BLOCKS=6" "mb7_$W|-DSSJB_TILE_MIN_BLOCKS=7" -- --workload $W; done
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_filter.py -x -q > gpurun_out/t1_pytest.log 2>&1; tail -2 gpurun_out/t1_pytest.log
+for W in cfg2_095 cfg2_090 cfg3; do bash tools/tune.sh "tg_$W|" "notg_$W|-DSSJB_RUN_TAGMAP=0" -- --workload $W; done
