@@ -12,5 +12,5 @@ for T in "${TOOLS[@]}"; do
      --log-file $OUT/sanitizer_${TAG}_${T}.log \
      python -m pytest $SEL -q -x -p no:cacheprovider > $OUT/sanitizer_${TAG}_${T}.out 2>&1
   echo "$T rc=$? $(tail -n 1 $OUT/sanitizer_${TAG}_${T}.out)"
-  grep -h "ERROR SUMMARY" $OUT/sanitizer_${TAG}_${T}.log | sort | uniq -c | head -5
+  grep -h "ERROR SUMMARY\|RACECHECK SUMMARY" $OUT/sanitizer_${TAG}_${T}.log | sort | uniq -c | head -5
 done
