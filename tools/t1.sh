@@ -1,1 +1,1 @@
-for W in cfg1 cfg3 cfg4; do bash tools/tune.sh "bc8_$W|" "bc4_$W|-DSSJB_BITMAP_CTAS_PER_SM=4" "bc2_$W|-DSSJB_BITMAP_CTAS_PER_SM=2" -- --workload $W; done
+bash tools/tune.sh "mp32|" "mp64|-DSSJB_MAX_PIECES=64" "mp128|-DSSJB_MAX_PIECES=128" "mp32b|" "mp64b|-DSSJB_MAX_PIECES=64" -- --workload cfg2 --e2e-steps 5
